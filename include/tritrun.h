@@ -1,0 +1,102 @@
+/*
+ * tritrun.h -- C-ABI of libtritrun.so, the B200 (sm_100a) TriRun hot path.
+ *
+ * Drop-in boundary for the reference package `tritpack`
+ * (/root/reference/pkg/src/tritpack).  The reference plugs kernels in through
+ * backend.resolve() (backend.py:54-63), which returns a *kernel module* with the
+ * duck-typed surface of _kernels.pyx:23-227 / _kernels_py.py:46-171.  Every
+ * entry point below is either one function of that surface (same argument
+ * meaning, same bit-exact results) or a piece of the GPU path the paper's
+ * TriRun kernel adds (repacker, fp16/bf16 GEMV/GEMM, dense dequant).
+ *
+ * Conventions:
+ *   - all array arguments are DEVICE pointers owned by the caller; nothing is
+ *     allocated on the hot path and nothing synchronises the host;
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); every call is
+ *     stream-ordered and thread-safe;
+ *   - return 0 on success, -1 on a rejected argument or CUDA launch error, with
+ *     a message in tr_last_error() (per calling thread).  The reference kernels
+ *     do no validation (_kernels.pyx:2-4); its Python callers raise ValueError
+ *     (linear.py:104-108, 123-129), which the Python host layer mirrors.
+ *   - fmt uses the reference DType tags: TQ2 = 2, TQ1 = 3 (blocks.py:45-52).
+ *   - act_dtype: 1 = fp16, 2 = bf16.
+ */
+#ifndef TRITRUN_H
+#define TRITRUN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TR_API __attribute__((visibility("default")))
+#else
+#define TR_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TR_FMT_TQ2 2
+#define TR_FMT_TQ1 3
+#define TR_ACT_F16 1
+#define TR_ACT_BF16 2
+#define TR_LINEAR_PDL 1 /* flags bit 0: launch with programmatic dependent launch */
+
+TR_API const char* tr_last_error(void);
+TR_API int tr_version(void);
+
+/* ---- reference kernel-module surface (bit-exact) --------------------------- */
+
+/* _kernels.pyx:23-35 pack_base4: digits u8[4m] -> words u8[m] */
+TR_API int tr_pack_base4(const uint8_t* digits, uint8_t* words, int64_t m, void* stream);
+/* _kernels.pyx:38-52 unpack_base4: words u8[m] -> digits u8[4m] */
+TR_API int tr_unpack_base4(const uint8_t* words, uint8_t* digits, int64_t m, void* stream);
+/* _kernels.pyx:55-70 encode_base3: digits u8[5m] -> codes u8[m] */
+TR_API int tr_encode_base3(const uint8_t* digits, uint8_t* codes, int64_t m, void* stream);
+/* _kernels.pyx:73-87 decode_base3 (Algorithm 1): codes u8[m] -> digits u8[5m] */
+TR_API int tr_decode_base3(const uint8_t* codes, uint8_t* digits, int64_t m, void* stream);
+/* _kernels.pyx:90-118 quantize_blocks: f32[nb,256] -> digits u8[nb,256], absmax f32[nb] */
+TR_API int tr_quantize_blocks(const float* values, uint8_t* digits, float* scales, int64_t nb, void* stream);
+/* _kernels.pyx:121-133 dequantize_blocks: digits u8[nb,256], f32[nb] -> f32[nb,256] */
+TR_API int tr_dequantize_blocks(const uint8_t* digits, const float* scales, float* out, int64_t nb,
+                                void* stream);
+/* _kernels.pyx:171-227 gemm_tq2 / gemm_tq1, bit-exact parity mode:
+ * payload u8[rows,nb,64|52], scales f32[rows,nb], x f32[batch, nb*256] (zero-padded
+ * by the caller, linear.py:151-152), out f32[batch,rows]; columns [row0,row1) written. */
+TR_API int tr_gemm_exact(int fmt, const uint8_t* payload, const float* scales, const float* x, float* out,
+                         int64_t rows, int64_t nb, int64_t batch, int64_t row0, int64_t row1, void* stream);
+
+/* ---- offline packing / repacking ------------------------------------------------ */
+
+/* linear.py:98-120 pack_matrix (+ blocks.py:142-161 quantize_rows) on the device:
+ * W f32[rows,cols] -> payload u8[rows,nb,64|52] + binary16 scales u16[rows,nb]. */
+TR_API int tr_quantize_pack(int fmt, const float* W, int64_t rows, int64_t cols, uint8_t* payload,
+                            uint16_t* scales_f16, void* stream);
+/* bytes of the device ("T16") layout of a rows x cols matrix (-1 if unsupported) */
+TR_API int64_t tr_layout_bytes(int fmt, int64_t rows, int64_t cols);
+/* PackedMatrix (linear.py:29-95: payload + scales) -> device layout; bit-exactly invertible */
+TR_API int tr_repack(int fmt, const uint8_t* payload, const uint16_t* scales_f16, int64_t rows, int64_t cols,
+                     void* dst, void* stream);
+/* device layout -> PackedMatrix payload + scales (exact inverse of tr_repack) */
+TR_API int tr_unrepack(int fmt, const void* src, int64_t rows, int64_t cols, uint8_t* payload,
+                       uint16_t* scales_f16, void* stream);
+/* linear.py:177-198 dequantize_matrix, to a dense fp16/bf16 [rows, cols] matrix
+ * (values scale*(d-1) are exact in fp16); feeds the cuBLAS baseline. */
+TR_API int tr_dequant_dense(int fmt, const uint8_t* payload, const uint16_t* scales_f16, int64_t rows,
+                            int64_t cols, int act_dtype, void* out, void* stream);
+
+/* ---- the hot path ------------------------------------------------------------------ */
+
+/* y[batch, rows] = x[batch, cols] @ W^T  (linear.py:137-166 gemm semantics with the
+ * paper's fp16/bf16 activations, fp32 accumulation, RNE output).  w is the device
+ * layout from tr_repack; x has leading dimension ldx, y has ldy (elements).
+ * flags: TR_LINEAR_PDL | (forced K-split << 8) (0 = automatic). */
+TR_API int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
+                     int act_dtype, int64_t ldx, int64_t ldy, int flags, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TRITRUN_H */

@@ -1,0 +1,66 @@
+// C-ABI entry points of libtritrun.so (declared in include/tritrun.h) that are
+// not defined next to their kernels: error plumbing, version, and the hot-path
+// dispatcher tr_linear (decoder-layer linear dispatch: GEMV / skinny-GEMM by
+// batch).
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "common.cuh"
+
+namespace tr {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: CUDA error: %s", what, cudaGetErrorString(e));
+    return -1;
+  }
+  return 0;
+}
+
+int gemv_tq2(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
+             int cols, int ks, int pdl, cudaStream_t st);
+
+}  // namespace tr
+
+using namespace tr;
+
+extern "C" {
+
+const char* tr_last_error(void) { return g_err; }
+
+int tr_version(void) { return 1; }
+
+int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
+              int act_dtype, int64_t ldx, int64_t ldy, int flags, void* stream) {
+  TR_REQUIRE(fmt == kFmtTq2, "tr_linear: fmt %d not supported by this entry point (TQ2=2)", fmt);
+  TR_REQUIRE(act_dtype == kActF16 || act_dtype == kActBf16, "tr_linear: act_dtype must be F16(1) or BF16(2)");
+  TR_REQUIRE(rows >= 1 && cols >= 1 && batch >= 0, "tr_linear: bad shape batch=%lld rows=%lld cols=%lld",
+             (long long)batch, (long long)rows, (long long)cols);
+  TR_REQUIRE(rows < (1LL << 30) && cols < (1LL << 30), "tr_linear: shape too large");
+  TR_REQUIRE(ldx >= cols && ldy >= rows, "tr_linear: leading dimensions too small");
+  TR_REQUIRE(((uintptr_t)w & 15) == 0, "tr_linear: weight buffer must be 16-byte aligned");
+  if (batch == 0) return 0;
+  const int pdl = flags & 1;
+  const int ks = (flags >> 8) & 0xFF;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t esz = 2;
+  for (int64_t n0 = 0; n0 < batch; n0 += 32) {
+    const int nb_ = (int)(batch - n0 < 32 ? batch - n0 : 32);
+    int rc = gemv_tq2(act_dtype, w, (const uint8_t*)x + n0 * ldx * esz, (uint8_t*)y + n0 * ldy * esz, ldx, ldy, nb_,
+                      (int)rows, (int)cols, ks, pdl, st);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// Shared definitions for the B200 (sm_100a) TriRun kernels.
+//
+// Formats follow the reference package `tritpack` (blocks.py:34-86): a block is
+// 256 consecutive K-elements of one row; TQ2 = 64 payload bytes (4 digits per
+// byte, element 4t+j at bits 2j), TQ1 = 52 payload bytes (5 digits per byte,
+// base-3, MSB first); one binary16 scale per (row, block).  Digits are
+// d = trit + 1 in {0, 1, 2}.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "tritrun.h"
+
+namespace tr {
+
+constexpr int kBlock = 256;         // BLOCK_ELEMENTS (blocks.py:34)
+constexpr int kTq2Payload = 64;     // DType.TQ2.payload_bytes (blocks.py:63-70)
+constexpr int kTq1Payload = 52;     // DType.TQ1.payload_bytes
+constexpr int kFmtTq2 = 2;          // DType.TQ2 (blocks.py:49-52)
+constexpr int kFmtTq1 = 3;          // DType.TQ1
+constexpr int kActF16 = 1;
+constexpr int kActBf16 = 2;
+constexpr int kActF32 = 3;
+
+// ---- T16 device layout -----------------
+// Rows are padded to a multiple of 128 (zero trits, zero scales).  For every
+// (256-block b, 16-row tile t) there is a 1 KB "tile-block" at byte offset
+// (b * n_tiles + t) * 1024 holding 64 16-byte units; unit u = half*32 + c*8 + g
+// is chunk c (block columns 64c..64c+63) of row 16t + 8*half + g, encoded so
+// that word i, bits 16h + 8hb + 2j (+1) hold the digit of chunk column
+// 16i + 8hb + 2j + h.  Scales: per (b, t) 8 x half2 = (s[16t+g], s[16t+8+g]).
+constexpr int kRowPad = 128;
+constexpr int kTileBlockBytes = 1024;
+constexpr int kTileScaleBytes = 32;
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t rows_padded(int64_t rows) { return ceil_div(rows, kRowPad) * kRowPad; }
+
+// ---- PTX helpers --------------------------------------------------------------
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t mask, uint32_t magic) {
+  uint32_t r;
+  // (a & mask) | magic  -> immLut = (0xF0 & 0xCC) | 0xAA = 0xEA
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(r) : "r"(a), "r"(mask), "r"(magic));
+  return r;
+}
+
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t ldg_nc_u32(const void* p) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];\n" : "=r"(r) : "l"(p));
+  return r;
+}
+
+// ---- activation type traits ----------------------------------------------------
+template <typename T> struct Act;
+template <> struct Act<__half> {
+  static constexpr int kId = kActF16;
+  __device__ static __half from_float(float v) { return __float2half_rn(v); }
+};
+template <> struct Act<__nv_bfloat16> {
+  static constexpr int kId = kActBf16;
+  __device__ static __nv_bfloat16 from_float(float v) { return __float2bfloat16_rn(v); }
+};
+
+}  // namespace tr
+
+// ---- error plumbing for the C-ABI ---------------------------------------------------
+namespace tr {
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+}  // namespace tr
+
+#define TR_REQUIRE(cond, ...)            \
+  do {                                   \
+    if (!(cond)) {                       \
+      ::tr::set_error(__VA_ARGS__);      \
+      return -1;                         \
+    }                                    \
+  } while (0)

@@ -1,0 +1,141 @@
+"""GPU-resident ternary weights and the fp16/bf16 hot path (TriRun on B200).
+
+New API (no reference analogue; SURVEY.md Appendix B "Recommended GPU
+additions"): ``TernaryWeight`` holds a matrix in the device T16 layout
+(DESIGN.md), ``linear(x, w)`` computes ``x @ W^T`` for fp16/bf16 activations
+with fp32 accumulation (paper App. F semantics), ``TernaryLinear`` wraps it as
+an nn.Module.  Everything dispatches to libtritrun.so; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .blocks import BLOCK_ELEMENTS, DType
+
+_ACT = {torch.float16: _lib.ACT_F16, torch.bfloat16: _lib.ACT_BF16}
+
+
+class TernaryWeight:
+    """A rows x cols ternary matrix resident on one GPU in the T16 layout."""
+
+    def __init__(self, data: torch.Tensor, rows: int, cols: int, fmt: DType):
+        self.data = data
+        self.rows = int(rows)
+        self.cols = int(cols)
+        self.fmt = DType(fmt)
+
+    # -- construction ---------------------------------------------------------------
+    @classmethod
+    def from_device_packed(cls, payload: torch.Tensor, scales_f16: torch.Tensor, rows: int, cols: int,
+                           fmt: DType = DType.TQ2) -> "TernaryWeight":
+        """Repack device-resident reference-layout payload/scales (linear.py:29-95) into T16."""
+        fmt = DType(fmt)
+        nbytes = _lib.lib().tr_layout_bytes(int(fmt), rows, cols)
+        if nbytes < 0:
+            raise NotImplementedError(f"{fmt.name} has no device layout yet")
+        data = torch.empty(nbytes, dtype=torch.uint8, device=payload.device)
+        _lib.call("tr_repack", int(fmt), payload.data_ptr(), scales_f16.data_ptr(), rows, cols, data.data_ptr(),
+                  _lib.stream_handle())
+        return cls(data, rows, cols, fmt)
+
+    @classmethod
+    def from_packed(cls, pm) -> "TernaryWeight":
+        """From a host PackedMatrix (the offline-packed checkpoint form)."""
+        payload = torch.from_numpy(np.ascontiguousarray(pm.payload)).cuda()
+        scales = torch.from_numpy(np.ascontiguousarray(pm.scales).view(np.uint16).view(np.float16)).cuda()
+        return cls.from_device_packed(payload, scales, pm.rows, pm.cols, pm.fmt)
+
+    @classmethod
+    def from_float(cls, W: torch.Tensor, fmt: DType = DType.TQ2) -> "TernaryWeight":
+        """Quantize + pack a dense device matrix (pack_matrix semantics) straight into T16."""
+        W = W.detach().to(device="cuda", dtype=torch.float32).contiguous()
+        rows, cols = W.shape
+        nb = -(-cols // BLOCK_ELEMENTS)
+        fmt = DType(fmt)
+        payload = torch.empty((rows, nb, fmt.payload_bytes), dtype=torch.uint8, device=W.device)
+        scales = torch.empty((rows, nb), dtype=torch.float16, device=W.device)
+        _lib.call("tr_quantize_pack", int(fmt), W.data_ptr(), rows, cols, payload.data_ptr(), scales.data_ptr(),
+                  _lib.stream_handle())
+        return cls.from_device_packed(payload, scales, rows, cols, fmt)
+
+    # -- inspection ---------------------------------------------------------------------
+    @property
+    def blocks_per_row(self) -> int:
+        return -(-self.cols // BLOCK_ELEMENTS)
+
+    @property
+    def weight_bytes(self) -> int:
+        """Algorithmic weight bytes per product (reference formula, linear.py:68-71)."""
+        return self.rows * self.blocks_per_row * self.fmt.block_bytes
+
+    def unpack(self):
+        """Exact inverse of the repack: (payload u8 (rows,nb,pb), scales f16 (rows,nb)) on the device."""
+        nb = self.blocks_per_row
+        payload = torch.empty((self.rows, nb, self.fmt.payload_bytes), dtype=torch.uint8, device=self.data.device)
+        scales = torch.empty((self.rows, nb), dtype=torch.float16, device=self.data.device)
+        _lib.call("tr_unrepack", int(self.fmt), self.data.data_ptr(), self.rows, self.cols, payload.data_ptr(),
+                  scales.data_ptr(), _lib.stream_handle())
+        return payload, scales
+
+    def dequantize(self, dtype=torch.float16) -> torch.Tensor:
+        """Dense (rows, cols) fp16/bf16 copy (values scale*(d-1), exact in fp16)."""
+        payload, scales = self.unpack()
+        out = torch.empty((self.rows, self.cols), dtype=dtype, device=self.data.device)
+        _lib.call("tr_dequant_dense", int(self.fmt), payload.data_ptr(), scales.data_ptr(), self.rows, self.cols,
+                  _ACT[dtype], out.data_ptr(), _lib.stream_handle())
+        return out
+
+    def __repr__(self) -> str:
+        return f"TernaryWeight({self.rows}x{self.cols}, {self.fmt.name}, {self.data.numel()} B on {self.data.device})"
+
+
+def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, pdl: bool = False,
+           ksplit: int = 0) -> torch.Tensor:
+    """y[..., rows] = x[..., cols] @ W^T for fp16/bf16 x on the GPU (TriRun hot path).
+
+    Accumulation is fp32: per 256-block partial sums are scaled by the block's
+    binary16 scale in fp32 and accumulated in ascending block order; the output
+    is rounded once to x.dtype.  ``pdl`` launches with programmatic dependent
+    launch (for CUDA-graph-chained layers); ``ksplit`` forces the K split.
+    """
+    if x.dtype not in _ACT:
+        raise TypeError(f"activations must be float16 or bfloat16, got {x.dtype}")
+    if not x.is_cuda:
+        raise ValueError("activations must be on a CUDA device")
+    if x.shape[-1] != w.cols:
+        raise ValueError(f"activation shape {tuple(x.shape)} does not match cols={w.cols}")
+    lead = x.shape[:-1]
+    x2 = x.reshape(-1, w.cols)
+    if x2.stride(-1) != 1:
+        x2 = x2.contiguous()
+    batch = x2.shape[0]
+    if out is None:
+        out = torch.empty((*lead, w.rows), dtype=x.dtype, device=x.device)
+    y2 = out.view(-1, w.rows)
+    flags = (_lib.LINEAR_PDL if pdl else 0) | ((int(ksplit) & 0xFF) << 8)
+    _lib.call("tr_linear", int(w.fmt), w.data.data_ptr(), x2.data_ptr(), y2.data_ptr(), batch, w.rows, w.cols,
+              _ACT[x.dtype], x2.stride(0), y2.stride(0), flags, _lib.stream_handle())
+    return out
+
+
+class TernaryLinear(torch.nn.Module):
+    """nn.Linear-shaped module over a TernaryWeight (no bias, like the paper's BitLinear layers)."""
+
+    def __init__(self, weight: TernaryWeight):
+        super().__init__()
+        self.weight_t = weight
+        self.in_features = weight.cols
+        self.out_features = weight.rows
+
+    @classmethod
+    def from_linear(cls, lin: torch.nn.Linear, fmt: DType = DType.TQ2) -> "TernaryLinear":
+        return cls(TernaryWeight.from_float(lin.weight, fmt))
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        return linear(x, self.weight_t)
+
+    def extra_repr(self) -> str:
+        return f"in_features={self.in_features}, out_features={self.out_features}, fmt={self.weight_t.fmt.name}"
