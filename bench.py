@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""bench.py -- TriRun ternary GEMV/GEMM on B200 (BASELINE.json configs[1]).
+
+Workload ("llama_linear_stack"): R replicas of the three Llama-style shapes of
+configs[1] -- 4096x4096, up 11008x4096, down 4096x11008 (rows x cols = out x in)
+-- chained x(4096) -> 4096 -> 11008 -> 4096 -> next replica, random-init
+ternary weights (T in {-1,0,1}, per-channel gamma_r = fp16(0.02(1+U))), TQ2
+format, fp16 activations.  One step = one pass over the stack at batch 1 (the
+decode regime), replayed from a CUDA graph with PDL-chained launches.  The
+working set (R * 27.6 MB = 883 MB at R = 32) is far larger than the 126 MB L2,
+so every step streams its weights from HBM.
+
+value  = algorithmic bytes (weights by the reference formula + fp16 x and y) per
+         step, summed over ranks, / max-over-ranks device time  -> GB/s.
+e2e    = the same metric through the public API with pinned host buffers: H2D of
+         x, LinearStack replay, D2H of y, all inside the timed region.
+sweep  = GB/s and TFLOP/s for batch 1..128 next to PyTorch fp16 (cuBLAS) on the
+         dequantized weights of the same stack.
+cpu_baseline = the reference's own compiled kernels (oracle/_ref, Cython -> C from
+         the reference sources) on this host's cores, bounded sample.
+--impl reference: the reference CPU path alone (rank 0), same metric/config.
+Multi-GPU (--gpus N under torchrun): weak scaling, each rank streams its own
+replica stack (independent layers; no data-path collective).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ternary GEMV/GEMM HBM GB/s & TFLOPS vs batch 1–128; decode tokens/s vs fp16"
+SHAPES = [(4096, 4096), (11008, 4096), (4096, 11008)]   # rows x cols, chained
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--replicas", type=int, default=32)
+    p.add_argument("--sweep", default="1,2,4,8,16,32,64,128")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ------------------------------------------------------------------------- CPU reference
+
+class CpuReference:
+    """The reference's compiled kernels (oracle/_ref) on one replica of the stack at batch 1."""
+
+    def __init__(self, threads: int):
+        import numpy as np
+
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle
+
+        self.oracle, self.np, self.threads = oracle, np, threads
+        self.kern, self.kind = oracle.ref_kernels(), "reference"
+        if self.kern is None:
+            self.kern, self.kind = oracle.kernels, "port"
+        rng = np.random.default_rng(0)
+        self.mats = []
+        for rows, cols in SHAPES:
+            T = (rng.integers(0, 3, size=(rows, cols), dtype=np.int8) - 1).astype(np.float32)
+            gam = np.float16(0.02 * (1 + rng.uniform(0, 1, size=(rows, 1)))).astype(np.float32)
+            payload, scales = oracle.pack_matrix(gam * T, oracle.TQ2)
+            self.mats.append((payload, scales, cols))
+        self.x = np.float16(rng.uniform(-1, 1, size=(1, 4096))).astype(np.float32)
+        self.nbytes = sum(p.shape[0] * p.shape[1] * 66 + 2 * (c + p.shape[0]) for p, _, c in self.mats)
+
+    def one_pass(self):
+        h = self.x
+        for payload, scales, cols in self.mats:
+            h = self.oracle.gemm(payload, scales, cols, self.oracle.TQ2, h, threads=self.threads, kern=self.kern)
+            h = h.astype(self.np.float16).astype(self.np.float32)   # fp16 activations between layers
+        return h
+
+    def sample(self, seconds: float, min_passes: int = 3):
+        self.one_pass()
+        times = []
+        t_end = time.perf_counter() + seconds
+        while time.perf_counter() < t_end or len(times) < min_passes:
+            t0 = time.perf_counter()
+            self.one_pass()
+            times.append(time.perf_counter() - t0)
+        med = statistics.median(times)
+        return {"value": round(self.nbytes / med / 1e9, 4), "unit": "GB/s", "cores": self.threads,
+                "kind": self.kind,
+                "sample": f"{len(times)} passes of one replica (4096x4096, 11008x4096, 4096x11008 TQ2) at batch 1 "
+                          f"(median {med * 1e3:.1f} ms/pass), {self.threads} host threads, reference "
+                          f"gemm_tq2 under the linear.gemm row-sharding harness"}
+
+
+def run_reference(args, rank):
+    """--impl reference: the reference CPU implementation on this box's host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    ref = CpuReference(os.cpu_count() or 1)
+    for _ in range(args.warmup):
+        ref.one_pass()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ref.one_pass()
+    dt = time.perf_counter() - t0
+    value = round(ref.nbytes * args.steps / dt / 1e9, 4)
+    cpu = {"value": value, "unit": "GB/s", "cores": ref.threads, "kind": ref.kind,
+           "sample": f"{args.steps} timed passes of one replica of the stack at batch 1 (each step a bounded "
+                     f"sample of the llama_linear_stack workload), {ref.threads} threads"}
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (random-init ternary weights, per-channel fp16 gamma)",
+            "config": {"workload": "llama_linear_stack", "shapes_rows_x_cols": SHAPES, "batch": 1,
+                       "format": "TQ2", "replicas_per_step": 1},
+            "cpu_baseline": cpu,
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------- GPU helpers
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons while the timed region runs."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        names = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+                 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in names.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def make_stack_weights(replicas, seed):
+    import torch
+    import paper_2506_23025_b200 as tp
+
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    ws = []
+    for _ in range(replicas):
+        for rows, cols in SHAPES:
+            T = torch.randint(0, 3, (rows, cols), generator=g, device="cuda", dtype=torch.int8).float() - 1
+            gam = (0.02 * (1 + torch.rand((rows, 1), generator=g, device="cuda"))).half().float()
+            ws.append(tp.TernaryWeight.from_float(gam * T))
+    return ws
+
+
+def timed_graph(replay, steps, warmup, dist):
+    import torch
+
+    for _ in range(warmup):
+        replay()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        replay()
+    b.record()
+    b.synchronize()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t)
+    return ms
+
+
+def dense_stack(weights, batch):
+    """PyTorch fp16 (cuBLAS) baseline on the dequantized weights of the same stack, CUDA-graphed."""
+    import torch
+
+    dws = [w.dequantize(torch.float16) for w in weights]
+    x = torch.zeros((batch, dws[0].shape[1]), dtype=torch.float16, device="cuda")
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+
+    def body():
+        h = x
+        for d in dws:
+            h = torch.nn.functional.linear(h, d)
+        return h
+
+    with torch.cuda.stream(s):
+        body()
+        s.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            body()
+    torch.cuda.synchronize()
+    return g, dws
+
+
+def run_ours(args, rank, world, dist):
+    import torch
+    import paper_2506_23025_b200 as tp
+    from paper_2506_23025_b200.graph import LinearStack
+
+    hbm, tf_burst, tf_sust, peak_kind = peaks()
+    ws = make_stack_weights(args.replicas, seed=1234 + rank)
+    stack = LinearStack(ws, batch=1)
+    nbytes = stack.algorithmic_bytes()
+    dev_index = torch.cuda.current_device()
+
+    with ClockSampler(dev_index) as clk:
+        ms = timed_graph(stack.replay, args.steps, args.warmup, dist)
+        # keep the GPU busy a little longer so the clock record covers a loaded period
+        extra = timed_graph(stack.replay, max(args.steps, 200), 1, None)
+    ms_per_step = ms / args.steps
+    value = world * nbytes / (ms_per_step * 1e-3) / 1e9
+    per_launch_us = ms_per_step * 1e3 / stack.launches
+    achieved = nbytes / stack.launches / (per_launch_us * 1e-6) / 1e9
+
+    # ---- e2e through the public API with pinned host buffers
+    x_host = torch.empty((1, 4096), dtype=torch.float16).pin_memory()
+    x_host.copy_(torch.rand(1, 4096) * 2 - 1)
+    y_host = torch.empty((1, 4096), dtype=torch.float16).pin_memory()
+    e2e_ms = timed_graph(lambda: stack.run_host(x_host, y_host), args.steps, args.warmup, dist) / args.steps
+    e2e = {"value": round(world * nbytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+           "h2d_bytes_per_step": x_host.numel() * 2, "d2h_bytes_per_step": y_host.numel() * 2,
+           "ms_per_step": round(e2e_ms, 4)}
+
+    # ---- batch sweep vs cuBLAS fp16 (rank-local)
+    sweep = []
+    if args.sweep:
+        for b in [int(v) for v in args.sweep.split(",") if v]:
+            st = LinearStack(ws, batch=b)
+            t = timed_graph(st.replay, 20, 3, None) / 20
+            g, dws = dense_stack(ws, b)
+            td = timed_graph(g.replay, 10, 2, None) / 10
+            dense_bytes = sum(d.numel() * 2 + b * (d.shape[0] + d.shape[1]) * 2 for d in dws)
+            sweep.append({"batch": b, "ms": round(t, 4), "gbs": round(st.algorithmic_bytes() / t / 1e6, 1),
+                          "tflops": round(st.flops() / t / 1e9, 2), "cublas_fp16_ms": round(td, 4),
+                          "cublas_fp16_gbs": round(dense_bytes / td / 1e6, 1),
+                          "cublas_fp16_tflops": round(st.flops() / td / 1e9, 2),
+                          "speedup_vs_fp16": round(td / t, 2)})
+            del st, g, dws
+            torch.cuda.empty_cache()
+
+    line = None
+    if rank == 0:
+        cpu = CpuReference(os.cpu_count() or 1).sample(args.cpu_seconds)
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "gemv_ncu_summary.json")
+        if os.path.exists(prof):
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+            "data": "synthetic (random-init ternary weights, per-channel fp16 gamma; uniform(-1,1) fp16 x)",
+            "config": {"workload": "llama_linear_stack", "shapes_rows_x_cols": SHAPES, "replicas": args.replicas,
+                       "batch": 1, "format": "TQ2", "parallelism": f"replicas x{world}",
+                       "l2": f"working set {nbytes / 2**20:.0f} MB per rank > 126 MB L2 (no flush needed)",
+                       "launches_per_step": stack.launches, "graph": "CUDA graph, PDL-chained"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                         "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "k_gemv_tq2", "avg_launch_us": round(per_launch_us, 3)},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": stack.launches * args.steps,
+            "clocks": clk.summary(),
+            "sweep": sweep,
+        }
+        print(json.dumps(line), flush=True)
+    return line
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    import torch
+
+    if world > 1:
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        tdist.init_process_group("nccl")
+        dist = tdist
+    else:
+        torch.cuda.set_device(0)
+    run_ours(args, rank, world, dist)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -88,12 +88,17 @@ TR_API int tr_dequant_dense(int fmt, const uint8_t* payload, const uint16_t* sca
 
 /* ---- the hot path ------------------------------------------------------------------ */
 
+/* Bytes of caller-owned device workspace tr_linear needs for this shape (0 on bad
+ * arguments).  The first 256 KiB are per-tile arrival counters: ZERO them once
+ * after allocating; kernels leave them zeroed.  One workspace per stream. */
+TR_API size_t tr_linear_workspace_size(int fmt, int64_t batch, int64_t rows, int64_t cols);
 /* y[batch, rows] = x[batch, cols] @ W^T  (linear.py:137-166 gemm semantics with the
  * paper's fp16/bf16 activations, fp32 accumulation, RNE output).  w is the device
  * layout from tr_repack; x has leading dimension ldx, y has ldy (elements).
  * flags: TR_LINEAR_PDL | (forced K-split << 8) (0 = automatic). */
 TR_API int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
-                     int act_dtype, int64_t ldx, int64_t ldy, int flags, void* stream);
+                     int act_dtype, int64_t ldx, int64_t ldy, int flags, void* workspace, size_t ws_bytes,
+                     void* stream);
 
 #ifdef __cplusplus
 }

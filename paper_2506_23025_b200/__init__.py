@@ -25,7 +25,7 @@ from .blocks import (
     ternarize,
 )
 from .device import TernaryLinear, TernaryWeight, linear
-from .linear import PackedMatrix, dequantize_matrix, gemm, gemv, gemv_reference, pack_matrix
+from .packed_linear import PackedMatrix, dequantize_matrix, gemm, gemv, gemv_reference, pack_matrix
 from .perf import BenchRow, bench, critical_batch
 
 __version__ = "0.1.0"

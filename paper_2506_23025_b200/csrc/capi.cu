@@ -28,7 +28,8 @@ int check_launch(const char* what) {
 }
 
 int gemv_tq2(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
-             int cols, int ks, int pdl, cudaStream_t st);
+             int cols, int ks, void* workspace, size_t ws_bytes, int pdl, int dbg, cudaStream_t st);
+size_t gemv_workspace_bytes(int batch, int rows, int cols);
 
 }  // namespace tr
 
@@ -40,8 +41,14 @@ const char* tr_last_error(void) { return g_err; }
 
 int tr_version(void) { return 1; }
 
+size_t tr_linear_workspace_size(int fmt, int64_t batch, int64_t rows, int64_t cols) {
+  if (fmt != kFmtTq2 || rows < 1 || cols < 1 || batch < 0) return 0;
+  return gemv_workspace_bytes((int)(batch < 32 ? batch : 32), (int)rows, (int)cols);
+}
+
 int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
-              int act_dtype, int64_t ldx, int64_t ldy, int flags, void* stream) {
+              int act_dtype, int64_t ldx, int64_t ldy, int flags, void* workspace, size_t ws_bytes,
+              void* stream) {
   TR_REQUIRE(fmt == kFmtTq2, "tr_linear: fmt %d not supported by this entry point (TQ2=2)", fmt);
   TR_REQUIRE(act_dtype == kActF16 || act_dtype == kActBf16, "tr_linear: act_dtype must be F16(1) or BF16(2)");
   TR_REQUIRE(rows >= 1 && cols >= 1 && batch >= 0, "tr_linear: bad shape batch=%lld rows=%lld cols=%lld",
@@ -57,7 +64,7 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
   for (int64_t n0 = 0; n0 < batch; n0 += 32) {
     const int nb_ = (int)(batch - n0 < 32 ? batch - n0 : 32);
     int rc = gemv_tq2(act_dtype, w, (const uint8_t*)x + n0 * ldx * esz, (uint8_t*)y + n0 * ldy * esz, ldx, ldy, nb_,
-                      (int)rows, (int)cols, ks, pdl, st);
+                      (int)rows, (int)cols, ks, workspace, ws_bytes, pdl, (flags >> 16) & 0xFF, st);
     if (rc) return rc;
   }
   return 0;

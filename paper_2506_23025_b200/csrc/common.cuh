@@ -26,15 +26,19 @@ constexpr int kActBf16 = 2;
 constexpr int kActF32 = 3;
 
 // ---- T16 device layout -----------------
-// Rows are padded to a multiple of 128 (zero trits, zero scales).  For every
-// (256-block b, 16-row tile t) there is a 1 KB "tile-block" at byte offset
-// (b * n_tiles + t) * 1024 holding 64 16-byte units; unit u = half*32 + c*8 + g
-// is chunk c (block columns 64c..64c+63) of row 16t + 8*half + g, encoded so
-// that word i, bits 16h + 8hb + 2j (+1) hold the digit of chunk column
-// 16i + 8hb + 2j + h.  Scales: per (b, t) 8 x half2 = (s[16t+g], s[16t+8+g]).
+// Rows are padded to a multiple of 128 (zero trits, zero scales).  The matrix is
+// cut into 16-row tiles t and 256-column blocks b; unit (t, b) is 1056 contiguous
+// bytes at offset (t * nb + b) * 1056 (tile-major, so a tile's K range is one
+// contiguous run that a single TMA bulk copy can fetch):
+//   bytes [0, 1024): 64 16-byte words; word u = half*32 + c*8 + g is chunk c
+//     (block columns 64c..64c+63) of row 16t + 8*half + g, encoded so that
+//     32-bit word w (0..3), bits 16h + 8hb + 2j (+1), hold the digit of chunk
+//     column 32*(w>>1) + 16hb + 4j + 2*(w&1) + h;
+//   bytes [1024, 1056): 8 half2 scale pairs (s[16t+g], s[16t+8+g]).
 constexpr int kRowPad = 128;
 constexpr int kTileBlockBytes = 1024;
 constexpr int kTileScaleBytes = 32;
+constexpr int kUnitBytes = kTileBlockBytes + kTileScaleBytes;   // 1056
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t rows_padded(int64_t rows) { return ceil_div(rows, kRowPad) * kRowPad; }

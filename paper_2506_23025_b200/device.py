@@ -17,6 +17,25 @@ from .blocks import BLOCK_ELEMENTS, DType
 
 _ACT = {torch.float16: _lib.ACT_F16, torch.bfloat16: _lib.ACT_BF16}
 
+_WORKSPACES: dict = {}
+
+
+def workspace(nbytes: int, device=None, stream=None) -> torch.Tensor:
+    """Per-(device, stream) zero-initialised workspace for tr_linear, grown on demand.
+
+    The kernels leave its counter region zeroed, so one buffer serves every
+    launch on that stream (including CUDA-graph replays, which bake the pointer in).
+    """
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    key = (dev.index, s.cuda_stream)
+    buf = _WORKSPACES.get(key)
+    if buf is None or buf.numel() < nbytes:
+        size = max(nbytes, 1 << 20, 0 if buf is None else 2 * buf.numel())
+        buf = torch.zeros(size, dtype=torch.uint8, device=dev)
+        _WORKSPACES[key] = buf
+    return buf
+
 
 class TernaryWeight:
     """A rows x cols ternary matrix resident on one GPU in the T16 layout."""
@@ -93,13 +112,14 @@ class TernaryWeight:
 
 
 def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, pdl: bool = False,
-           ksplit: int = 0) -> torch.Tensor:
+           ksplit: int = 0, ws: torch.Tensor | None = None, _dbg: int = 0) -> torch.Tensor:
     """y[..., rows] = x[..., cols] @ W^T for fp16/bf16 x on the GPU (TriRun hot path).
 
     Accumulation is fp32: per 256-block partial sums are scaled by the block's
     binary16 scale in fp32 and accumulated in ascending block order; the output
     is rounded once to x.dtype.  ``pdl`` launches with programmatic dependent
-    launch (for CUDA-graph-chained layers); ``ksplit`` forces the K split.
+    launch (for CUDA-graph-chained layers); ``ksplit`` forces the number of
+    K slices (0 = heuristic); ``ws`` overrides the per-stream workspace.
     """
     if x.dtype not in _ACT:
         raise TypeError(f"activations must be float16 or bfloat16, got {x.dtype}")
@@ -115,9 +135,12 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
     if out is None:
         out = torch.empty((*lead, w.rows), dtype=x.dtype, device=x.device)
     y2 = out.view(-1, w.rows)
-    flags = (_lib.LINEAR_PDL if pdl else 0) | ((int(ksplit) & 0xFF) << 8)
+    flags = (_lib.LINEAR_PDL if pdl else 0) | ((int(ksplit) & 0xFF) << 8) | ((int(_dbg) & 0xFF) << 16)
+    need = _lib.lib().tr_linear_workspace_size(int(w.fmt), batch, w.rows, w.cols)
+    if ws is None:
+        ws = workspace(need, x.device)
     _lib.call("tr_linear", int(w.fmt), w.data.data_ptr(), x2.data_ptr(), y2.data_ptr(), batch, w.rows, w.cols,
-              _ACT[x.dtype], x2.stride(0), y2.stride(0), flags, _lib.stream_handle())
+              _ACT[x.dtype], x2.stride(0), y2.stride(0), flags, ws.data_ptr(), ws.numel(), _lib.stream_handle())
     return out
 
 

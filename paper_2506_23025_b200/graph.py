@@ -1,0 +1,75 @@
+"""CUDA-graph execution of chained ternary linears (decode-style layer streams).
+
+A decode step is a long chain of small, HBM-bound products; at batch 1 a
+4096x4096 TQ2 GEMV moves only 4.3 MB (0.66 us at 6.5 TB/s), so launch
+overhead and the DRAM-latency ramp of each kernel dominate unless the launches
+are (a) captured once in a CUDA graph and (b) chained with programmatic
+dependent launch, which lets layer i+1 fetch its weights while layer i
+finishes (weights do not depend on the previous output; only x does).
+``LinearStack`` is that executor; ``run_host`` is the end-to-end call with
+host (pinned) buffers used by bench.py's e2e measurement.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .device import TernaryWeight, linear
+
+
+class LinearStack:
+    """y = W_{n-1}( ... W_1(W_0 x)) over TernaryWeights, replayed from one CUDA graph."""
+
+    def __init__(self, weights: list[TernaryWeight], batch: int, dtype=torch.float16, pdl: bool = True):
+        if not weights:
+            raise ValueError("empty stack")
+        for a, b in zip(weights, weights[1:]):
+            if a.rows != b.cols:
+                raise ValueError(f"chain mismatch: {a.rows} outputs feed {b.cols} inputs")
+        self.weights = weights
+        self.batch = int(batch)
+        self.dtype = dtype
+        self.pdl = pdl
+        dev = weights[0].data.device
+        self.x = torch.zeros((self.batch, weights[0].cols), dtype=dtype, device=dev)
+        self.bufs = [torch.empty((self.batch, w.rows), dtype=dtype, device=dev) for w in weights]
+        self.stream = torch.cuda.Stream(device=dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(self.stream):
+            self._body()                      # warm-up (lazy kernel attribute setup) outside capture
+            self.stream.synchronize()
+            with torch.cuda.graph(self.graph, stream=self.stream):
+                self._body()
+        torch.cuda.synchronize(dev)
+
+    def _body(self) -> None:
+        cur = self.x
+        for w, out in zip(self.weights, self.bufs):
+            linear(cur, w, out=out, pdl=self.pdl)
+            cur = out
+
+    @property
+    def out(self) -> torch.Tensor:
+        return self.bufs[-1]
+
+    @property
+    def launches(self) -> int:
+        return len(self.weights)
+
+    def algorithmic_bytes(self) -> int:
+        """Weights by the reference formula (linear.py:68-71) + activations in + outputs out, per replay."""
+        es = torch.finfo(self.dtype).bits // 8
+        return sum(w.weight_bytes + self.batch * (w.cols + w.rows) * es for w in self.weights)
+
+    def flops(self) -> int:
+        return sum(2 * w.rows * w.cols * self.batch for w in self.weights)
+
+    def replay(self) -> None:
+        """Enqueue one pass on the current stream (no host sync)."""
+        self.graph.replay()
+
+    def run_host(self, x_host: torch.Tensor, y_host: torch.Tensor) -> None:
+        """End-to-end: pinned host x -> device, graph replay, device -> pinned host y (async on the current stream)."""
+        self.x.copy_(x_host, non_blocking=True)
+        self.graph.replay()
+        y_host.copy_(self.out, non_blocking=True)

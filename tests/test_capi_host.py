@@ -37,8 +37,9 @@ def test_library_rejects_bad_arguments_without_gpu():
 
     assert _lib.lib().tr_layout_bytes(2, 0, 5) == -1
     assert _lib.lib().tr_layout_bytes(2, 4096, 4096) == 16 * 256 * (1024 + 32)
-    rc = _lib.lib().tr_linear(9, None, None, None, 1, 1, 1, 1, 1, 1, 0, None)
+    rc = _lib.lib().tr_linear(9, None, None, None, 1, 1, 1, 1, 1, 1, 0, None, 0, None)
     assert rc == -1 and b"fmt" in _lib.lib().tr_last_error()
+    assert _lib.lib().tr_linear_workspace_size(2, 1, 4096, 4096) > 4096 * 4 // 16
     with pytest.raises(_lib.TriRunError):
         _lib.call("tr_quantize_pack", 7, None, 1, 1, None, None, None)
 

@@ -29,6 +29,20 @@ def tp():
     return tp
 
 
+@pytest.fixture(autouse=True)
+def workspace_counters_stay_zero(tp):
+    """Invariant: every tr_linear launch leaves its split-tile arrival counters at zero."""
+    yield
+    from paper_2506_23025_b200 import device
+
+    torch.cuda.synchronize()
+    for key, buf in device._WORKSPACES.items():
+        cnt = buf[: 256 * 1024].view(torch.int32)   # the fixed counter region
+        idx = torch.nonzero(cnt).flatten()
+        assert idx.numel() == 0, (f"workspace {key} (ptr {buf.data_ptr():#x}, {buf.numel()} B): {idx.numel()} non-zero "
+                                  f"counters, first at {idx[:8].tolist()} = {cnt[idx[:8]].tolist()}")
+
+
 def rel_err(y, ref):
     y = np.asarray(y, np.float64)
     ref = np.asarray(ref, np.float64)
