@@ -28,7 +28,7 @@ int check_launch(const char* what) {
 }
 
 int gemv_tq2(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
-             int cols, int ks, void* workspace, size_t ws_bytes, int pdl, int dbg, cudaStream_t st);
+             int cols, int ctas, int pdl, cudaStream_t st);
 size_t gemv_workspace_bytes(int batch, int rows, int cols);
 
 }  // namespace tr
@@ -43,7 +43,7 @@ int tr_version(void) { return 1; }
 
 size_t tr_linear_workspace_size(int fmt, int64_t batch, int64_t rows, int64_t cols) {
   if (fmt != kFmtTq2 || rows < 1 || cols < 1 || batch < 0) return 0;
-  return gemv_workspace_bytes((int)(batch < 32 ? batch : 32), (int)rows, (int)cols);
+  return 256 * 1024 + gemv_workspace_bytes((int)(batch < 32 ? batch : 32), (int)rows, (int)cols);
 }
 
 int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
@@ -58,13 +58,13 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
   TR_REQUIRE(((uintptr_t)w & 15) == 0, "tr_linear: weight buffer must be 16-byte aligned");
   if (batch == 0) return 0;
   const int pdl = flags & 1;
-  const int ks = (flags >> 8) & 0xFF;
+  const int ctas = (flags >> 8) & 0xFFFF;
   cudaStream_t st = (cudaStream_t)stream;
   const size_t esz = 2;
   for (int64_t n0 = 0; n0 < batch; n0 += 32) {
     const int nb_ = (int)(batch - n0 < 32 ? batch - n0 : 32);
     int rc = gemv_tq2(act_dtype, w, (const uint8_t*)x + n0 * ldx * esz, (uint8_t*)y + n0 * ldy * esz, ldx, ldy, nb_,
-                      (int)rows, (int)cols, ks, workspace, ws_bytes, pdl, (flags >> 16) & 0xFF, st);
+                      (int)rows, (int)cols, ctas, pdl, st);
     if (rc) return rc;
   }
   return 0;

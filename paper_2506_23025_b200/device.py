@@ -112,14 +112,15 @@ class TernaryWeight:
 
 
 def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, pdl: bool = False,
-           ksplit: int = 0, ws: torch.Tensor | None = None, _dbg: int = 0) -> torch.Tensor:
+           ctas: int = 0, ws: torch.Tensor | None = None) -> torch.Tensor:
     """y[..., rows] = x[..., cols] @ W^T for fp16/bf16 x on the GPU (TriRun hot path).
 
     Accumulation is fp32: per 256-block partial sums are scaled by the block's
     binary16 scale in fp32 and accumulated in ascending block order; the output
     is rounded once to x.dtype.  ``pdl`` launches with programmatic dependent
-    launch (for CUDA-graph-chained layers); ``ksplit`` forces the number of
-    K slices (0 = heuristic); ``ws`` overrides the per-stream workspace.
+    launch (for CUDA-graph-chained layers); ``ctas`` forces the number of
+    CTAs the rows are partitioned over (0 = one per SM); ``ws`` overrides the
+    per-stream workspace.
     """
     if x.dtype not in _ACT:
         raise TypeError(f"activations must be float16 or bfloat16, got {x.dtype}")
@@ -135,7 +136,7 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
     if out is None:
         out = torch.empty((*lead, w.rows), dtype=x.dtype, device=x.device)
     y2 = out.view(-1, w.rows)
-    flags = (_lib.LINEAR_PDL if pdl else 0) | ((int(ksplit) & 0xFF) << 8) | ((int(_dbg) & 0xFF) << 16)
+    flags = (_lib.LINEAR_PDL if pdl else 0) | ((int(ctas) & 0xFFFF) << 8)
     need = _lib.lib().tr_linear_workspace_size(int(w.fmt), batch, w.rows, w.cols)
     if ws is None:
         ws = workspace(need, x.device)

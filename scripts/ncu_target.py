@@ -1,15 +1,15 @@
-"""Minimal launcher for ncu captures: rows cols batch [rt ks] -> rotating-copy linear calls."""
+"""Minimal launcher for ncu captures: rows cols batch [ctas] -> rotating-copy linear calls."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2506_23025_b200 as tp
 rows, cols, batch = (int(v) for v in sys.argv[1:4])
-ks = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+ctas = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 wb = rows * (-(-cols // 256)) * 66
 copies = max(2, min(32, -(-3 * 126 * 2**20 // wb)))
 ws = [tp.TernaryWeight.from_float(torch.randn(rows, cols, device="cuda")) for _ in range(copies)]
 x = torch.randn(batch, cols, device="cuda").half()
 for i in range(3 * copies):
-    tp.linear(x, ws[i % copies], ksplit=ks)
+    tp.linear(x, ws[i % copies], ctas=ctas)
 torch.cuda.synchronize()
 print("ok")

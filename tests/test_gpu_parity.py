@@ -184,18 +184,18 @@ def test_linear_vs_oracle(tp, dtype, rows, cols, batch):
     assert err <= (2e-3 if dtype == "float16" else 6e-3)
 
 
-@pytest.mark.parametrize("ks", [1, 2, 3, 5, 8])
-def test_linear_ksplit_consistent(tp, ks):
+@pytest.mark.parametrize("ctas", [1, 2, 3, 5, 8, 148])
+def test_linear_partition_consistent(tp, ctas):
     rng = np.random.default_rng(9)
     rows, cols = 512, 8192
     W = (rng.integers(0, 3, size=(rows, cols)) - 1).astype(np.float32)
     pm = tp.pack_matrix(W, tp.DType.TQ2)
     w = pm.to_device()
     x = torch.from_numpy(rng.uniform(-1, 1, size=(4, cols)).astype(np.float32)).half().cuda()
-    y = tp.linear(x, w, ksplit=ks).float().cpu().numpy()
+    y = tp.linear(x, w, ctas=ctas).float().cpu().numpy()
     ref = (W.astype(np.float64) @ x.float().cpu().numpy().astype(np.float64).T).T
     assert rel_err(y, ref) <= 2e-3
-    y2 = tp.linear(x, w, ksplit=ks).float().cpu().numpy()
+    y2 = tp.linear(x, w, ctas=ctas).float().cpu().numpy()
     np.testing.assert_array_equal(y, y2)   # run-to-run deterministic
 
 
