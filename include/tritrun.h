@@ -41,7 +41,10 @@ extern "C" {
 #define TR_FMT_TQ1 3
 #define TR_ACT_F16 1
 #define TR_ACT_BF16 2
-#define TR_LINEAR_PDL 1 /* flags bit 0: launch with programmatic dependent launch */
+#define TR_LINEAR_PDL 1            /* flags bit 0: launch with programmatic dependent launch */
+#define TR_LINEAR_UNIFORM_SCALE 2  /* bit 1: caller asserts each row has one scale for all its blocks */
+#define TR_LINEAR_FORCE_UMMA 4     /* bit 2: force the tcgen05 tensor-core GEMM */
+#define TR_LINEAR_FORCE_GEMV 8     /* bit 3: force the mma.sync GEMV */
 
 TR_API const char* tr_last_error(void);
 TR_API int tr_version(void);
@@ -95,7 +98,8 @@ TR_API size_t tr_linear_workspace_size(int fmt, int64_t batch, int64_t rows, int
 /* y[batch, rows] = x[batch, cols] @ W^T  (linear.py:137-166 gemm semantics with the
  * paper's fp16/bf16 activations, fp32 accumulation, RNE output).  w is the device
  * layout from tr_repack; x has leading dimension ldx, y has ldy (elements).
- * flags: TR_LINEAR_PDL | (forced CTA count << 8) (0 = one CTA per SM). */
+ * Batches >= 24 run the tcgen05 GEMM (K5), smaller ones the GEMV (K3).
+ * flags: TR_LINEAR_* bits | (knob << 8): GEMV CTA count / GEMM K split (0 = automatic). */
 TR_API int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
                      int act_dtype, int64_t ldx, int64_t ldy, int flags, void* workspace, size_t ws_bytes,
                      void* stream);

@@ -20,6 +20,9 @@ FMT_TQ1 = 3
 ACT_F16 = 1
 ACT_BF16 = 2
 LINEAR_PDL = 1
+LINEAR_UNIFORM_SCALE = 2
+LINEAR_FORCE_UMMA = 4
+LINEAR_FORCE_GEMV = 8
 
 _lock = threading.Lock()
 _lib = None

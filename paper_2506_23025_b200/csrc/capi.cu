@@ -30,6 +30,12 @@ int check_launch(const char* what) {
 int gemv_tq2(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
              int cols, int ctas, int pdl, cudaStream_t st);
 size_t gemv_workspace_bytes(int batch, int rows, int cols);
+int gemm_umma(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
+              int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st);
+size_t umma_workspace_bytes(int batch, int rows, int cols);
+
+// batch at which the tensor-core (tcgen05) GEMM takes over from the mma.sync GEMV
+constexpr int64_t kUmmaMinBatch = 24;
 
 }  // namespace tr
 
@@ -43,7 +49,9 @@ int tr_version(void) { return 1; }
 
 size_t tr_linear_workspace_size(int fmt, int64_t batch, int64_t rows, int64_t cols) {
   if (fmt != kFmtTq2 || rows < 1 || cols < 1 || batch < 0) return 0;
-  return 256 * 1024 + gemv_workspace_bytes((int)(batch < 32 ? batch : 32), (int)rows, (int)cols);
+  const size_t g = 256 * 1024 + gemv_workspace_bytes((int)(batch < 32 ? batch : 32), (int)rows, (int)cols);
+  const size_t u = umma_workspace_bytes((int)(batch > 0 ? batch : 1), (int)rows, (int)cols);
+  return g > u ? g : u;
 }
 
 int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
@@ -57,14 +65,25 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
   TR_REQUIRE(ldx >= cols && ldy >= rows, "tr_linear: leading dimensions too small");
   TR_REQUIRE(((uintptr_t)w & 15) == 0, "tr_linear: weight buffer must be 16-byte aligned");
   if (batch == 0) return 0;
-  const int pdl = flags & 1;
-  const int ctas = (flags >> 8) & 0xFFFF;
+  const int pdl = flags & TR_LINEAR_PDL;
+  const int uniform = (flags & TR_LINEAR_UNIFORM_SCALE) ? 1 : 0;
+  const int knob = (flags >> 8) & 0xFFFF;   // GEMV: CTA count; UMMA: K split (0 = automatic)
   cudaStream_t st = (cudaStream_t)stream;
+  const bool aligned = (ldx % 8) == 0 && ((uintptr_t)x & 15) == 0;
+  bool use_umma = batch >= kUmmaMinBatch && aligned;
+  if (flags & TR_LINEAR_FORCE_UMMA) {
+    TR_REQUIRE(aligned, "tr_linear: the tensor-core path needs 16-byte aligned activation rows");
+    use_umma = true;
+  }
+  if (flags & TR_LINEAR_FORCE_GEMV) use_umma = false;
+  if (use_umma)
+    return gemm_umma(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, uniform, workspace,
+                     ws_bytes, pdl, st);
   const size_t esz = 2;
   for (int64_t n0 = 0; n0 < batch; n0 += 32) {
     const int nb_ = (int)(batch - n0 < 32 ? batch - n0 : 32);
     int rc = gemv_tq2(act_dtype, w, (const uint8_t*)x + n0 * ldx * esz, (uint8_t*)y + n0 * ldy * esz, ldx, ldy, nb_,
-                      (int)rows, (int)cols, ctas, pdl, st);
+                      (int)rows, (int)cols, knob, pdl, st);
     if (rc) return rc;
   }
   return 0;

@@ -1,0 +1,498 @@
+// K5: ternary GEMM on the 5th-generation tensor cores (tcgen05 / TMEM / TMA), TQ2 weights.
+//
+// Semantics (reference linear.py:137-166, _kernels.pyx:136-168; paper App. F):
+//   y[n, r] = sum_b s[r, b] * (sum_{k in block b} trit[r, k] * x[n, k])
+// fp16/bf16 activations, fp32 accumulation, each 256-block's sum scaled by the fp32
+// value of its binary16 scale; one rounding of the output.
+//
+// B200 design:
+//  * CTA tile = 128 weight rows (8 T16 tiles) x N activation rows (N = 16..128),
+//    over a K range of 256-blocks (split-K when the grid would not fill the SMs);
+//  * A operand = the decoded trits, written by the CUDA cores straight into TMEM
+//    (tcgen05.st), double-buffered per 256-block: per half2 one LOP3 (field | magic
+//    exponent) + one HFMA2 gives trit values exactly, in natural K order;
+//  * B operand = activations, loaded by TMA (128B-swizzled, K-major boxes of 64),
+//    so the tensor core reads them from shared memory without any thread touching them;
+//  * one elected thread issues 16 tcgen05.mma (M=128, N, K=16, A from TMEM) per
+//    block into a TMEM accumulator; workers read it back (tcgen05.ld) and apply the
+//    block's fp32 scale (per-block mode), or -- when every row has one scale for all
+//    its blocks (per-channel gamma) -- the MMA accumulates over all K and the scale is
+//    applied once;
+//  * warp roles: 8 decode/epilogue warps (two per TMEM lane quadrant), 1 TMA producer
+//    warp (weights by cp.async.bulk, activations by cp.async.bulk.tensor), 1 MMA warp.
+//    All hand-offs are mbarriers; there is no __syncthreads in the main loop.
+#include <cuda.h>
+
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace tr {
+
+namespace umma {
+
+constexpr int kWorkers = 8;                    // decode/epilogue warps
+constexpr int kThreads = (kWorkers + 2) * 32;  // + producer warp + MMA warp
+constexpr int kRowsPerCta = 128;
+constexpr int kStageWBytes = 8 * kUnitBytes;   // 8 T16 units = 128 rows x one 256-block
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// D[tmem] (+)= A[tmem] * B[smem desc]
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, int acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
+      ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+               ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n"
+      ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+        "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),
+        "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+// shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row core groups 1024 B apart
+__device__ __forceinline__ uint64_t desc_sw128(const void* p) {
+  const uint64_t addr = smem_u32(p);
+  return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// trit decode: field (digit d at mantissa bits 2j of each half, j-class of the E layout)
+// -> exact trit d - 1 as a half2 / bfloat162.  One LOP3 + one HFMA2.
+template <typename T> struct Dec;
+template <> struct Dec<__half> {
+  static constexpr uint32_t kMagic = 0x64006400u;   // 1024.0
+  __device__ static uint32_t trit2(uint32_t w, uint32_t w8, int hb, int j) {
+    const uint32_t v = lop3_and_or(hb ? w8 : w, 0x00030003u << (2 * j), kMagic);   // 1024 + 4^j d
+    const float m = (float)(1 << (2 * j));
+    const __half2 r = __hfma2(*reinterpret_cast<const __half2*>(&v), __float2half2_rn(1.0f / m),
+                              __float2half2_rn(-(1024.0f / m + 1.0f)));
+    return *reinterpret_cast<const uint32_t*>(&r);
+  }
+};
+template <> struct Dec<__nv_bfloat16> {
+  static constexpr uint32_t kMagic = 0x43004300u;   // 128.0 (7 mantissa bits: fields j < 3)
+  __device__ static uint32_t trit2(uint32_t w, uint32_t w8, int hb, int j) {
+    uint32_t v;
+    float m;
+    if (j < 3) {
+      v = lop3_and_or(hb ? w8 : w, 0x00030003u << (2 * j), kMagic);   // 128 + 4^j d
+      m = (float)(1 << (2 * j));
+    } else {
+      v = lop3_and_or(w >> (hb ? 14 : 6), 0x00030003u, kMagic);        // 128 + d
+      m = 1.0f;
+    }
+    const __nv_bfloat162 r = __hfma2(*reinterpret_cast<const __nv_bfloat162*>(&v), __float2bfloat162_rn(1.0f / m),
+                                     __float2bfloat162_rn(-(128.0f / m + 1.0f)));
+    return *reinterpret_cast<const uint32_t*>(&r);
+  }
+};
+
+}  // namespace umma
+
+struct UmmaArgs {
+  const uint8_t* w;   // T16 units, tile-major
+  void* y;            // [batch][ldy]
+  float* ws;          // split-K partials
+  int* counters;      // per-(m, n) tile arrival counters (zero between launches)
+  int64_t ldy;
+  int rows, nb, batch;
+  int m_tiles, n_tiles, ks;
+  int uniform;        // every row has one scale for all its blocks
+};
+
+template <typename T, int N>
+struct UmmaCfg {
+  static constexpr int kStages = N <= 64 ? 4 : 3;
+  static constexpr int kStageBBytes = N * 512;                    // N rows x 256 K fp16 (4 swizzled boxes)
+  static constexpr size_t kBOff = 1024;                           // 1024-aligned for the 128B swizzle
+  static constexpr size_t kWOff = kBOff + (size_t)kStages * kStageBBytes;
+  static constexpr size_t kSmem = kWOff + (size_t)kStages * umma::kStageWBytes + 1024;   // + alignment slack
+};
+
+template <typename T, int N>
+__global__ void __launch_bounds__(umma::kThreads, 1)
+    k_gemm_umma(const __grid_constant__ CUtensorMap tmx, const UmmaArgs a) {
+  using namespace umma;
+  using Cfg = UmmaCfg<T, N>;
+  constexpr int R = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);       // R
+  uint64_t* empty = full + R;                                // R
+  uint64_t* a_full = empty + R;                              // 2
+  uint64_t* a_empty = a_full + 2;                            // 2
+  uint64_t* d_full = a_empty + 2;                            // 2
+  uint64_t* d_empty = d_full + 2;                            // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
+  uint8_t* sB = smem + Cfg::kBOff;
+  uint8_t* sW = smem + Cfg::kWOff;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mt = blockIdx.x % a.m_tiles;
+  const int nt = (blockIdx.x / a.m_tiles) % a.n_tiles;
+  const int kslice = blockIdx.x / (a.m_tiles * a.n_tiles);
+  const int kb0 = (int)((int64_t)kslice * a.nb / a.ks), kb1 = (int)((int64_t)(kslice + 1) * a.nb / a.ks);
+  const int nblk = kb1 - kb0;
+  const bool per_block = !a.uniform;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < R; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWorkers + 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&a_full[i], kWorkers);
+      mbar_init(&a_empty[i], 1);
+      mbar_init(&d_full[i], 1);
+      mbar_init(&d_empty[i], kWorkers);
+    }
+    mbar_fence_init();
+  }
+  if (warp == kWorkers + 1) {   // TMEM: A double buffer (2 x 128 cols) + D (2 x N cols)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tA = tmem, tD = tmem + 256;
+  griddep_launch_dependents();
+
+  if (warp == kWorkers) {
+    // ================= TMA producer (one thread) =================
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      const uint8_t* wbase = a.w + ((int64_t)mt * 8 * a.nb + kb0) * kUnitBytes;
+      auto issue_w = [&](int i, int s) {
+#pragma unroll 1
+        for (int t = 0; t < 8; ++t)
+          bulk_g2s(sW + s * kStageWBytes + t * kUnitBytes, wbase + ((int64_t)t * a.nb + i) * kUnitBytes, kUnitBytes,
+                   &full[s], pol);
+      };
+      auto issue_b = [&](int i, int s) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          tma_load_2d(sB + s * Cfg::kStageBBytes + q * N * 128, &tmx, (kb0 + i) * kBlock + q * 64, nt * N, &full[s]);
+      };
+      const int pre = nblk < R ? nblk : R;
+      for (int i = 0; i < pre; ++i) {   // weights do not depend on the previous kernel
+        mbar_expect_tx(&full[i], kStageWBytes + Cfg::kStageBBytes);
+        issue_w(i, i);
+      }
+      griddep_wait();
+      for (int i = 0; i < pre; ++i) issue_b(i, i);
+      for (int i = R; i < nblk; ++i) {
+        const int s = i % R;
+        mbar_wait(&empty[s], ((i / R) & 1) ^ 1);
+        mbar_expect_tx(&full[s], kStageWBytes + Cfg::kStageBBytes);
+        issue_w(i, s);
+        issue_b(i, s);
+      }
+    }
+  } else if (warp == kWorkers + 1) {
+    // ================= MMA issuer (one thread) =================
+    constexpr uint32_t kFmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+    constexpr uint32_t idesc = (1u << 4) | (kFmt << 7) | (kFmt << 10) | ((uint32_t)(N >> 3) << 17) |
+                               ((uint32_t)(kRowsPerCta >> 4) << 24);
+    if (lane == 0) {
+      for (int i = 0; i < nblk; ++i) {
+        const int s = i % R, ab = i & 1;
+        mbar_wait(&full[s], (i / R) & 1);          // activations (and weights) landed
+        mbar_wait(&a_full[ab], (i >> 1) & 1);      // trits decoded into TMEM
+        if (per_block) mbar_wait(&d_empty[ab], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = per_block ? tD + ab * N : tD;
+        const uint8_t* b = sB + s * Cfg::kStageBBytes;
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+          const uint64_t bd = desc_sw128(b + (kk >> 2) * N * 128 + (kk & 3) * 32);
+          mma_ts(d, tA + ab * 128 + kk * 8, bd, idesc, (kk > 0 || (!per_block && i > 0)) ? 1 : 0);
+        }
+        mma_commit(&empty[s]);                     // smem stage reusable once these MMAs finish
+        mma_commit(&a_empty[ab]);                  // TMEM A buffer reusable
+        if (per_block || i == nblk - 1) mma_commit(&d_full[per_block ? ab : 0]);
+      }
+    }
+  } else {
+    // ================= decode + epilogue warps =================
+    const int quad = warp & 3, half_k = warp >> 2;     // TMEM lanes 32 quad..; K chunks 2 half_k, +1
+    const int r = quad * 32 + lane;                    // row within the CTA tile
+    const int tl = r >> 4, rt = r & 15;                // T16 tile, row in tile
+    const int hrow = rt >> 3, g = rt & 7;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    constexpr int NH = N / 2;                          // epilogue columns per thread
+    float acc[NH];
+#pragma unroll
+    for (int i = 0; i < NH; ++i) acc[i] = 0.0f;
+    float s_prev = 0.0f, s_first = 0.0f;
+
+    auto epilogue_block = [&](int i, float s) {        // acc += s * D_i (this thread's half of N)
+      const int ab = i & 1;
+      mbar_wait(&d_full[ab], (i >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c8 = 0; c8 < NH; c8 += 8) {
+        float v[8];
+        tmem_ld8(tD + lane_off + ab * N + half_k * NH + c8, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[c8 + e] = fmaf(s, v[e], acc[c8 + e]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&d_empty[ab]);
+    };
+
+    for (int i = 0; i < nblk; ++i) {
+      const int s = i % R, ab = i & 1;
+      mbar_wait(&full[s], (i / R) & 1);
+      const uint8_t* unit = sW + s * kStageWBytes + tl * kUnitBytes;
+      uint4 wv[2];
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) wv[cc] = lds128(unit + (hrow * 32 + (2 * half_k + cc) * 8 + g) * 16);
+      const uint32_t sv = *reinterpret_cast<const uint32_t*>(unit + kTileBlockBytes + g * 4);
+      const float s_cur = __half2float(hrow ? __high2half(*reinterpret_cast<const __half2*>(&sv))
+                                            : __low2half(*reinterpret_cast<const __half2*>(&sv)));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);            // weights read into registers
+      if (i == 0) s_first = s_cur;
+      mbar_wait(&a_empty[ab], ((i >> 1) & 1) ^ 1);      // MMA of block i-2 done with this A buffer
+      tc_fence_after();
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const uint32_t W[4] = {wv[cc].x, wv[cc].y, wv[cc].z, wv[cc].w};
+        uint32_t col[32];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const uint32_t w8 = W[w] >> 8;
+#pragma unroll
+          for (int hb = 0; hb < 2; ++hb)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)   // columns (2q, 2q+1) of chunk: q = 16(w>>1) + 8hb + 2j + (w&1)
+              col[16 * (w >> 1) + 8 * hb + 2 * j + (w & 1)] = Dec<T>::trit2(W[w], w8, hb, j);
+        }
+        tmem_st32(tA + lane_off + ab * 128 + (2 * half_k + cc) * 32, col);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_full[ab]);
+      if (per_block && i > 0) epilogue_block(i - 1, s_prev);
+      s_prev = s_cur;
+    }
+    if (nblk > 0) {
+      if (per_block) {
+        epilogue_block(nblk - 1, s_prev);
+      } else {
+        epilogue_block(0, s_first);   // the single accumulator (committed after the last block)
+      }
+    }
+    griddep_wait();
+    // ---- store: whole K in this CTA -> y; else partials + last-arriver reduction (fixed order)
+    T* y = reinterpret_cast<T*>(a.y);
+    const int row = mt * kRowsPerCta + r;
+    const int n0 = nt * N + half_k * NH;
+    if (a.ks == 1) {
+      if (row < a.rows)
+#pragma unroll
+        for (int e = 0; e < NH; ++e)
+          if (n0 + e < a.batch) y[(int64_t)(n0 + e) * a.ldy + row] = Act<T>::from_float(acc[e]);
+    } else {
+      const int tile_mn = nt * a.m_tiles + mt;
+      float* part = a.ws + ((int64_t)tile_mn * a.ks + kslice) * (kRowsPerCta * N);
+#pragma unroll
+      for (int e = 0; e < NH; ++e) __stcg(part + (half_k * NH + e) * kRowsPerCta + r, acc[e]);
+      __threadfence();
+      // one arrival per worker warp; the last of the ks * 8 arrivals reduces
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) last = atomicAdd(a.counters + tile_mn, 1) == a.ks * kWorkers - 1;
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        // this warp reduces all 128 rows x N of the tile: lane = row group
+        __threadfence();
+        const float* base = a.ws + (int64_t)tile_mn * a.ks * (kRowsPerCta * N);
+        for (int idx = lane; idx < kRowsPerCta * N; idx += 32) {
+          const int nn = idx / kRowsPerCta, rr = idx % kRowsPerCta;
+          float v = 0.0f;
+          for (int q = 0; q < a.ks; ++q) v += __ldcg(base + (int64_t)q * kRowsPerCta * N + idx);
+          const int orow = mt * kRowsPerCta + rr, on = nt * N + nn;
+          if (orow < a.rows && on < a.batch) y[(int64_t)on * a.ldy + orow] = Act<T>::from_float(v);
+        }
+        if (lane == 0) a.counters[tile_mn] = 0;   // self-reset
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == kWorkers + 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
+// ------------------------------------------------------------------------------------ host
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+constexpr size_t kUmmaCounterBytes = 256 * 1024;   // per-(m, n) tile counters (the workspace's fixed counter region)
+
+struct UmmaPlan {
+  int n, n_tiles, m_tiles, ks;
+  size_t ws_bytes;
+};
+
+static UmmaPlan plan_umma(int batch, int rows, int cols, int ks_force, int sms) {
+  UmmaPlan p;
+  p.n = batch <= 16 ? 16 : batch <= 32 ? 32 : batch <= 64 ? 64 : 128;
+  p.n_tiles = (int)ceil_div(batch, p.n);
+  p.m_tiles = (int)(rows_padded(rows) / 128);
+  const int nb = (int)ceil_div(cols, kBlock);
+  const int base = p.m_tiles * p.n_tiles;
+  int ks = ks_force > 0 ? ks_force : (base >= sms ? 1 : sms / base);
+  if (ks > nb / 2) ks = nb / 2 > 0 ? nb / 2 : 1;
+  if (ks > 16) ks = 16;
+  if (ks < 1) ks = 1;
+  p.ks = ks;
+  p.ws_bytes = ks > 1 ? (size_t)base * ks * 128 * p.n * 4 : 0;
+  return p;
+}
+
+size_t umma_workspace_bytes(int batch, int rows, int cols) {
+  size_t ws = 0;
+  for (int ks = 0; ks <= 16; ++ks) {
+    UmmaPlan p = plan_umma(batch, rows, cols, ks, sm_count());
+    if (p.ws_bytes > ws) ws = p.ws_bytes;
+  }
+  return kUmmaCounterBytes + ws;
+}
+
+template <typename T, int N>
+static int launch_umma(const CUtensorMap& map, const UmmaArgs& a, int grid, int pdl, cudaStream_t st) {
+  auto kern = k_gemm_umma<T, N>;
+  static int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UmmaCfg<T, N>::kSmem);
+    configured_dev = dev;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(umma::kThreads, 1, 1);
+  cfg.dynamicSmemBytes = UmmaCfg<T, N>::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  int na = 0;
+  if (pdl) {
+    attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attrs;
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, a);
+  if (e != cudaSuccess) {
+    set_error("tr_linear(umma): launch failed: %s (grid %d)", cudaGetErrorString(e), grid);
+    return -1;
+  }
+  return 0;
+}
+
+int gemm_umma(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
+              int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st) {
+  UmmaPlan p = plan_umma(batch, rows, cols, ks, sm_count());
+  if ((ldx % 8) != 0 || ((uintptr_t)x & 15) != 0) {
+    set_error("tr_linear(umma): activations need 16-byte aligned rows (ldx %% 8 == 0)");
+    return -1;
+  }
+  if ((size_t)p.m_tiles * p.n_tiles * 4 > kUmmaCounterBytes || workspace == nullptr ||
+      ws_bytes < kUmmaCounterBytes + p.ws_bytes) {
+    set_error("tr_linear(umma): workspace too small (%zu < %zu)", ws_bytes, kUmmaCounterBytes + p.ws_bytes);
+    return -1;
+  }
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) {
+    set_error("tr_linear(umma): cuTensorMapEncodeTiled unavailable");
+    return -1;
+  }
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)batch};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldx * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)p.n};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult cr = enc(&map, act == kActBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                    const_cast<void*>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) {
+    set_error("tr_linear(umma): cuTensorMapEncodeTiled failed (%d)", (int)cr);
+    return -1;
+  }
+  UmmaArgs a;
+  a.w = (const uint8_t*)w;
+  a.y = y;
+  a.counters = (int*)workspace;
+  a.ws = (float*)((uint8_t*)workspace + kUmmaCounterBytes);
+  a.ldy = ldy;
+  a.rows = rows;
+  a.nb = (int)ceil_div(cols, kBlock);
+  a.batch = batch;
+  a.m_tiles = p.m_tiles;
+  a.n_tiles = p.n_tiles;
+  a.ks = p.ks;
+  a.uniform = uniform;
+  const int grid = p.m_tiles * p.n_tiles * p.ks;
+  const bool bf = act == kActBf16;
+  switch (p.n) {
+    case 16: return bf ? launch_umma<__nv_bfloat16, 16>(map, a, grid, pdl, st) : launch_umma<__half, 16>(map, a, grid, pdl, st);
+    case 32: return bf ? launch_umma<__nv_bfloat16, 32>(map, a, grid, pdl, st) : launch_umma<__half, 32>(map, a, grid, pdl, st);
+    case 64: return bf ? launch_umma<__nv_bfloat16, 64>(map, a, grid, pdl, st) : launch_umma<__half, 64>(map, a, grid, pdl, st);
+    default: return bf ? launch_umma<__nv_bfloat16, 128>(map, a, grid, pdl, st) : launch_umma<__half, 128>(map, a, grid, pdl, st);
+  }
+}
+
+}  // namespace tr

@@ -40,11 +40,14 @@ def workspace(nbytes: int, device=None, stream=None) -> torch.Tensor:
 class TernaryWeight:
     """A rows x cols ternary matrix resident on one GPU in the T16 layout."""
 
-    def __init__(self, data: torch.Tensor, rows: int, cols: int, fmt: DType):
+    def __init__(self, data: torch.Tensor, rows: int, cols: int, fmt: DType, uniform_scale: bool = False):
         self.data = data
         self.rows = int(rows)
         self.cols = int(cols)
         self.fmt = DType(fmt)
+        # every row has one scale for all its blocks (per-channel gamma): the tensor-core
+        # path may then apply the scale once per row instead of once per 256-block
+        self.uniform_scale = bool(uniform_scale)
 
     # -- construction ---------------------------------------------------------------
     @classmethod
@@ -58,7 +61,9 @@ class TernaryWeight:
         data = torch.empty(nbytes, dtype=torch.uint8, device=payload.device)
         _lib.call("tr_repack", int(fmt), payload.data_ptr(), scales_f16.data_ptr(), rows, cols, data.data_ptr(),
                   _lib.stream_handle())
-        return cls(data, rows, cols, fmt)
+        s = scales_f16.view(torch.int16).reshape(rows, -1)
+        uniform = bool((s == s[:, :1]).all())
+        return cls(data, rows, cols, fmt, uniform_scale=uniform)
 
     @classmethod
     def from_packed(cls, pm) -> "TernaryWeight":
@@ -111,16 +116,20 @@ class TernaryWeight:
         return f"TernaryWeight({self.rows}x{self.cols}, {self.fmt.name}, {self.data.numel()} B on {self.data.device})"
 
 
+_PATHS = {"auto": 0, "umma": _lib.LINEAR_FORCE_UMMA, "gemv": _lib.LINEAR_FORCE_GEMV}
+
+
 def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, pdl: bool = False,
-           ctas: int = 0, ws: torch.Tensor | None = None) -> torch.Tensor:
+           ctas: int = 0, ws: torch.Tensor | None = None, path: str = "auto", ksplit: int = 0) -> torch.Tensor:
     """y[..., rows] = x[..., cols] @ W^T for fp16/bf16 x on the GPU (TriRun hot path).
 
     Accumulation is fp32: per 256-block partial sums are scaled by the block's
     binary16 scale in fp32 and accumulated in ascending block order; the output
     is rounded once to x.dtype.  ``pdl`` launches with programmatic dependent
-    launch (for CUDA-graph-chained layers); ``ctas`` forces the number of
-    CTAs the rows are partitioned over (0 = one per SM); ``ws`` overrides the
-    per-stream workspace.
+    launch (for CUDA-graph-chained layers).  Batches >= 24 run the tcgen05
+    tensor-core GEMM, smaller ones the decode GEMV; ``path`` ("umma" / "gemv")
+    forces one.  ``ctas`` forces the GEMV's CTA count and ``ksplit`` the GEMM's
+    K split (0 = automatic); ``ws`` overrides the per-stream workspace.
     """
     if x.dtype not in _ACT:
         raise TypeError(f"activations must be float16 or bfloat16, got {x.dtype}")
@@ -136,7 +145,9 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
     if out is None:
         out = torch.empty((*lead, w.rows), dtype=x.dtype, device=x.device)
     y2 = out.view(-1, w.rows)
-    flags = (_lib.LINEAR_PDL if pdl else 0) | ((int(ctas) & 0xFFFF) << 8)
+    flags = (_lib.LINEAR_PDL if pdl else 0) | (_lib.LINEAR_UNIFORM_SCALE if w.uniform_scale else 0) | _PATHS[path]
+    umma = path == "umma" or (path == "auto" and batch >= 24)
+    flags |= ((int(ksplit if umma else ctas)) & 0xFFFF) << 8
     need = _lib.lib().tr_linear_workspace_size(int(w.fmt), batch, w.rows, w.cols)
     if ws is None:
         ws = workspace(need, x.device)

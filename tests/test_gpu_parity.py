@@ -260,3 +260,73 @@ def test_linear_baseline_shapes_vs_fp32(tp, rows, cols, batch):
     ref = x.float() @ dense.T
     err = ((y - ref).abs().amax(dim=1) / ref.abs().amax(dim=1)).max().item()
     assert err <= 2e-3, err
+
+
+# ---------------------------------------------------------------- tcgen05 tensor-core GEMM (K5)
+
+def _rand_packed(rng, rows, cols, per_block):
+    T = (rng.integers(0, 3, size=(rows, cols)) - 1).astype(np.float32)
+    gam = np.float16(0.02 * (1 + rng.uniform(0, 1, size=(rows, 1)))).astype(np.float32)
+    W = gam * T
+    if per_block:   # scales that differ between the 256-blocks of a row
+        nb = -(-cols // 256)
+        f = rng.choice([1.0, 0.5, 0.25], size=(rows, nb)).astype(np.float32)
+        W = W * np.repeat(f, 256, axis=1)[:, :cols]
+    return orc.pack_matrix(W, 2)
+
+
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
+@pytest.mark.parametrize("rows,cols", [(128, 256), (256, 4096), (300, 1000), (640, 11008)])
+@pytest.mark.parametrize("batch", [1, 16, 40, 128, 200])
+@pytest.mark.parametrize("per_block", [False, True])
+def test_umma_vs_oracle(tp, dtype, rows, cols, batch, per_block):
+    tdt = getattr(torch, dtype)
+    rng = np.random.default_rng(rows + 3 * cols + 7 * batch + per_block)
+    payload, scales = _rand_packed(rng, rows, cols, per_block)
+    pm = tp.PackedMatrix(rows=rows, cols=cols, fmt=tp.DType.TQ2, payload=payload, scales=scales)
+    w = pm.to_device()
+    if cols > 256:
+        assert w.uniform_scale == (not per_block)
+    x = torch.from_numpy(rng.uniform(-1, 1, size=(batch, cols)).astype(np.float32)).to(tdt).cuda()
+    y = tp.linear(x, w, path="umma").float().cpu().numpy()
+    ref = _oracle_ref(payload, scales, cols, 2, x.float().cpu().numpy())
+    err = rel_err(y, ref)
+    assert err <= TOL, f"rel err {err:.3e}"
+    assert err <= (2e-3 if dtype == "float16" else 6e-3), err
+
+
+@pytest.mark.parametrize("ks", [1, 2, 3, 7])
+def test_umma_ksplit_consistent(tp, ks):
+    rng = np.random.default_rng(31 + ks)
+    rows, cols, batch = 512, 8192, 64
+    payload, scales = _rand_packed(rng, rows, cols, True)
+    pm = tp.PackedMatrix(rows=rows, cols=cols, fmt=tp.DType.TQ2, payload=payload, scales=scales)
+    w = pm.to_device()
+    x = torch.from_numpy(rng.uniform(-1, 1, size=(batch, cols)).astype(np.float32)).half().cuda()
+    y = tp.linear(x, w, path="umma", ksplit=ks)
+    ref = _oracle_ref(payload, scales, cols, 2, x.float().cpu().numpy())
+    assert rel_err(y.float().cpu().numpy(), ref) <= 2e-3
+    assert torch.equal(y, tp.linear(x, w, path="umma", ksplit=ks))   # deterministic
+
+
+def test_umma_exact_cases(tp):
+    # all-ones row sums activations exactly; basis vectors return the dequantized columns
+    pm1 = tp.pack_matrix(np.full((1, 256), 0.5, np.float32), tp.DType.TQ2)
+    y1 = tp.linear(torch.ones(32, 256, dtype=torch.float16, device="cuda"), pm1.to_device(), path="umma")
+    assert torch.all(y1.float() == 128.0)
+    rng = np.random.default_rng(46)
+    pmb = tp.pack_matrix(rng.normal(size=(6, 40)).astype(np.float32), tp.DType.TQ2)
+    dense16 = tp.dequantize_matrix(pmb, np.float16)
+    Yb = tp.linear(torch.eye(40, dtype=torch.float16, device="cuda"), pmb.to_device(), path="umma")
+    np.testing.assert_array_equal(Yb.cpu().numpy().T, dense16)
+
+
+@pytest.mark.parametrize("batch", [32, 64, 128])
+def test_umma_matches_gemv(tp, batch):
+    # both hot paths on the same resident weights agree within fp32-accumulation noise
+    g = torch.Generator(device="cuda").manual_seed(batch)
+    w = tp.TernaryWeight.from_float(torch.randn(4096, 4096, generator=g, device="cuda"))
+    x = (torch.rand(batch, 4096, generator=g, device="cuda") * 2 - 1).half()
+    a = tp.linear(x, w, path="umma").float()
+    b = tp.linear(x, w, path="gemv").float()
+    assert ((a - b).abs().amax(1) / b.abs().amax(1)).max().item() <= 2e-3
