@@ -31,7 +31,7 @@ int gemv_tq2(int act, const void* w, const void* x, void* y, int64_t ldx, int64_
              int cols, int ctas, int pdl, cudaStream_t st);
 size_t gemv_workspace_bytes(int batch, int rows, int cols);
 int gemm_umma(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
-              int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st);
+              int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg);
 size_t umma_workspace_bytes(int batch, int rows, int cols);
 
 // batch at which the tensor-core (tcgen05) GEMM takes over from the mma.sync GEMV
@@ -78,7 +78,7 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
   if (flags & TR_LINEAR_FORCE_GEMV) use_umma = false;
   if (use_umma)
     return gemm_umma(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, uniform, workspace,
-                     ws_bytes, pdl, st);
+                     ws_bytes, pdl, st, (flags >> 24) & 0xF);
   const size_t esz = 2;
   for (int64_t n0 = 0; n0 < batch; n0 += 32) {
     const int nb_ = (int)(batch - n0 < 32 ? batch - n0 : 32);

@@ -34,7 +34,6 @@ namespace umma {
 constexpr int kWorkers = 8;                    // decode/epilogue warps
 constexpr int kThreads = (kWorkers + 2) * 32;  // + producer warp + MMA warp
 constexpr int kRowsPerCta = 128;
-constexpr int kStageWBytes = 8 * kUnitBytes;   // 8 T16 units = 128 rows x one 256-block
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -46,15 +45,18 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// D[tmem] (+)= A[tmem] * B[smem desc]
+// D[tmem] (+)= A[tmem] * B[smem desc].  Called by a whole warp with warp-uniform operands;
+// elect.sync picks the issuing lane (a lane-0 branch makes the compiler serialise the
+// uniform-register set-up per MMA and costs ~3x the issue rate).
 __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, int acc) {
   asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
       ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+  asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+               "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n"
                ::"r"(smem_u32(bar)) : "memory");
 }
 
@@ -128,32 +130,65 @@ struct UmmaArgs {
   int rows, nb, batch;
   int m_tiles, n_tiles, ks;
   int uniform;        // every row has one scale for all its blocks
+  int dbg;            // development probes: 1 = skip MMAs, 2 = skip decode/TMEM stores
+  int map3d;          // activations described by the 3-D tensor map (one TMA request per block)
 };
 
 template <typename T, int N>
 struct UmmaCfg {
-  static constexpr int kStages = N <= 64 ? 4 : 3;
-  static constexpr int kStageBBytes = N * 512;                    // N rows x 256 K fp16 (4 swizzled boxes)
-  static constexpr size_t kBOff = 1024;                           // 1024-aligned for the 128B swizzle
-  static constexpr size_t kWOff = kBOff + (size_t)kStages * kStageBBytes;
-  static constexpr size_t kSmem = kWOff + (size_t)kStages * umma::kStageWBytes + 1024;   // + alignment slack
+  // TMA requests cost ~100 SM cycles each whatever their size, so the weights move in
+  // stages of KS blocks (8 requests of KS x 1056 B) and the activations in one 3-D box per block
+  static constexpr int KS = N <= 32 ? 4 : 2;                 // 256-blocks per weight stage
+  static constexpr int RW = N <= 32 ? 4 : 3;                 // weight stages
+  static constexpr int RB = N <= 32 ? 4 : N <= 64 ? 3 : 2;   // activation stages (one block each)
+  static constexpr int kStageWBytes = 8 * KS * kUnitBytes;   // 128 rows x KS blocks
+  static constexpr int kStageBBytes = N * 512;               // N rows x 256 K (4 swizzled 64-K atoms)
+  // independent accumulation chains: consecutive MMAs into one accumulator serialise on it,
+  // so the 16 K-steps of a block round-robin over C accumulators (summed in the epilogue)
+  static constexpr int C = N <= 16 ? 8 : 128 / N;
+  static constexpr int kDCols = C * N;                       // one accumulator set
+  static constexpr size_t kBOff = 1024;                      // 1024-aligned for the 128B swizzle
+  static constexpr size_t kWOff = kBOff + (size_t)RB * kStageBBytes;
+  static constexpr size_t kSmem = kWOff + (size_t)RW * kStageWBytes + 1024;   // + alignment slack
 };
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
+  uint32_t r;
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(r) : "r"(addr));
+  return r;
+}
 
 template <typename T, int N>
 __global__ void __launch_bounds__(umma::kThreads, 1)
     k_gemm_umma(const __grid_constant__ CUtensorMap tmx, const UmmaArgs a) {
   using namespace umma;
   using Cfg = UmmaCfg<T, N>;
-  constexpr int R = Cfg::kStages;
+  constexpr int KS = Cfg::KS, RW = Cfg::RW, RB = Cfg::RB;
+  constexpr int kStageW = Cfg::kStageWBytes, kStageB = Cfg::kStageBBytes;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);       // R
-  uint64_t* empty = full + R;                                // R
-  uint64_t* a_full = empty + R;                              // 2
+  uint64_t* full_w = reinterpret_cast<uint64_t*>(smem);     // RW
+  uint64_t* empty_w = full_w + RW;                           // RW
+  uint64_t* full_b = empty_w + RW;                           // RB
+  uint64_t* empty_b = full_b + RB;                           // RB
+  uint64_t* a_full = empty_b + RB;                           // 2
   uint64_t* a_empty = a_full + 2;                            // 2
   uint64_t* d_full = a_empty + 2;                            // 2
   uint64_t* d_empty = d_full + 2;                            // 2
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
+  int* flag = reinterpret_cast<int*>(tmem_slot + 1);
   uint8_t* sB = smem + Cfg::kBOff;
   uint8_t* sW = smem + Cfg::kWOff;
 
@@ -163,12 +198,17 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
   const int kslice = blockIdx.x / (a.m_tiles * a.n_tiles);
   const int kb0 = (int)((int64_t)kslice * a.nb / a.ks), kb1 = (int)((int64_t)(kslice + 1) * a.nb / a.ks);
   const int nblk = kb1 - kb0;
+  const int nws = (nblk + KS - 1) / KS;   // weight stages
   const bool per_block = !a.uniform;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < R; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kWorkers + 1);
+    for (int s = 0; s < RW; ++s) {
+      mbar_init(&full_w[s], 1);
+      mbar_init(&empty_w[s], kWorkers);
+    }
+    for (int s = 0; s < RB; ++s) {
+      mbar_init(&full_b[s], 1);
+      mbar_init(&empty_b[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&a_full[i], kWorkers);
@@ -187,37 +227,46 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tA = tmem, tD = tmem + 256;
+  constexpr int C = Cfg::C, kDCols = Cfg::kDCols;
   griddep_launch_dependents();
 
   if (warp == kWorkers) {
     // ================= TMA producer (one thread) =================
     if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmx) : "memory");
       const uint64_t pol = policy_evict_first();
       const uint8_t* wbase = a.w + ((int64_t)mt * 8 * a.nb + kb0) * kUnitBytes;
-      auto issue_w = [&](int i, int s) {
+      auto issue_w = [&](int si) {   // weight stage si: blocks [si KS, si KS + c) of the CTA's 8 tiles
+        const int s = si % RW, c = min(KS, nblk - si * KS);
+        mbar_expect_tx(&full_w[s], 8 * c * kUnitBytes);
 #pragma unroll 1
         for (int t = 0; t < 8; ++t)
-          bulk_g2s(sW + s * kStageWBytes + t * kUnitBytes, wbase + ((int64_t)t * a.nb + i) * kUnitBytes, kUnitBytes,
-                   &full[s], pol);
+          bulk_g2s(sW + s * kStageW + t * KS * kUnitBytes, wbase + ((int64_t)t * a.nb + si * KS) * kUnitBytes,
+                   c * kUnitBytes, &full_w[s], pol);
       };
-      auto issue_b = [&](int i, int s) {
+      auto issue_b = [&](int i) {
+        const int s = i % RB;
+        mbar_expect_tx(&full_b[s], kStageB);
+        if (a.map3d) {
+          tma_load_3d(sB + s * kStageB, &tmx, 0, nt * N, (kb0 + i) * 4, &full_b[s]);
+        } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          tma_load_2d(sB + s * Cfg::kStageBBytes + q * N * 128, &tmx, (kb0 + i) * kBlock + q * 64, nt * N, &full[s]);
+          for (int q = 0; q < 4; ++q)
+            tma_load_2d(sB + s * kStageB + q * N * 128, &tmx, (kb0 + i) * kBlock + q * 64, nt * N, &full_b[s]);
+        }
       };
-      const int pre = nblk < R ? nblk : R;
-      for (int i = 0; i < pre; ++i) {   // weights do not depend on the previous kernel
-        mbar_expect_tx(&full[i], kStageWBytes + Cfg::kStageBBytes);
-        issue_w(i, i);
-      }
+      int nw_ = nws < RW ? nws : RW, nb_ = nblk < RB ? nblk : RB;
+      for (int si = 0; si < nw_; ++si) issue_w(si);   // weights do not depend on the previous kernel
       griddep_wait();
-      for (int i = 0; i < pre; ++i) issue_b(i, i);
-      for (int i = R; i < nblk; ++i) {
-        const int s = i % R;
-        mbar_wait(&empty[s], ((i / R) & 1) ^ 1);
-        mbar_expect_tx(&full[s], kStageWBytes + Cfg::kStageBBytes);
-        issue_w(i, s);
-        issue_b(i, s);
+      for (int i = 0; i < nb_; ++i) issue_b(i);
+      while (nw_ < nws || nb_ < nblk) {                // refill whichever ring is needed first
+        if (nw_ < nws && (nw_ * KS <= nb_ || nb_ >= nblk)) {
+          mbar_wait(&empty_w[nw_ % RW], ((nw_ / RW) & 1) ^ 1);
+          issue_w(nw_++);
+        } else {
+          mbar_wait(&empty_b[nb_ % RB], ((nb_ / RB) & 1) ^ 1);
+          issue_b(nb_++);
+        }
       }
     }
   } else if (warp == kWorkers + 1) {
@@ -225,22 +274,24 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
     constexpr uint32_t kFmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
     constexpr uint32_t idesc = (1u << 4) | (kFmt << 7) | (kFmt << 10) | ((uint32_t)(N >> 3) << 17) |
                                ((uint32_t)(kRowsPerCta >> 4) << 24);
-    if (lane == 0) {
+    {   // the whole warp runs the loop; each MMA / commit is issued by one elected lane
       for (int i = 0; i < nblk; ++i) {
-        const int s = i % R, ab = i & 1;
-        mbar_wait(&full[s], (i / R) & 1);          // activations (and weights) landed
-        mbar_wait(&a_full[ab], (i >> 1) & 1);      // trits decoded into TMEM
+        const int s = i % RB, ab = i & 1;
+        mbar_wait(&full_b[s], (i / RB) & 1);         // activations landed
+        mbar_wait(&a_full[ab], (i >> 1) & 1);        // trits decoded into TMEM
         if (per_block) mbar_wait(&d_empty[ab], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = per_block ? tD + ab * N : tD;
-        const uint8_t* b = sB + s * Cfg::kStageBBytes;
+        const uint32_t d = per_block ? tD + ab * kDCols : tD;
+        const uint8_t* b = sB + s * kStageB;
+        if (!(a.dbg & 1)) {
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-          const uint64_t bd = desc_sw128(b + (kk >> 2) * N * 128 + (kk & 3) * 32);
-          mma_ts(d, tA + ab * 128 + kk * 8, bd, idesc, (kk > 0 || (!per_block && i > 0)) ? 1 : 0);
+          for (int kk = 0; kk < 16; ++kk) {
+            const uint64_t bd = desc_sw128(b + (kk >> 2) * N * 128 + (kk & 3) * 32);
+            mma_ts(d + (kk % C) * N, tA + ab * 128 + kk * 8, bd, idesc, (kk >= C || (!per_block && i > 0)) ? 1 : 0);
+          }
         }
-        mma_commit(&empty[s]);                     // smem stage reusable once these MMAs finish
-        mma_commit(&a_empty[ab]);                  // TMEM A buffer reusable
+        mma_commit(&empty_b[s]);                     // activation stage reusable once these MMAs finish
+        mma_commit(&a_empty[ab]);                    // TMEM A buffer reusable
         if (per_block || i == nblk - 1) mma_commit(&d_full[per_block ? ab : 0]);
       }
     }
@@ -256,6 +307,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
 #pragma unroll
     for (int i = 0; i < NH; ++i) acc[i] = 0.0f;
     float s_prev = 0.0f, s_first = 0.0f;
+    const uint32_t sW32 = smem_u32(sW) + tl * KS * kUnitBytes;
 
     auto epilogue_block = [&](int i, float s) {        // acc += s * D_i (this thread's half of N)
       const int ab = i & 1;
@@ -263,8 +315,15 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
       tc_fence_after();
 #pragma unroll
       for (int c8 = 0; c8 < NH; c8 += 8) {
-        float v[8];
-        tmem_ld8(tD + lane_off + ab * N + half_k * NH + c8, v);
+        float v[8], u[8];
+        tmem_ld8(tD + lane_off + ab * kDCols + half_k * NH + c8, v);
+#pragma unroll
+        for (int q = 1; q < C; ++q) {
+          tmem_ld8(tD + lane_off + ab * kDCols + q * N + half_k * NH + c8, u);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] += u[e];
+        }
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[c8 + e] = fmaf(s, v[e], acc[c8 + e]);
@@ -275,22 +334,25 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
     };
 
     for (int i = 0; i < nblk; ++i) {
-      const int s = i % R, ab = i & 1;
-      mbar_wait(&full[s], (i / R) & 1);
-      const uint8_t* unit = sW + s * kStageWBytes + tl * kUnitBytes;
+      const int si = i / KS, j = i - si * KS, s = si % RW, ab = i & 1;
+      if (j == 0) mbar_wait(&full_w[s], (si / RW) & 1);
+      const uint32_t unit = sW32 + s * kStageW + j * kUnitBytes;
       uint4 wv[2];
 #pragma unroll
-      for (int cc = 0; cc < 2; ++cc) wv[cc] = lds128(unit + (hrow * 32 + (2 * half_k + cc) * 8 + g) * 16);
-      const uint32_t sv = *reinterpret_cast<const uint32_t*>(unit + kTileBlockBytes + g * 4);
+      for (int cc = 0; cc < 2; ++cc) wv[cc] = ld_shared_v4(unit + (hrow * 32 + (2 * half_k + cc) * 8 + g) * 16);
+      const uint32_t sv = ld_shared_u32(unit + kTileBlockBytes + g * 4);
       const float s_cur = __half2float(hrow ? __high2half(*reinterpret_cast<const __half2*>(&sv))
                                             : __low2half(*reinterpret_cast<const __half2*>(&sv)));
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);            // weights read into registers
+      if (j == KS - 1 || i == nblk - 1) {               // weight stage fully read into registers
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_w[s]);
+      }
       if (i == 0) s_first = s_cur;
       mbar_wait(&a_empty[ab], ((i >> 1) & 1) ^ 1);      // MMA of block i-2 done with this A buffer
       tc_fence_after();
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
+        if (a.dbg & 2) break;
         const uint32_t W[4] = {wv[cc].x, wv[cc].y, wv[cc].z, wv[cc].w};
         uint32_t col[32];
 #pragma unroll
@@ -299,8 +361,8 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
 #pragma unroll
           for (int hb = 0; hb < 2; ++hb)
 #pragma unroll
-            for (int j = 0; j < 4; ++j)   // columns (2q, 2q+1) of chunk: q = 16(w>>1) + 8hb + 2j + (w&1)
-              col[16 * (w >> 1) + 8 * hb + 2 * j + (w & 1)] = Dec<T>::trit2(W[w], w8, hb, j);
+            for (int jj = 0; jj < 4; ++jj)   // columns (2q, 2q+1) of the chunk: q = 16(w>>1) + 8hb + 2jj + (w&1)
+              col[16 * (w >> 1) + 8 * hb + 2 * jj + (w & 1)] = Dec<T>::trit2(W[w], w8, hb, jj);
         }
         tmem_st32(tA + lane_off + ab * 128 + (2 * half_k + cc) * 32, col);
       }
@@ -312,14 +374,11 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
       s_prev = s_cur;
     }
     if (nblk > 0) {
-      if (per_block) {
-        epilogue_block(nblk - 1, s_prev);
-      } else {
-        epilogue_block(0, s_first);   // the single accumulator (committed after the last block)
-      }
+      if (per_block) epilogue_block(nblk - 1, s_prev);
+      else epilogue_block(0, s_first);   // the single accumulator (committed after the last block)
     }
     griddep_wait();
-    // ---- store: whole K in this CTA -> y; else partials + last-arriver reduction (fixed order)
+    // ---- store: whole K in this CTA -> y; else partials + last-CTA reduction (fixed slice order)
     T* y = reinterpret_cast<T*>(a.y);
     const int row = mt * kRowsPerCta + r;
     const int n0 = nt * N + half_k * NH;
@@ -334,23 +393,20 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
 #pragma unroll
       for (int e = 0; e < NH; ++e) __stcg(part + (half_k * NH + e) * kRowsPerCta + r, acc[e]);
       __threadfence();
-      // one arrival per worker warp; the last of the ks * 8 arrivals reduces
-      __syncwarp();
-      int last = 0;
-      if (lane == 0) last = atomicAdd(a.counters + tile_mn, 1) == a.ks * kWorkers - 1;
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) {
-        // this warp reduces all 128 rows x N of the tile: lane = row group
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kWorkers * 32) : "memory");   // all workers stored
+      if (threadIdx.x == 0) *flag = atomicAdd(a.counters + tile_mn, 1) == a.ks - 1;
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kWorkers * 32) : "memory");
+      if (*flag) {   // the last CTA of this tile sums the ks partials in slice order
         __threadfence();
         const float* base = a.ws + (int64_t)tile_mn * a.ks * (kRowsPerCta * N);
-        for (int idx = lane; idx < kRowsPerCta * N; idx += 32) {
-          const int nn = idx / kRowsPerCta, rr = idx % kRowsPerCta;
-          float v = 0.0f;
-          for (int q = 0; q < a.ks; ++q) v += __ldcg(base + (int64_t)q * kRowsPerCta * N + idx);
-          const int orow = mt * kRowsPerCta + rr, on = nt * N + nn;
-          if (orow < a.rows && on < a.batch) y[(int64_t)on * a.ldy + orow] = Act<T>::from_float(v);
-        }
-        if (lane == 0) a.counters[tile_mn] = 0;   // self-reset
+        if (row < a.rows)
+          for (int e = 0; e < NH; ++e) {
+            const int idx = (half_k * NH + e) * kRowsPerCta + r;
+            float v = 0.0f;
+            for (int q = 0; q < a.ks; ++q) v += __ldcg(base + (int64_t)q * kRowsPerCta * N + idx);
+            if (n0 + e < a.batch) y[(int64_t)(n0 + e) * a.ldy + row] = Act<T>::from_float(v);
+          }
+        if (threadIdx.x == 0) a.counters[tile_mn] = 0;   // self-reset
       }
     }
   }
@@ -444,7 +500,7 @@ static int launch_umma(const CUtensorMap& map, const UmmaArgs& a, int grid, int 
 }
 
 int gemm_umma(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
-              int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st) {
+              int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg) {
   UmmaPlan p = plan_umma(batch, rows, cols, ks, sm_count());
   if ((ldx % 8) != 0 || ((uintptr_t)x & 15) != 0) {
     set_error("tr_linear(umma): activations need 16-byte aligned rows (ldx %% 8 == 0)");
@@ -461,13 +517,26 @@ int gemm_umma(int act, const void* w, const void* x, void* y, int64_t ldx, int64
     return -1;
   }
   CUtensorMap map;
-  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)batch};
-  const cuuint64_t strides[1] = {(cuuint64_t)ldx * 2};
-  const cuuint32_t box[2] = {64, (cuuint32_t)p.n};
-  const cuuint32_t estr[2] = {1, 1};
-  CUresult cr = enc(&map, act == kActBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
-                    const_cast<void*>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUtensorMapDataType dt = act == kActBf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  int map3d = 0;
+  CUresult cr = CUDA_ERROR_INVALID_VALUE;
+  if (cols % kBlock == 0) {   // x as [cols/64][batch][64]: one request loads a whole 256-block
+    const cuuint64_t dims[3] = {64, (cuuint64_t)batch, (cuuint64_t)(cols / 64)};
+    const cuuint64_t strides[2] = {(cuuint64_t)ldx * 2, 128};
+    const cuuint32_t box[3] = {64, (cuuint32_t)p.n, 4};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    cr = enc(&map, dt, 3, const_cast<void*>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    map3d = cr == CUDA_SUCCESS;
+  }
+  if (!map3d) {
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)batch};
+    const cuuint64_t strides[1] = {(cuuint64_t)ldx * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)p.n};
+    const cuuint32_t estr[2] = {1, 1};
+    cr = enc(&map, dt, 2, const_cast<void*>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   if (cr != CUDA_SUCCESS) {
     set_error("tr_linear(umma): cuTensorMapEncodeTiled failed (%d)", (int)cr);
     return -1;
@@ -485,6 +554,8 @@ int gemm_umma(int act, const void* w, const void* x, void* y, int64_t ldx, int64
   a.n_tiles = p.n_tiles;
   a.ks = p.ks;
   a.uniform = uniform;
+  a.dbg = dbg;
+  a.map3d = map3d;
   const int grid = p.m_tiles * p.n_tiles * p.ks;
   const bool bf = act == kActBf16;
   switch (p.n) {

@@ -120,7 +120,8 @@ _PATHS = {"auto": 0, "umma": _lib.LINEAR_FORCE_UMMA, "gemv": _lib.LINEAR_FORCE_G
 
 
 def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, pdl: bool = False,
-           ctas: int = 0, ws: torch.Tensor | None = None, path: str = "auto", ksplit: int = 0) -> torch.Tensor:
+           ctas: int = 0, ws: torch.Tensor | None = None, path: str = "auto", ksplit: int = 0,
+           _probe: int = 0) -> torch.Tensor:
     """y[..., rows] = x[..., cols] @ W^T for fp16/bf16 x on the GPU (TriRun hot path).
 
     Accumulation is fp32: per 256-block partial sums are scaled by the block's
@@ -148,6 +149,7 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
     flags = (_lib.LINEAR_PDL if pdl else 0) | (_lib.LINEAR_UNIFORM_SCALE if w.uniform_scale else 0) | _PATHS[path]
     umma = path == "umma" or (path == "auto" and batch >= 24)
     flags |= ((int(ksplit if umma else ctas)) & 0xFFFF) << 8
+    flags |= (int(_probe) & 0xF) << 24   # development probes (see csrc); 0 in production
     need = _lib.lib().tr_linear_workspace_size(int(w.fmt), batch, w.rows, w.cols)
     if ws is None:
         ws = workspace(need, x.device)

@@ -7,6 +7,8 @@ from paper_2506_23025_b200.graph import LinearStack
 
 shapes = [(4096, 4096), (11008, 4096), (4096, 11008), (8192, 8192), (28672, 8192), (8192, 28672)]
 batches = [int(b) for b in (sys.argv[1] if len(sys.argv) > 1 else "1,8,16,32").split(",")]
+paths = (sys.argv[2] if len(sys.argv) > 2 else "auto").split(",")
+shapes = [tuple(int(v) for v in s.split("x")) for s in sys.argv[3].split(",")] if len(sys.argv) > 3 else shapes
 res = []
 for rows, cols in shapes:
     wb = rows * (cols // 256) * 66
@@ -16,16 +18,16 @@ for rows, cols in shapes:
     for b in batches:
         x = torch.randn(b, cols, device="cuda").half()
         ys = [torch.empty(b, rows, device="cuda", dtype=torch.half) for _ in range(R)]
-        for pdl in (False, True):
+        for pdl, path in [(True, p) for p in paths]:
             s = torch.cuda.Stream()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.stream(s):
                 for w, y in zip(ws, ys):
-                    tp.linear(x, w, out=y, pdl=pdl)
+                    tp.linear(x, w, out=y, pdl=pdl, path=path)
                 s.synchronize()
                 with torch.cuda.graph(g, stream=s):
                     for w, y in zip(ws, ys):
-                        tp.linear(x, w, out=y, pdl=pdl)
+                        tp.linear(x, w, out=y, pdl=pdl, path=path)
             torch.cuda.synchronize()
             for _ in range(3):
                 g.replay()
@@ -39,7 +41,7 @@ for rows, cols in shapes:
             e1.synchronize()
             us = e0.elapsed_time(e1) * 1e3 / n / R
             nbytes = wb + b * (rows + cols) * 2
-            res.append(dict(rows=rows, cols=cols, batch=b, pdl=pdl, us=round(us, 3), gbs=round(nbytes / us / 1e3, 1)))
+            res.append(dict(rows=rows, cols=cols, batch=b, path=path, tflops=round(2*rows*cols*b/us/1e6, 1), us=round(us, 3), gbs=round(nbytes / us / 1e3, 1)))
             print(json.dumps(res[-1]), flush=True)
         # correctness spot check vs dense
         dense = ws[0].dequantize(torch.float16).float()
