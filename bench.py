@@ -295,9 +295,13 @@ def run_ours(args, rank, world, dist):
     if rank == 0:
         cpu = CpuReference(os.cpu_count() or 1).sample(args.cpu_seconds)
         traffic = None
-        prof = os.path.join(ROOT, "profiles", "gemv_ncu_summary.json")
-        if os.path.exists(prof):
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        prof = os.path.join(ROOT, "profiles", "r01_ncu_full_summary.json")
+        if os.path.exists(prof):   # one `ncu --set full` capture of the GEMV (scripts/profile_round.sh)
+            g = json.load(open(prof)).get("k_gemv_tq2", {})
+            if g.get("dram__bytes_read.sum"):
+                traffic = {"bytes_per_launch": round((float(g["dram__bytes_read.sum"]) +
+                                                      float(g.get("dram__bytes_write.sum") or 0)) * 1e6),
+                           "shape": g.get("shape"), "algorithmic_bytes": 11008 * 16 * 66 + 2 * (11008 + 4096)}
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,

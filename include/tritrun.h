@@ -98,7 +98,7 @@ TR_API size_t tr_linear_workspace_size(int fmt, int64_t batch, int64_t rows, int
 /* y[batch, rows] = x[batch, cols] @ W^T  (linear.py:137-166 gemm semantics with the
  * paper's fp16/bf16 activations, fp32 accumulation, RNE output).  w is the device
  * layout from tr_repack; x has leading dimension ldx, y has ldy (elements).
- * Batches >= 24 run the tcgen05 GEMM (K5), smaller ones the GEMV (K3).
+ * Batches >= 9 run the tcgen05 GEMM (K5), smaller ones the GEMV (K3).
  * flags: TR_LINEAR_* bits | (knob << 8): GEMV CTA count / GEMM K split (0 = automatic). */
 TR_API int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
                      int act_dtype, int64_t ldx, int64_t ldy, int flags, void* workspace, size_t ws_bytes,

@@ -35,7 +35,7 @@ int gemm_umma(int act, const void* w, const void* x, void* y, int64_t ldx, int64
 size_t umma_workspace_bytes(int batch, int rows, int cols);
 
 // batch at which the tensor-core (tcgen05) GEMM takes over from the mma.sync GEMV
-constexpr int64_t kUmmaMinBatch = 24;
+constexpr int64_t kUmmaMinBatch = 9;
 
 }  // namespace tr
 

@@ -143,10 +143,7 @@ struct UmmaCfg {
   static constexpr int RB = N <= 32 ? 4 : N <= 64 ? 3 : 2;   // activation stages (one block each)
   static constexpr int kStageWBytes = 8 * KS * kUnitBytes;   // 128 rows x KS blocks
   static constexpr int kStageBBytes = N * 512;               // N rows x 256 K (4 swizzled 64-K atoms)
-  // independent accumulation chains: consecutive MMAs into one accumulator serialise on it,
-  // so the 16 K-steps of a block round-robin over C accumulators (summed in the epilogue)
-  static constexpr int C = N <= 16 ? 8 : 128 / N;
-  static constexpr int kDCols = C * N;                       // one accumulator set
+  static constexpr int kMaxA = 3;                            // TMEM A buffers (128 columns = one block each)
   static constexpr size_t kBOff = 1024;                      // 1024-aligned for the 128B swizzle
   static constexpr size_t kWOff = kBOff + (size_t)RB * kStageBBytes;
   static constexpr size_t kSmem = kWOff + (size_t)RW * kStageWBytes + 1024;   // + alignment slack
@@ -183,9 +180,9 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
   uint64_t* empty_w = full_w + RW;                           // RW
   uint64_t* full_b = empty_w + RW;                           // RB
   uint64_t* empty_b = full_b + RB;                           // RB
-  uint64_t* a_full = empty_b + RB;                           // 2
-  uint64_t* a_empty = a_full + 2;                            // 2
-  uint64_t* d_full = a_empty + 2;                            // 2
+  uint64_t* a_full = empty_b + RB;                           // kMaxA
+  uint64_t* a_empty = a_full + Cfg::kMaxA;                   // kMaxA
+  uint64_t* d_full = a_empty + Cfg::kMaxA;                   // 2
   uint64_t* d_empty = d_full + 2;                            // 2
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
   int* flag = reinterpret_cast<int*>(tmem_slot + 1);
@@ -210,9 +207,11 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
       mbar_init(&full_b[s], 1);
       mbar_init(&empty_b[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < Cfg::kMaxA; ++i) {
       mbar_init(&a_full[i], kWorkers);
       mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&d_full[i], 1);
       mbar_init(&d_empty[i], kWorkers);
     }
@@ -226,8 +225,11 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tA = tmem, tD = tmem + 256;
-  constexpr int C = Cfg::C, kDCols = Cfg::kDCols;
+  // TMEM: NA A buffers of 128 columns, then the accumulator(s): 2 x N (per-block, double
+  // buffered) or N (uniform scale, one accumulator over all K)
+  const int dcols = per_block ? 2 * N : N;
+  const int NA = (512 - dcols) / 128 < Cfg::kMaxA ? (512 - dcols) / 128 : Cfg::kMaxA;
+  const uint32_t tA = tmem, tD = tmem + NA * 128;
   griddep_launch_dependents();
 
   if (warp == kWorkers) {
@@ -276,23 +278,23 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
                                ((uint32_t)(kRowsPerCta >> 4) << 24);
     {   // the whole warp runs the loop; each MMA / commit is issued by one elected lane
       for (int i = 0; i < nblk; ++i) {
-        const int s = i % RB, ab = i & 1;
+        const int s = i % RB, ab = i % NA, db = i & 1;
         mbar_wait(&full_b[s], (i / RB) & 1);         // activations landed
-        mbar_wait(&a_full[ab], (i >> 1) & 1);        // trits decoded into TMEM
-        if (per_block) mbar_wait(&d_empty[ab], ((i >> 1) & 1) ^ 1);
+        mbar_wait(&a_full[ab], (i / NA) & 1);        // trits decoded into TMEM
+        if (per_block) mbar_wait(&d_empty[db], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = per_block ? tD + ab * kDCols : tD;
+        const uint32_t d = per_block ? tD + db * N : tD;
         const uint8_t* b = sB + s * kStageB;
         if (!(a.dbg & 1)) {
 #pragma unroll
           for (int kk = 0; kk < 16; ++kk) {
             const uint64_t bd = desc_sw128(b + (kk >> 2) * N * 128 + (kk & 3) * 32);
-            mma_ts(d + (kk % C) * N, tA + ab * 128 + kk * 8, bd, idesc, (kk >= C || (!per_block && i > 0)) ? 1 : 0);
+            mma_ts(d, tA + ab * 128 + kk * 8, bd, idesc, (kk > 0 || (!per_block && i > 0)) ? 1 : 0);
           }
         }
         mma_commit(&empty_b[s]);                     // activation stage reusable once these MMAs finish
         mma_commit(&a_empty[ab]);                    // TMEM A buffer reusable
-        if (per_block || i == nblk - 1) mma_commit(&d_full[per_block ? ab : 0]);
+        if (per_block || i == nblk - 1) mma_commit(&d_full[per_block ? db : 0]);
       }
     }
   } else {
@@ -315,15 +317,8 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
       tc_fence_after();
 #pragma unroll
       for (int c8 = 0; c8 < NH; c8 += 8) {
-        float v[8], u[8];
-        tmem_ld8(tD + lane_off + ab * kDCols + half_k * NH + c8, v);
-#pragma unroll
-        for (int q = 1; q < C; ++q) {
-          tmem_ld8(tD + lane_off + ab * kDCols + q * N + half_k * NH + c8, u);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] += u[e];
-        }
+        float v[8];
+        tmem_ld8(tD + lane_off + ab * N + half_k * NH + c8, v);
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[c8 + e] = fmaf(s, v[e], acc[c8 + e]);
@@ -334,7 +329,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
     };
 
     for (int i = 0; i < nblk; ++i) {
-      const int si = i / KS, j = i - si * KS, s = si % RW, ab = i & 1;
+      const int si = i / KS, j = i - si * KS, s = si % RW, ab = i % NA;
       if (j == 0) mbar_wait(&full_w[s], (si / RW) & 1);
       const uint32_t unit = sW32 + s * kStageW + j * kUnitBytes;
       uint4 wv[2];
@@ -348,7 +343,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
         if (lane == 0) mbar_arrive(&empty_w[s]);
       }
       if (i == 0) s_first = s_cur;
-      mbar_wait(&a_empty[ab], ((i >> 1) & 1) ^ 1);      // MMA of block i-2 done with this A buffer
+      mbar_wait(&a_empty[ab], ((i / NA) & 1) ^ 1);      // MMA of block i-NA done with this A buffer
       tc_fence_after();
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {

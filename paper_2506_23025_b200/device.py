@@ -127,7 +127,7 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
     Accumulation is fp32: per 256-block partial sums are scaled by the block's
     binary16 scale in fp32 and accumulated in ascending block order; the output
     is rounded once to x.dtype.  ``pdl`` launches with programmatic dependent
-    launch (for CUDA-graph-chained layers).  Batches >= 24 run the tcgen05
+    launch (for CUDA-graph-chained layers).  Batches >= 9 run the tcgen05
     tensor-core GEMM, smaller ones the decode GEMV; ``path`` ("umma" / "gemv")
     forces one.  ``ctas`` forces the GEMV's CTA count and ``ksplit`` the GEMM's
     K split (0 = automatic); ``ws`` overrides the per-stream workspace.
@@ -147,7 +147,7 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
         out = torch.empty((*lead, w.rows), dtype=x.dtype, device=x.device)
     y2 = out.view(-1, w.rows)
     flags = (_lib.LINEAR_PDL if pdl else 0) | (_lib.LINEAR_UNIFORM_SCALE if w.uniform_scale else 0) | _PATHS[path]
-    umma = path == "umma" or (path == "auto" and batch >= 24)
+    umma = path == "umma" or (path == "auto" and batch >= 9)
     flags |= ((int(ksplit if umma else ctas)) & 0xFFFF) << 8
     flags |= (int(_probe) & 0xF) << 24   # development probes (see csrc); 0 in production
     need = _lib.lib().tr_linear_workspace_size(int(w.fmt), batch, w.rows, w.cols)

@@ -7,7 +7,13 @@ rows, cols, batch = (int(v) for v in sys.argv[1:4])
 ctas = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 wb = rows * (-(-cols // 256)) * 66
 copies = max(2, min(32, -(-3 * 126 * 2**20 // wb)))
-ws = [tp.TernaryWeight.from_float(torch.randn(rows, cols, device="cuda")) for _ in range(copies)]
+def weight():   # the bench's synthetic weights: random trits, per-channel fp16 gamma
+    T = torch.randint(-1, 2, (rows, cols), device="cuda").float()
+    gam = (0.02 * (1 + torch.rand((rows, 1), device="cuda"))).half().float()
+    return tp.TernaryWeight.from_float(gam * T)
+
+
+ws = [weight() for _ in range(copies)]
 x = torch.randn(batch, cols, device="cuda").half()
 for i in range(3 * copies):
     tp.linear(x, ws[i % copies], ctas=ctas)
