@@ -1,0 +1,179 @@
+"""TriLM-shaped decoder stack over the ternary linear path (BASELINE configs[2]).
+
+The paper's end-to-end benchmark (serving metrics 669-680) decodes
+with every transformer linear in TQ2 and fp16 embeddings / lm_head.  This module is
+the decoder-layer linear dispatch around the hot path: per layer one fused QKV
+projection, the attention output projection, one fused gate|up projection and the
+down projection -- all ``device.linear`` (batch 1 -> the decode GEMV, the 64-token
+prompt -> the tcgen05 GEMM) -- with RMSNorm, rotary embeddings, attention over a
+static KV cache and SwiGLU done by PyTorch (plumbing, not the product).
+
+One decode step (all layers + lm_head + greedy argmax + cache update) is captured
+in a CUDA graph whose inputs (token, position) live on the device and are advanced
+by the graph itself, so N output tokens are N back-to-back graph replays with no
+host round trip.  ``dense=True`` builds the fp16 cuBLAS twin on the same (exactly
+dequantized) weights for the speed-up baseline.
+
+Shape (SURVEY §8(d) shape note): d_model 3072, 30 layers, 24 heads x 128, SwiGLU
+9216, vocab 32000, untied fp16 embedding / lm_head -> 3.877B parameters.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.nn.functional as F
+
+from .device import TernaryWeight, linear
+
+
+@dataclass(frozen=True)
+class DecoderConfig:
+    d_model: int = 3072
+    n_layers: int = 30
+    n_heads: int = 24
+    d_ff: int = 9216
+    vocab: int = 32000
+    max_seq: int = 128
+    eps: float = 1e-5
+    rope_theta: float = 10000.0
+
+    @property
+    def head_dim(self) -> int:
+        return self.d_model // self.n_heads
+
+    def n_params(self) -> int:
+        d, f = self.d_model, self.d_ff
+        return self.n_layers * (4 * d * d + 3 * d * f + 2 * d) + 2 * self.vocab * d + d
+
+    def ternary_bytes(self) -> int:
+        """Packed bytes of the ternary linears (reference formula, 66 B per 256 weights)."""
+        d, f = self.d_model, self.d_ff
+        per = lambda r, c: r * (-(-c // 256)) * 66
+        return self.n_layers * (per(3 * d, d) + per(d, d) + per(2 * f, d) + per(d, f))
+
+
+def _ternary(rows, cols, gen, device):
+    """Random-init ternary matrix with per-channel fp16 gamma (the bench's synthetic weights)."""
+    T = torch.randint(0, 3, (rows, cols), generator=gen, device=device, dtype=torch.int8).float() - 1
+    gam = (0.02 * (1 + torch.rand((rows, 1), generator=gen, device=device))).half().float()
+    return TernaryWeight.from_float(gam * T)
+
+
+class TernaryDecoder:
+    def __init__(self, cfg: DecoderConfig = DecoderConfig(), device="cuda", seed: int = 0, dense: bool = False,
+                 weights=None, dtype=torch.float16):
+        self.cfg, self.device, self.dense, self.dtype = cfg, torch.device(device), dense, dtype
+        d, f, L = cfg.d_model, cfg.d_ff, cfg.n_layers
+        gen = torch.Generator(device=self.device).manual_seed(seed)
+        if weights is None:   # ternary weights, built once and shared with a dense twin
+            weights = {
+                "layers": [{"qkv": _ternary(3 * d, d, gen, self.device), "o": _ternary(d, d, gen, self.device),
+                            "gate_up": _ternary(2 * f, d, gen, self.device), "down": _ternary(d, f, gen, self.device)}
+                           for _ in range(L)],
+                "embed": (torch.randn((cfg.vocab, d), generator=gen, device=self.device) * 0.02).to(dtype),
+                "lm_head": (torch.randn((cfg.vocab, d), generator=gen, device=self.device) * 0.02).to(dtype),
+            }
+        self.weights = weights
+        if dense:   # fp16 cuBLAS twin: the exact dequantized values (scale * trit is exact in fp16)
+            self.lin = [{k: w.dequantize(dtype) for k, w in lw.items()} for lw in weights["layers"]]
+        else:
+            self.lin = weights["layers"]
+        self.norm_attn = [torch.ones(d, device=self.device, dtype=dtype) for _ in range(L)]
+        self.norm_mlp = [torch.ones(d, device=self.device, dtype=dtype) for _ in range(L)]
+        self.norm_out = torch.ones(d, device=self.device, dtype=dtype)
+        H, D, S = cfg.n_heads, cfg.head_dim, cfg.max_seq
+        self.k_cache = torch.zeros((L, 1, H, S, D), device=self.device, dtype=dtype)
+        self.v_cache = torch.zeros((L, 1, H, S, D), device=self.device, dtype=dtype)
+        inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, D, 2, device=self.device).float() / D))
+        ang = torch.arange(S, device=self.device).float()[:, None] * inv[None, :]
+        self.cos, self.sin = ang.cos().to(dtype), ang.sin().to(dtype)
+        # device-resident decode state, advanced inside the captured graph
+        self.tok = torch.zeros(1, dtype=torch.long, device=self.device)
+        self.pos = torch.zeros(1, dtype=torch.long, device=self.device)
+        self.out_tokens = torch.zeros(S, dtype=torch.long, device=self.device)
+        self.graph = None
+
+    # -- building blocks ----------------------------------------------------------------
+    def _lin(self, x, w):
+        return F.linear(x, w) if self.dense else linear(x, w)
+
+    def _rms(self, x, wgt):
+        xf = x.float()
+        return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + self.cfg.eps)).to(self.dtype) * wgt
+
+    def _rope(self, x, pos):   # x [T, H, D], pos [T]
+        c, s = self.cos[pos][:, None, :], self.sin[pos][:, None, :]
+        x1, x2 = x[..., 0::2], x[..., 1::2]
+        return torch.stack((x1 * c - x2 * s, x1 * s + x2 * c), dim=-1).flatten(-2)
+
+    def _layer(self, i, h, pos, T):
+        cfg, lw = self.cfg, self.lin[i]
+        H, D, d = cfg.n_heads, cfg.head_dim, cfg.d_model
+        qkv = self._lin(self._rms(h, self.norm_attn[i]), lw["qkv"]).view(T, 3, H, D)
+        q, k, v = self._rope(qkv[:, 0], pos), self._rope(qkv[:, 1], pos), qkv[:, 2]
+        self.k_cache[i, 0].index_copy_(1, pos, k.transpose(0, 1))
+        self.v_cache[i, 0].index_copy_(1, pos, v.transpose(0, 1))
+        # attention over the static cache; positions after the query's are masked
+        keys = torch.arange(cfg.max_seq, device=self.device)
+        mask = keys[None, :] <= pos[:, None]                                  # [T, S]
+        att = F.scaled_dot_product_attention(q.transpose(0, 1)[None], self.k_cache[i], self.v_cache[i],
+                                             attn_mask=mask[None, None])      # [1, H, T, D]
+        h = h + self._lin(att[0].transpose(0, 1).reshape(T, d), lw["o"])
+        gu = self._lin(self._rms(h, self.norm_mlp[i]), lw["gate_up"])
+        g, u = gu[:, : cfg.d_ff], gu[:, cfg.d_ff:]
+        return h + self._lin(F.silu(g) * u, lw["down"])
+
+    def forward(self, tokens, pos):
+        """tokens [T] at positions pos [T] -> logits of the last position [vocab] (fills the cache)."""
+        T = tokens.shape[0]
+        h = self.weights["embed"][tokens]
+        for i in range(self.cfg.n_layers):
+            h = self._layer(i, h, pos, T)
+        h = self._rms(h[-1:], self.norm_out)
+        return F.linear(h, self.weights["lm_head"])[0]
+
+    # -- serving --------------------------------------------------------------------------
+    def prefill(self, prompt: torch.Tensor) -> None:
+        """Run the prompt (one batched pass: the tcgen05 GEMM path) and seed the decode state."""
+        T = prompt.shape[0]
+        logits = self.forward(prompt, torch.arange(T, device=self.device))
+        self.tok.copy_(logits.argmax().view(1))
+        self.pos.fill_(T)
+
+    def _decode_body(self):
+        logits = self.forward(self.tok, self.pos)
+        nxt = logits.argmax().view(1)
+        self.out_tokens.index_copy_(0, self.pos, nxt)
+        self.tok.copy_(nxt)
+        self.pos.add_(1)
+
+    def capture(self) -> None:
+        """Capture one greedy decode step (state advanced on the device) as a CUDA graph."""
+        s = torch.cuda.Stream(device=self.device)
+        saved = (self.tok.clone(), self.pos.clone(), self.k_cache.clone(), self.v_cache.clone())
+        with torch.cuda.stream(s):
+            self._decode_body()   # warm-up (lazy kernel set-up) outside capture
+            s.synchronize()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=s):
+                self._decode_body()
+        torch.cuda.synchronize(self.device)
+        self.tok.copy_(saved[0])
+        self.pos.copy_(saved[1])
+        self.k_cache.copy_(saved[2])
+        self.v_cache.copy_(saved[3])
+
+    def decode(self, n: int) -> None:
+        """n greedy decode steps as n graph replays (no host synchronisation)."""
+        if self.graph is None:
+            self.capture()
+        for _ in range(n):
+            self.graph.replay()
+
+    def reset(self) -> None:
+        self.k_cache.zero_()
+        self.v_cache.zero_()
+        self.tok.zero_()
+        self.pos.zero_()
