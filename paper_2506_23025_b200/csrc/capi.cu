@@ -30,7 +30,7 @@ int check_launch(const char* what) {
 int gemv_tq2(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
              int cols, int ctas, int pdl, cudaStream_t st);
 size_t gemv_workspace_bytes(int batch, int rows, int cols);
-int gemm_umma(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
+int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
               int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg);
 size_t umma_workspace_bytes(int batch, int rows, int cols);
 
@@ -48,7 +48,7 @@ const char* tr_last_error(void) { return g_err; }
 int tr_version(void) { return 1; }
 
 size_t tr_linear_workspace_size(int fmt, int64_t batch, int64_t rows, int64_t cols) {
-  if (fmt != kFmtTq2 || rows < 1 || cols < 1 || batch < 0) return 0;
+  if ((fmt != kFmtTq2 && fmt != kFmtTq1) || rows < 1 || cols < 1 || batch < 0) return 0;
   const size_t g = 256 * 1024 + gemv_workspace_bytes((int)(batch < 32 ? batch : 32), (int)rows, (int)cols);
   const size_t u = umma_workspace_bytes((int)(batch > 0 ? batch : 1), (int)rows, (int)cols);
   return g > u ? g : u;
@@ -57,7 +57,7 @@ size_t tr_linear_workspace_size(int fmt, int64_t batch, int64_t rows, int64_t co
 int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
               int act_dtype, int64_t ldx, int64_t ldy, int flags, void* workspace, size_t ws_bytes,
               void* stream) {
-  TR_REQUIRE(fmt == kFmtTq2, "tr_linear: fmt %d not supported by this entry point (TQ2=2)", fmt);
+  TR_REQUIRE(fmt == kFmtTq2 || fmt == kFmtTq1, "tr_linear: fmt must be TQ2 (2) or TQ1 (3), got %d", fmt);
   TR_REQUIRE(act_dtype == kActF16 || act_dtype == kActBf16, "tr_linear: act_dtype must be F16(1) or BF16(2)");
   TR_REQUIRE(rows >= 1 && cols >= 1 && batch >= 0, "tr_linear: bad shape batch=%lld rows=%lld cols=%lld",
              (long long)batch, (long long)rows, (long long)cols);
@@ -76,8 +76,13 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
     use_umma = true;
   }
   if (flags & TR_LINEAR_FORCE_GEMV) use_umma = false;
+  if (fmt == kFmtTq1) {   // 1.6-bit weights are decoded on the fly by the tensor-core kernel only
+    TR_REQUIRE(aligned, "tr_linear: TQ1 needs 16-byte aligned activation rows (ldx %% 8 == 0)");
+    TR_REQUIRE(!(flags & TR_LINEAR_FORCE_GEMV), "tr_linear: TQ1 has no mma.sync GEMV path");
+    use_umma = true;
+  }
   if (use_umma)
-    return gemm_umma(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, uniform, workspace,
+    return gemm_umma(fmt, act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, uniform, workspace,
                      ws_bytes, pdl, st, (flags >> 24) & 0xF);
   const size_t esz = 2;
   for (int64_t n0 = 0; n0 < batch; n0 += 32) {

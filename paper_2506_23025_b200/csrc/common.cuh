@@ -40,6 +40,23 @@ constexpr int kTileBlockBytes = 1024;
 constexpr int kTileScaleBytes = 32;
 constexpr int kUnitBytes = kTileBlockBytes + kTileScaleBytes;   // 1056
 
+// ---- T16-Q1 device layout for TQ1 (1.6 bit, 5 trits per byte) -------------------
+// Same tiling (16-row tiles x 256-column blocks, tile-major units, rows padded to 128),
+// unit = 16 rows x 52 payload bytes + the same 32 bytes of half2 scale pairs.  Row r of
+// a unit (bytes 52 r ..) holds 26 pair-groups: group g covers columns 10g .. 10g+9 as
+// byte A_g = base-3 code of the even columns (10g, +2, +4, +6, +8) and byte B_g = code
+// of the odd ones (10g+1, .. +9), MSB first, codes canonical (codec.py:180-200);
+// columns >= 256 (group 25's last two steps) are pad digits 1.  Placing A_g | B_g << 16
+// in one register, each Algorithm-1 step (p = 3s, digit = p >> 8, s = p & 0xFF) on both
+// 16-bit lanes at once yields the half2 of columns (10g + 2k, 10g + 2k + 1): natural-order
+// K pairs for the tensor core.  Same 54 B per 256 weights as the reference TQ1 block.
+constexpr int kQ1RowBytes = 52;
+constexpr int kQ1TileBlockBytes = 16 * kQ1RowBytes;              // 832
+constexpr int kQ1UnitBytes = kQ1TileBlockBytes + kTileScaleBytes;   // 864
+
+__host__ __device__ inline int unit_bytes(int fmt) { return fmt == 3 ? kQ1UnitBytes : kUnitBytes; }
+__host__ __device__ inline int tile_block_bytes(int fmt) { return fmt == 3 ? kQ1TileBlockBytes : kTileBlockBytes; }
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t rows_padded(int64_t rows) { return ceil_div(rows, kRowPad) * kRowPad; }
 

@@ -119,6 +119,45 @@ template <> struct Dec<__nv_bfloat16> {
   }
 };
 
+// TQ1 pair-group decode (layout in common.cuh): register A_g | B_g << 16, Algorithm-1 step
+// p = 3s on both 16-bit lanes, digit at bits 8..9 of each lane -> exact trit half2 of the
+// natural-order column pair (10g + 2k, 10g + 2k + 1).  Half 0 of a row writes TMEM columns
+// 0..63 (groups 0..11, group 12 steps 0..3), half 1 columns 64..127 (group 12 step 4,
+// groups 13..24, group 25 steps 0..2).
+template <typename T> __device__ __forceinline__ uint32_t q1_trit2(uint32_t p);
+template <> __device__ __forceinline__ uint32_t q1_trit2<__half>(uint32_t p) {
+  const uint32_t v = lop3_and_or(p, 0x03000300u, 0x64006400u);   // 1024 + 256 d
+  const __half2 r = __hfma2(*reinterpret_cast<const __half2*>(&v), __float2half2_rn(1.0f / 256.0f),
+                            __float2half2_rn(-5.0f));
+  return *reinterpret_cast<const uint32_t*>(&r);
+}
+template <> __device__ __forceinline__ uint32_t q1_trit2<__nv_bfloat16>(uint32_t p) {
+  const uint32_t v = lop3_and_or(p >> 8, 0x00030003u, 0x43004300u);   // 128 + d
+  const __nv_bfloat162 r = __hadd2(*reinterpret_cast<const __nv_bfloat162*>(&v), __float2bfloat162_rn(-129.0f));
+  return *reinterpret_cast<const uint32_t*>(&r);
+}
+template <typename T, int G0, int G1, int K0LAST, int KLAST, int C0>
+__device__ __forceinline__ void q1_groups(const uint32_t (&wq)[7], int wbase, uint32_t (&col)[64]) {
+  // groups G0..G1 (inclusive); group G0 contributes steps K0LAST.. only (first group of
+  // half 1), group G1 steps ..KLAST; columns from C0
+#pragma unroll
+  for (int g = G0; g <= G1; ++g) {
+    uint32_t s = __byte_perm(wq[(g >> 1) - wbase], 0u, (g & 1) ? 0x4342u : 0x4140u);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const uint32_t p = s * 3u;
+      const int c = C0 + 5 * (g - G0) + k - K0LAST;
+      if (!(g == G0 && k < K0LAST) && !(g == G1 && k > KLAST)) col[c] = q1_trit2<T>(p);
+      s = p & 0x00FF00FFu;
+    }
+  }
+}
+template <typename T>
+__device__ __forceinline__ void decode_q1(const uint32_t (&wq)[7], int half, uint32_t (&col)[64]) {
+  if (half == 0) q1_groups<T, 0, 12, 0, 3, 0>(wq, 0, col);     // cols 0..63
+  else q1_groups<T, 12, 25, 4, 2, 0>(wq, 6, col);              // cols 64..127 (as 0..63)
+}
+
 }  // namespace umma
 
 struct UmmaArgs {
@@ -134,14 +173,16 @@ struct UmmaArgs {
   int map3d;          // activations described by the 3-D tensor map (one TMA request per block)
 };
 
-template <typename T, int N>
+template <typename T, int N, int FMT>
 struct UmmaCfg {
+  static constexpr int UB = FMT == kFmtTq1 ? kQ1UnitBytes : kUnitBytes;   // bytes per 16x256 unit
+  static constexpr int TBB = FMT == kFmtTq1 ? kQ1TileBlockBytes : kTileBlockBytes;
   // TMA requests cost ~100 SM cycles each whatever their size, so the weights move in
   // stages of KS blocks (8 requests of KS x 1056 B) and the activations in one 3-D box per block
   static constexpr int KS = N <= 32 ? 4 : 2;                 // 256-blocks per weight stage
   static constexpr int RW = N <= 32 ? 4 : 3;                 // weight stages
   static constexpr int RB = N <= 32 ? 4 : N <= 64 ? 3 : 2;   // activation stages (one block each)
-  static constexpr int kStageWBytes = 8 * KS * kUnitBytes;   // 128 rows x KS blocks
+  static constexpr int kStageWBytes = 8 * KS * UB;          // 128 rows x KS blocks
   static constexpr int kStageBBytes = N * 512;               // N rows x 256 K (4 swizzled 64-K atoms)
   static constexpr int kMaxA = 3;                            // TMEM A buffers (128 columns = one block each)
   static constexpr size_t kBOff = 1024;                      // 1024-aligned for the 128B swizzle
@@ -167,11 +208,12 @@ __device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
   return r;
 }
 
-template <typename T, int N>
+template <typename T, int N, int FMT>
 __global__ void __launch_bounds__(umma::kThreads, 1)
     k_gemm_umma(const __grid_constant__ CUtensorMap tmx, const UmmaArgs a) {
   using namespace umma;
-  using Cfg = UmmaCfg<T, N>;
+  using Cfg = UmmaCfg<T, N, FMT>;
+  constexpr int UB = Cfg::UB;
   constexpr int KS = Cfg::KS, RW = Cfg::RW, RB = Cfg::RB;
   constexpr int kStageW = Cfg::kStageWBytes, kStageB = Cfg::kStageBBytes;
   extern __shared__ uint8_t smem_raw[];
@@ -237,14 +279,14 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmx) : "memory");
       const uint64_t pol = policy_evict_first();
-      const uint8_t* wbase = a.w + ((int64_t)mt * 8 * a.nb + kb0) * kUnitBytes;
+      const uint8_t* wbase = a.w + ((int64_t)mt * 8 * a.nb + kb0) * UB;
       auto issue_w = [&](int si) {   // weight stage si: blocks [si KS, si KS + c) of the CTA's 8 tiles
         const int s = si % RW, c = min(KS, nblk - si * KS);
-        mbar_expect_tx(&full_w[s], 8 * c * kUnitBytes);
+        mbar_expect_tx(&full_w[s], 8 * c * UB);
 #pragma unroll 1
         for (int t = 0; t < 8; ++t)
-          bulk_g2s(sW + s * kStageW + t * KS * kUnitBytes, wbase + ((int64_t)t * a.nb + si * KS) * kUnitBytes,
-                   c * kUnitBytes, &full_w[s], pol);
+          bulk_g2s(sW + s * kStageW + t * KS * UB, wbase + ((int64_t)t * a.nb + si * KS) * UB, c * UB, &full_w[s],
+                   pol);
       };
       auto issue_b = [&](int i) {
         const int s = i % RB;
@@ -309,7 +351,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
 #pragma unroll
     for (int i = 0; i < NH; ++i) acc[i] = 0.0f;
     float s_prev = 0.0f, s_first = 0.0f;
-    const uint32_t sW32 = smem_u32(sW) + tl * KS * kUnitBytes;
+    const uint32_t sW32 = smem_u32(sW) + tl * KS * UB;
 
     auto epilogue_block = [&](int i, float s) {        // acc += s * D_i (this thread's half of N)
       const int ab = i & 1;
@@ -331,11 +373,17 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
     for (int i = 0; i < nblk; ++i) {
       const int si = i / KS, j = i - si * KS, s = si % RW, ab = i % NA;
       if (j == 0) mbar_wait(&full_w[s], (si / RW) & 1);
-      const uint32_t unit = sW32 + s * kStageW + j * kUnitBytes;
+      const uint32_t unit = sW32 + s * kStageW + j * UB;
       uint4 wv[2];
+      uint32_t wq[7];
+      if constexpr (FMT == kFmtTq1) {
 #pragma unroll
-      for (int cc = 0; cc < 2; ++cc) wv[cc] = ld_shared_v4(unit + (hrow * 32 + (2 * half_k + cc) * 8 + g) * 16);
-      const uint32_t sv = ld_shared_u32(unit + kTileBlockBytes + g * 4);
+        for (int m = 0; m < 7; ++m) wq[m] = ld_shared_u32(unit + rt * kQ1RowBytes + (half_k * 6 + m) * 4);
+      } else {
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) wv[cc] = ld_shared_v4(unit + (hrow * 32 + (2 * half_k + cc) * 8 + g) * 16);
+      }
+      const uint32_t sv = ld_shared_u32(unit + Cfg::TBB + g * 4);
       const float s_cur = __half2float(hrow ? __high2half(*reinterpret_cast<const __half2*>(&sv))
                                             : __low2half(*reinterpret_cast<const __half2*>(&sv)));
       if (j == KS - 1 || i == nblk - 1) {               // weight stage fully read into registers
@@ -345,6 +393,14 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
       if (i == 0) s_first = s_cur;
       mbar_wait(&a_empty[ab], ((i / NA) & 1) ^ 1);      // MMA of block i-NA done with this A buffer
       tc_fence_after();
+      if constexpr (FMT == kFmtTq1) {
+        if (!(a.dbg & 2)) {
+          uint32_t col[64];
+          decode_q1<T>(wq, half_k, col);
+          tmem_st32(tA + lane_off + ab * 128 + half_k * 64, *reinterpret_cast<const uint32_t(*)[32]>(col));
+          tmem_st32(tA + lane_off + ab * 128 + half_k * 64 + 32, *reinterpret_cast<const uint32_t(*)[32]>(col + 32));
+        }
+      } else
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
         if (a.dbg & 2) break;
@@ -462,20 +518,20 @@ size_t umma_workspace_bytes(int batch, int rows, int cols) {
   return kUmmaCounterBytes + ws;
 }
 
-template <typename T, int N>
+template <typename T, int N, int FMT>
 static int launch_umma(const CUtensorMap& map, const UmmaArgs& a, int grid, int pdl, cudaStream_t st) {
-  auto kern = k_gemm_umma<T, N>;
+  auto kern = k_gemm_umma<T, N, FMT>;
   static int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured_dev != dev) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UmmaCfg<T, N>::kSmem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UmmaCfg<T, N, FMT>::kSmem);
     configured_dev = dev;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(umma::kThreads, 1, 1);
-  cfg.dynamicSmemBytes = UmmaCfg<T, N>::kSmem;
+  cfg.dynamicSmemBytes = UmmaCfg<T, N, FMT>::kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
   int na = 0;
@@ -494,7 +550,7 @@ static int launch_umma(const CUtensorMap& map, const UmmaArgs& a, int grid, int 
   return 0;
 }
 
-int gemm_umma(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
+int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
               int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg) {
   UmmaPlan p = plan_umma(batch, rows, cols, ks, sm_count());
   if ((ldx % 8) != 0 || ((uintptr_t)x & 15) != 0) {
@@ -553,12 +609,21 @@ int gemm_umma(int act, const void* w, const void* x, void* y, int64_t ldx, int64
   a.map3d = map3d;
   const int grid = p.m_tiles * p.n_tiles * p.ks;
   const bool bf = act == kActBf16;
+#define TR_UMMA_CASE(NN)                                                                              \
+  case NN:                                                                                            \
+    if (fmt == kFmtTq1)                                                                               \
+      return bf ? launch_umma<__nv_bfloat16, NN, kFmtTq1>(map, a, grid, pdl, st)                      \
+                : launch_umma<__half, NN, kFmtTq1>(map, a, grid, pdl, st);                            \
+    return bf ? launch_umma<__nv_bfloat16, NN, kFmtTq2>(map, a, grid, pdl, st)                        \
+              : launch_umma<__half, NN, kFmtTq2>(map, a, grid, pdl, st);
   switch (p.n) {
-    case 16: return bf ? launch_umma<__nv_bfloat16, 16>(map, a, grid, pdl, st) : launch_umma<__half, 16>(map, a, grid, pdl, st);
-    case 32: return bf ? launch_umma<__nv_bfloat16, 32>(map, a, grid, pdl, st) : launch_umma<__half, 32>(map, a, grid, pdl, st);
-    case 64: return bf ? launch_umma<__nv_bfloat16, 64>(map, a, grid, pdl, st) : launch_umma<__half, 64>(map, a, grid, pdl, st);
-    default: return bf ? launch_umma<__nv_bfloat16, 128>(map, a, grid, pdl, st) : launch_umma<__half, 128>(map, a, grid, pdl, st);
+    TR_UMMA_CASE(16)
+    TR_UMMA_CASE(32)
+    TR_UMMA_CASE(64)
+    default:
+    TR_UMMA_CASE(128)
   }
+#undef TR_UMMA_CASE
 }
 
 }  // namespace tr

@@ -80,6 +80,80 @@ __global__ void k_unrepack_tq2(const uint8_t* __restrict__ src, int64_t rows, in
   }
 }
 
+// ---- TQ1 <-> T16-Q1 -----------------------------------------------------------------
+__device__ __forceinline__ uint8_t enc5(const uint8_t* d, int stride) {   // codec.py:180-200
+  uint32_t n = 0;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) n = n * 3u + d[j * stride];
+  return (uint8_t)((n * 256u + 242u) / 243u);
+}
+__device__ __forceinline__ void dec5(uint32_t s, uint8_t* d, int stride) {   // Algorithm 1
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    const uint32_t p = s * 3u;
+    d[j * stride] = (uint8_t)(p >> 8);
+    s = p & 0xFFu;
+  }
+}
+
+// one thread per (padded row, block): reference codes -> digits -> pair-group codes
+__global__ void k_repack_tq1(const uint8_t* __restrict__ payload, const __half* __restrict__ scales, int64_t rows,
+                             int64_t nb, int64_t rows_pad, uint8_t* __restrict__ dst) {
+  const int64_t total = rows_pad * nb;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = q / nb, b = q % nb, t = row / 16;
+    const int rt = (int)(row % 16);
+    uint8_t d[260];
+    if (row < rows) {
+      const uint8_t* src = payload + (row * nb + b) * kTq1Payload;
+      for (int c = 0; c < kTq1Payload; ++c) dec5(src[c], d + 5 * c, 1);
+    } else {
+      for (int i = 0; i < 260; ++i) d[i] = 1;
+    }
+    for (int i = 256; i < 260; ++i) d[i] = 1;   // pad digits (blocks.py:154-158)
+    uint8_t* unit = dst + (t * nb + b) * kQ1UnitBytes;
+    uint8_t* out = unit + rt * kQ1RowBytes;
+    for (int g = 0; g < 26; ++g) {
+      uint8_t ev[5], od[5];
+      for (int k = 0; k < 5; ++k) {
+        const int ce = 10 * g + 2 * k, co = ce + 1;
+        ev[k] = ce < 256 ? d[ce] : 1;
+        od[k] = co < 256 ? d[co] : 1;
+      }
+      out[2 * g] = enc5(ev, 1);
+      out[2 * g + 1] = enc5(od, 1);
+    }
+    const __half s = row < rows ? scales[row * nb + b] : __ushort_as_half(0);
+    reinterpret_cast<__half*>(unit + kQ1TileBlockBytes)[2 * (rt & 7) + (rt >> 3)] = s;
+  }
+}
+
+// inverse: one thread per (row, block): pair-group codes -> digits -> reference codes
+__global__ void k_unrepack_tq1(const uint8_t* __restrict__ src, int64_t rows, int64_t nb,
+                               uint8_t* __restrict__ payload, __half* __restrict__ scales) {
+  const int64_t total = rows * nb;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = q / nb, b = q % nb, t = row / 16;
+    const int rt = (int)(row % 16);
+    const uint8_t* unit = src + (t * nb + b) * kQ1UnitBytes;
+    const uint8_t* in = unit + rt * kQ1RowBytes;
+    uint8_t d[260];
+    for (int g = 0; g < 26; ++g) {
+      uint8_t ev[5], od[5];
+      dec5(in[2 * g], ev, 1);
+      dec5(in[2 * g + 1], od, 1);
+      for (int k = 0; k < 5; ++k) {
+        d[10 * g + 2 * k] = ev[k];
+        d[10 * g + 2 * k + 1] = od[k];
+      }
+    }
+    for (int i = 256; i < 260; ++i) d[i] = 1;
+    uint8_t* out = payload + (row * nb + b) * kTq1Payload;
+    for (int c = 0; c < kTq1Payload; ++c) out[c] = enc5(d + 5 * c, 1);
+    scales[row * nb + b] = reinterpret_cast<const __half*>(unit + kQ1TileBlockBytes)[2 * (rt & 7) + (rt >> 3)];
+  }
+}
+
 }  // namespace tr
 
 using namespace tr;
@@ -90,13 +164,22 @@ int64_t tr_layout_bytes(int fmt, int64_t rows, int64_t cols) {
   if (rows < 1 || cols < 1) return -1;
   int64_t nb = ceil_div(cols, kBlock), n_tiles = rows_padded(rows) / 16;
   if (fmt == kFmtTq2) return nb * n_tiles * kUnitBytes;
+  if (fmt == kFmtTq1) return nb * n_tiles * kQ1UnitBytes;
   return -1;
 }
 
 int tr_repack(int fmt, const uint8_t* payload, const uint16_t* scales_f16, int64_t rows, int64_t cols, void* dst,
               void* stream) {
-  TR_REQUIRE(fmt == kFmtTq2, "tr_repack: only TQ2 (2) uses the T16 layout, got fmt %d", fmt);
+  TR_REQUIRE(fmt == kFmtTq2 || fmt == kFmtTq1, "tr_repack: fmt must be TQ2 (2) or TQ1 (3), got %d", fmt);
   TR_REQUIRE(rows >= 1 && cols >= 1, "tr_repack: matrix must be non-empty");
+  if (fmt == kFmtTq1) {
+    TR_REQUIRE(((uintptr_t)dst & 15) == 0, "tr_repack: misaligned buffers");
+    const int64_t nb = ceil_div(cols, kBlock), rp = rows_padded(rows);
+    const int grid = (int)(ceil_div(rp * nb, 128) > 148 * 32 ? 148 * 32 : ceil_div(rp * nb, 128));
+    k_repack_tq1<<<grid, 128, 0, (cudaStream_t)stream>>>(payload, (const __half*)scales_f16, rows, nb, rp,
+                                                         (uint8_t*)dst);
+    return check_launch("tr_repack(tq1)");
+  }
   TR_REQUIRE(((uintptr_t)payload & 3) == 0 && ((uintptr_t)dst & 15) == 0, "tr_repack: misaligned buffers");
   int64_t nb = ceil_div(cols, kBlock), n_tiles = rows_padded(rows) / 16;
   int64_t total = nb * n_tiles * 256;
@@ -108,8 +191,15 @@ int tr_repack(int fmt, const uint8_t* payload, const uint16_t* scales_f16, int64
 
 int tr_unrepack(int fmt, const void* src, int64_t rows, int64_t cols, uint8_t* payload, uint16_t* scales_f16,
                 void* stream) {
-  TR_REQUIRE(fmt == kFmtTq2, "tr_unrepack: only TQ2 (2) uses the T16 layout, got fmt %d", fmt);
+  TR_REQUIRE(fmt == kFmtTq2 || fmt == kFmtTq1, "tr_unrepack: fmt must be TQ2 (2) or TQ1 (3), got %d", fmt);
   TR_REQUIRE(rows >= 1 && cols >= 1, "tr_unrepack: matrix must be non-empty");
+  if (fmt == kFmtTq1) {
+    const int64_t nb = ceil_div(cols, kBlock);
+    const int grid = (int)(ceil_div(rows * nb, 128) > 148 * 32 ? 148 * 32 : ceil_div(rows * nb, 128));
+    k_unrepack_tq1<<<grid, 128, 0, (cudaStream_t)stream>>>((const uint8_t*)src, rows, nb, payload,
+                                                           (__half*)scales_f16);
+    return check_launch("tr_unrepack(tq1)");
+  }
   int64_t nb = ceil_div(cols, kBlock), n_tiles = rows_padded(rows) / 16;
   int64_t total = rows * nb * 16;
   int grid = (int)(ceil_div(total, 256) > 148 * 64 ? 148 * 64 : ceil_div(total, 256));

@@ -350,3 +350,54 @@ def test_decoder_ternary_matches_dense_twin(tp):
     tern.prefill(prompt)
     tern.decode(5)   # graph-captured greedy steps advance the device-side state
     assert int(tern.pos) == 17
+
+
+# ---------------------------------------------------------------- TQ1 (1.6-bit) decoded on the fly (config 4)
+
+@pytest.mark.parametrize("rows,cols", [(1, 5), (37, 1500), (128, 256), (300, 1000), (8192, 8192)])
+def test_tq1_repack_roundtrip(tp, rows, cols):
+    rng = np.random.default_rng(rows * 3 + cols)
+    W = (rng.normal(size=(rows, cols)) * rng.choice([0.0, 1.0], size=(rows, cols), p=[0.2, 0.8])).astype(np.float32)
+    payload, scales = orc.pack_matrix(W, orc.TQ1)          # canonical reference TQ1 codes
+    pd = torch.from_numpy(payload).cuda()
+    sd = torch.from_numpy(scales.view(np.uint16)).view(torch.float16).cuda()
+    w = tp.TernaryWeight.from_device_packed(pd, sd, rows, cols, tp.DType.TQ1)
+    assert w.data.numel() == -(-rows // 128) * 128 // 16 * (-(-cols // 256)) * 864
+    p2, s2 = w.unpack()
+    assert torch.equal(p2, pd)
+    assert torch.equal(s2.view(torch.int16), sd.view(torch.int16))
+    dense = w.dequantize(torch.float16).float().cpu().numpy()
+    np.testing.assert_array_equal(dense, orc.dequantize_matrix(payload, scales, cols, orc.TQ1, np.float32))
+
+
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
+@pytest.mark.parametrize("rows,cols", [(128, 256), (300, 1000), (640, 8192)])
+@pytest.mark.parametrize("batch", [1, 8, 40])
+@pytest.mark.parametrize("per_block", [False, True])
+def test_tq1_linear_vs_oracle(tp, dtype, rows, cols, batch, per_block):
+    tdt = getattr(torch, dtype)
+    rng = np.random.default_rng(rows + 5 * cols + 11 * batch + per_block)
+    T = (rng.integers(0, 3, size=(rows, cols)) - 1).astype(np.float32)
+    gam = np.float16(0.02 * (1 + rng.uniform(0, 1, size=(rows, 1)))).astype(np.float32)
+    W = gam * T
+    if per_block:
+        f = rng.choice([1.0, 0.5, 0.25], size=(rows, -(-cols // 256))).astype(np.float32)
+        W = W * np.repeat(f, 256, axis=1)[:, :cols]
+    payload, scales = orc.pack_matrix(W, orc.TQ1)
+    pm = tp.PackedMatrix(rows=rows, cols=cols, fmt=tp.DType.TQ1, payload=payload, scales=scales)
+    w = pm.to_device()
+    x = torch.from_numpy(rng.uniform(-1, 1, size=(batch, cols)).astype(np.float32)).to(tdt).cuda()
+    y = tp.linear(x, w).float().cpu().numpy()
+    ref = _oracle_ref(payload, scales, cols, orc.TQ1, x.float().cpu().numpy())
+    err = rel_err(y, ref)
+    assert err <= (2e-3 if dtype == "float16" else 6e-3), err
+
+
+def test_tq1_matches_tq2_same_trits(tp):
+    # the same trits packed both ways give the same products (both paths exact in the products)
+    rng = np.random.default_rng(12)
+    W = (0.03 * (rng.integers(0, 3, size=(512, 4096)) - 1)).astype(np.float32)
+    x = (torch.rand(16, 4096, device="cuda") * 2 - 1).half()
+    y1 = tp.linear(x, tp.pack_matrix(W, tp.DType.TQ1).to_device())
+    y2 = tp.linear(x, tp.pack_matrix(W, tp.DType.TQ2).to_device(), path="umma")
+    assert torch.equal(y1, y2)
