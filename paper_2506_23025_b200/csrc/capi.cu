@@ -33,6 +33,7 @@ size_t gemv_workspace_bytes(int batch, int rows, int cols);
 int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
               int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg);
 size_t umma_workspace_bytes(int batch, int rows, int cols);
+bool gemv_stages_x(int batch, int rows, int cols);
 
 // batch at which the tensor-core (tcgen05) GEMM takes over from the mma.sync GEMV
 constexpr int64_t kUmmaMinBatch = 9;
@@ -70,7 +71,9 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
   const int knob = (flags >> 8) & 0xFFFF;   // GEMV: CTA count; UMMA: K split (0 = automatic)
   cudaStream_t st = (cudaStream_t)stream;
   const bool aligned = (ldx % 8) == 0 && ((uintptr_t)x & 15) == 0;
-  bool use_umma = batch >= kUmmaMinBatch && aligned;
+  // measured crossover (scripts/dev/gemv_sweep.py): the mma.sync GEMV wins at batch 1-2 and,
+  // while it can stage the activations in shared memory, up to 8; the tensor-core GEMM beyond
+  bool use_umma = aligned && (batch >= kUmmaMinBatch || (batch >= 3 && !gemv_stages_x((int)batch, (int)rows, (int)cols)));
   if (flags & TR_LINEAR_FORCE_UMMA) {
     TR_REQUIRE(aligned, "tr_linear: the tensor-core path needs 16-byte aligned activation rows");
     use_umma = true;

@@ -450,11 +450,35 @@ static int launch_gemv_x(const GemvArgs& a, int grid, int pdl, cudaStream_t st) 
   return 0;
 }
 
+template <int NT>
+static size_t gemv_smem(const GemvArgs& a, int grid, bool xs) {
+  using Cfg = GemvCfg<NT>;
+  const int nrx = a.batch < 8 * NT ? a.batch : 8 * NT;
+  const int tiles_max = (int)ceil_div(a.n_tiles, grid);
+  const int ops = (int)ceil_div(ceil_div((int64_t)tiles_max * a.nb, Cfg::kWarps), Cfg::kSU);
+  const int ns_max = kNSMax * 2 / Cfg::kSU;
+  const int ns = ops >= ns_max ? ns_max : ops > 1 ? 2 : 1;
+  return Cfg::smem(a.nb, nrx, xs, ns);
+}
+
 template <typename T, int NT>
 static int launch_gemv(const GemvArgs& a, int grid, int pdl, cudaStream_t st) {
   const int nrx = a.batch < 8 * NT ? a.batch : 8 * NT;
-  if ((size_t)nrx * GemvCfg<NT>::x_stride(a.nb) <= kXsBudget) return launch_gemv_x<T, NT, true>(a, grid, pdl, st);
+  if ((size_t)nrx * GemvCfg<NT>::x_stride(a.nb) <= kXsBudget && gemv_smem<NT>(a, grid, true) <= 227 * 1024)
+    return launch_gemv_x<T, NT, true>(a, grid, pdl, st);
   return launch_gemv_x<T, NT, false>(a, grid, pdl, st);
+}
+
+// true when the GEMV can stage this batch's activations in shared memory (its fast path)
+bool gemv_stages_x(int batch, int rows, int cols) {
+  GemvArgs a = {};
+  a.nb = (int)ceil_div(cols, kBlock);
+  a.n_tiles = (int)ceil_div(rows, 16);
+  a.batch = batch;
+  int grid = sm_count() < a.n_tiles ? sm_count() : a.n_tiles;
+  if (batch <= 8)
+    return (size_t)batch * GemvCfg<1>::x_stride(a.nb) <= kXsBudget && gemv_smem<1>(a, grid, true) <= 227 * 1024;
+  return false;
 }
 
 int gemv_tq2(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,

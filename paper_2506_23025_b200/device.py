@@ -147,8 +147,8 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
         out = torch.empty((*lead, w.rows), dtype=x.dtype, device=x.device)
     y2 = out.view(-1, w.rows)
     flags = (_lib.LINEAR_PDL if pdl else 0) | (_lib.LINEAR_UNIFORM_SCALE if w.uniform_scale else 0) | _PATHS[path]
-    umma = path == "umma" or (path == "auto" and batch >= 9) or w.fmt is DType.TQ1   # TQ1: tensor-core path only
-    flags |= ((int(ksplit if umma else ctas)) & 0xFFFF) << 8
+    # one knob: the GEMV's CTA count or the tensor-core GEMM's K split, whichever path runs
+    flags |= ((int(ksplit or ctas)) & 0xFFFF) << 8
     flags |= (int(_probe) & 0xF) << 24   # development probes (see csrc); 0 in production
     need = _lib.lib().tr_linear_workspace_size(int(w.fmt), batch, w.rows, w.cols)
     if ws is None:
