@@ -104,6 +104,23 @@ TR_API int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t bat
                      int act_dtype, int64_t ldx, int64_t ldy, int flags, void* workspace, size_t ws_bytes,
                      void* stream);
 
+/* ---- decoder-layer glue (configs[2] decode stack; no reference analogue) ---------- */
+
+/* h[r] += delta[r] (delta may be NULL); y[r] = h[r] * rsqrt(mean(h[r]^2) + eps) * w; rows x d */
+TR_API int tr_add_rmsnorm(int act_dtype, void* h, const void* delta, const void* w, void* y, int64_t rows,
+                          int64_t d, float eps, void* stream);
+/* qkv [T,3,H,D] -> rotary q [T,H,D]; rotary k and v appended to k/v caches [H,S,D] at pos[t] (int64, device) */
+TR_API int tr_rope_kv(int act_dtype, const void* qkv, const int64_t* pos, const void* cos_t, const void* sin_t,
+                      void* q, void* k_cache, void* v_cache, int64_t tokens, int64_t heads, int64_t head_dim,
+                      int64_t max_seq, void* stream);
+/* one decode token, fused: rotary q/k of qkv [3,H,D] at pos[0], k/v appended to the caches
+ * [H,S,D], out [H,D] = softmax(q k^T scale over keys 0..pos[0]) v  (head_dim 128, S <= 128) */
+TR_API int tr_attn_decode(int act_dtype, const void* qkv, const int64_t* pos, const void* cos_t, const void* sin_t,
+                          void* k_cache, void* v_cache, void* out, int64_t heads, int64_t head_dim, int64_t max_seq,
+                          float scale, void* stream);
+/* gu [T, 2F] = (gate | up) -> out [T, F] = silu(gate) * up */
+TR_API int tr_silu_mul(int act_dtype, const void* gu, void* out, int64_t tokens, int64_t ff, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

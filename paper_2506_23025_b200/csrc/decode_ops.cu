@@ -1,0 +1,336 @@
+// Decoder-layer glue around the ternary linears (BASELINE configs[2]):
+// one kernel each for residual-add + RMSNorm, rotary embedding + KV-cache append,
+// single-token attention over the cache, and SwiGLU.  These are not part of the reference
+// package (it has no model code); they exist so a decode step is ~8 launches per layer
+// instead of ~50 PyTorch ops, and are used identically by the ternary model and its fp16
+// cuBLAS twin (decoder.py).  All are HBM/latency-trivial: a few KB per launch.
+#include "common.cuh"
+
+namespace tr {
+
+template <typename T> __device__ __forceinline__ float to_f(T v);
+template <> __device__ __forceinline__ float to_f<__half>(__half v) { return __half2float(v); }
+template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  float s = 0.0f;
+  for (int i = 0; i < nw; ++i) s += red[i];   // fixed order: deterministic
+  return s;
+}
+
+// h[r] += delta[r] (if delta); y[r] = h[r] * rsqrt(mean(h[r]^2) + eps) * w   (one CTA per row)
+// Latency-bound (a 3072-wide row is 6 KB): every thread issues its 16-byte loads of h,
+// delta and w up front, then one block reduction.
+template <typename T>
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+  const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = to_f(e[i]);
+}
+template <typename T>
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 v;
+  T* e = reinterpret_cast<T*>(&v);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) e[i] = Act<T>::from_float(f[i]);
+  return v;
+}
+
+template <typename T, int V>   // V: 8-element vectors per thread
+__global__ void k_add_rmsnorm(T* __restrict__ h, const T* __restrict__ delta, const T* __restrict__ w,
+                              T* __restrict__ y, int d, float eps) {
+  griddep_wait();   // PDL: inputs come from the previous kernel
+  griddep_launch_dependents();
+  __shared__ float red[32];
+  uint4* hr = reinterpret_cast<uint4*>(h + (int64_t)blockIdx.x * d);
+  const uint4* dr = delta ? reinterpret_cast<const uint4*>(delta + (int64_t)blockIdx.x * d) : nullptr;
+  uint4* yr = reinterpret_cast<uint4*>(y + (int64_t)blockIdx.x * d);
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  const int nv = d / 8;
+  uint4 hv[V], dv[V], wv[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int i = threadIdx.x + j * blockDim.x;
+    if (i < nv) {
+      hv[j] = hr[i];
+      wv[j] = wr[i];
+      if (dr) dv[j] = dr[i];
+    }
+  }
+  float ss = 0.0f;
+  float hf[V][8];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int i = threadIdx.x + j * blockDim.x;
+    if (i < nv) {
+      unpack8<T>(hv[j], hf[j]);
+      if (dr) {
+        float df[8];
+        unpack8<T>(dv[j], df);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) hf[j][e] += df[e];
+        hv[j] = pack8<T>(hf[j]);
+        hr[i] = hv[j];
+        unpack8<T>(hv[j], hf[j]);   // the stored (rounded) residual is what the next layer sees
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ss += hf[j][e] * hf[j][e];
+    }
+  }
+  const float inv = rsqrtf(block_sum(ss, red) / d + eps);
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int i = threadIdx.x + j * blockDim.x;
+    if (i < nv) {
+      float wf[8], o[8];
+      unpack8<T>(wv[j], wf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = to_f(Act<T>::from_float(hf[j][e] * inv)) * wf[e];
+      yr[i] = pack8<T>(o);
+    }
+  }
+}
+
+// qkv [T, 3, H, D] -> q [T, H, D] (rotated); rotated k and v written to the caches
+// [H, S, D] at position pos[t].  Interleaved pairs (2i, 2i+1), angle cos/sin [S, D/2].
+template <typename T>
+__global__ void k_rope_kv(const T* __restrict__ qkv, const int64_t* __restrict__ pos, const T* __restrict__ cs,
+                          const T* __restrict__ sn, T* __restrict__ q, T* __restrict__ kc, T* __restrict__ vc,
+                          int H, int D, int S) {
+  griddep_wait();   // PDL: inputs come from the previous kernel
+  griddep_launch_dependents();
+  const int t = blockIdx.y, hh = blockIdx.x;
+  const int64_t p = pos[t];
+  const T* base = qkv + (int64_t)t * 3 * H * D;
+  for (int i = threadIdx.x; i < D / 2; i += blockDim.x) {
+    const float c = to_f(cs[p * (D / 2) + i]), s = to_f(sn[p * (D / 2) + i]);
+    const float q1 = to_f(base[hh * D + 2 * i]), q2 = to_f(base[hh * D + 2 * i + 1]);
+    const float k1 = to_f(base[(H + hh) * D + 2 * i]), k2 = to_f(base[(H + hh) * D + 2 * i + 1]);
+    T* qo = q + ((int64_t)t * H + hh) * D;
+    qo[2 * i] = Act<T>::from_float(q1 * c - q2 * s);
+    qo[2 * i + 1] = Act<T>::from_float(q1 * s + q2 * c);
+    T* ko = kc + ((int64_t)hh * S + p) * D;
+    ko[2 * i] = Act<T>::from_float(k1 * c - k2 * s);
+    ko[2 * i + 1] = Act<T>::from_float(k1 * s + k2 * c);
+    T* vo = vc + ((int64_t)hh * S + p) * D;
+    vo[2 * i] = base[(2 * H + hh) * D + 2 * i];
+    vo[2 * i + 1] = base[(2 * H + hh) * D + 2 * i + 1];
+  }
+}
+
+// One decode token, fused: rotary q/k of head hh from qkv [3, H, D], k/v appended to the
+// caches [H, S, D] at pos, then out[hh] = softmax(q k^T * scale over keys 0..pos) v.
+// One CTA (128 threads) per head; thread t scores key t with 16-byte loads issued up front,
+// the value sum is split over the 4 warps (lanes cover D) and combined in fixed order.
+template <typename T, int D>
+__global__ void __launch_bounds__(128) k_attn_decode(const T* __restrict__ qkv, const int64_t* __restrict__ pos,
+                                                     const T* __restrict__ cs, const T* __restrict__ sn,
+                                                     T* __restrict__ kc, T* __restrict__ vc, T* __restrict__ out,
+                                                     int H, int S, float scale) {
+  griddep_wait();
+  griddep_launch_dependents();
+  static_assert(D == 128, "one key per thread, 4 dims per lane");
+  __shared__ float qs[D];
+  __shared__ float sc[128];
+  __shared__ float part[4][D];
+  __shared__ float red[32];
+  const int hh = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int p = (int)pos[0], n = p + 1;
+  // rotary embedding of this token's q and k; k and v into the caches
+  if (tid < D / 2) {
+    const float c = to_f(cs[(int64_t)p * (D / 2) + tid]), s = to_f(sn[(int64_t)p * (D / 2) + tid]);
+    const float q1 = to_f(qkv[hh * D + 2 * tid]), q2 = to_f(qkv[hh * D + 2 * tid + 1]);
+    const float k1 = to_f(qkv[(H + hh) * D + 2 * tid]), k2 = to_f(qkv[(H + hh) * D + 2 * tid + 1]);
+    qs[2 * tid] = to_f(Act<T>::from_float(q1 * c - q2 * s));
+    qs[2 * tid + 1] = to_f(Act<T>::from_float(q1 * s + q2 * c));
+    T* ko = kc + ((int64_t)hh * S + p) * D;
+    ko[2 * tid] = Act<T>::from_float(k1 * c - k2 * s);
+    ko[2 * tid + 1] = Act<T>::from_float(k1 * s + k2 * c);
+    T* vo = vc + ((int64_t)hh * S + p) * D;
+    vo[2 * tid] = qkv[(2 * H + hh) * D + 2 * tid];
+    vo[2 * tid + 1] = qkv[(2 * H + hh) * D + 2 * tid + 1];
+  }
+  __threadfence_block();
+  __syncthreads();
+  // scores: thread tid <-> key tid
+  float v = -INFINITY;
+  if (tid < n) {
+    const uint4* kr = reinterpret_cast<const uint4*>(kc + ((int64_t)hh * S + tid) * D);
+    uint4 kv[D / 8];
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) kv[j] = kr[j];
+    float acc = 0.0f;
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) {
+      float kf[8];
+      unpack8<T>(kv[j], kf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc += qs[8 * j + e] * kf[e];
+    }
+    v = acc * scale;
+  }
+  float m = v;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  m = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  const float e = tid < n ? __expf(v - m) : 0.0f;
+  sc[tid] = e;
+  const float z = block_sum(e, red);   // (syncs; sc visible afterwards)
+  // value sum: warp w takes keys w, w+4, ...; lane covers dims 4 lane .. 4 lane + 3
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  for (int s0 = warp; s0 < n; s0 += 16) {
+    uint2 vv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int s = s0 + 4 * u;
+      vv[u] = s < n ? *reinterpret_cast<const uint2*>(vc + ((int64_t)hh * S + s) * D + 4 * lane) : make_uint2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int s = s0 + 4 * u;
+      if (s < n) {
+        const T* ve = reinterpret_cast<const T*>(&vv[u]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] += sc[s] * to_f(ve[q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) part[warp][4 * lane + q] = acc[q];
+  __syncthreads();
+  const float r = ((part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid])) / z;
+  out[(int64_t)hh * D + tid] = Act<T>::from_float(r);
+}
+
+// gu [T, 2F] = (gate | up) -> out [T, F] = silu(gate) * up   (8 elements per thread)
+template <typename T>
+__global__ void k_silu_mul(const T* __restrict__ gu, T* __restrict__ out, int F, int64_t n8) {
+  griddep_wait();   // PDL: inputs come from the previous kernel
+  griddep_launch_dependents();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = (i * 8) / F, f = (i * 8) % F;
+    float g[8], u[8], o[8];
+    unpack8<T>(*reinterpret_cast<const uint4*>(gu + t * 2 * F + f), g);
+    unpack8<T>(*reinterpret_cast<const uint4*>(gu + t * 2 * F + F + f), u);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = to_f(Act<T>::from_float(g[e] / (1.0f + __expf(-g[e])))) * u[e];
+    *reinterpret_cast<uint4*>(out + t * F + f) = pack8<T>(o);
+  }
+}
+
+// launch with programmatic dependent launch so chained decode kernels overlap their
+// launch latency (the kernels call griddepcontrol.wait before touching their inputs)
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+}  // namespace tr
+
+using namespace tr;
+
+#define TR_ACT_DISPATCH(act, KCALL_H, KCALL_B)                                            \
+  do {                                                                                     \
+    if ((act) == kActF16) {                                                                \
+      KCALL_H;                                                                             \
+    } else if ((act) == kActBf16) {                                                        \
+      KCALL_B;                                                                             \
+    } else {                                                                               \
+      TR_REQUIRE(false, "act_dtype must be F16(1) or BF16(2), got %d", (act));            \
+    }                                                                                      \
+  } while (0)
+
+extern "C" {
+
+int tr_add_rmsnorm(int act, void* h, const void* delta, const void* w, void* y, int64_t rows, int64_t d, float eps,
+                   void* stream) {
+  TR_REQUIRE(rows >= 0 && d >= 8 && (d % 8) == 0 && d <= 4 * 8 * 1024, "tr_add_rmsnorm: d must be a multiple of 8");
+  if (rows == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nv = (int)(d / 8);
+  const int threads = nv <= 1024 ? ((nv + 31) / 32) * 32 : 1024;
+  const int V = (int)ceil_div(nv, threads);
+  cudaError_t e = cudaSuccess;
+#define TR_RMS(TT, VV) e = launch_pdl(k_add_rmsnorm<TT, VV>, dim3((int)rows), dim3(threads), 0, st, (TT*)h, \
+                                      (const TT*)delta, (const TT*)w, (TT*)y, (int)d, eps)
+  if (act == kActF16) {
+    if (V == 1) TR_RMS(__half, 1); else if (V == 2) TR_RMS(__half, 2); else TR_RMS(__half, 4);
+  } else if (act == kActBf16) {
+    if (V == 1) TR_RMS(__nv_bfloat16, 1); else if (V == 2) TR_RMS(__nv_bfloat16, 2); else TR_RMS(__nv_bfloat16, 4);
+  } else {
+    TR_REQUIRE(false, "tr_add_rmsnorm: act_dtype must be F16(1) or BF16(2)");
+  }
+#undef TR_RMS
+  (void)e;
+  return check_launch("tr_add_rmsnorm");
+}
+
+int tr_rope_kv(int act, const void* qkv, const int64_t* pos, const void* cos_t, const void* sin_t, void* q,
+               void* k_cache, void* v_cache, int64_t tokens, int64_t heads, int64_t head_dim, int64_t max_seq,
+               void* stream) {
+  TR_REQUIRE(tokens >= 0 && heads >= 1 && head_dim >= 2 && (head_dim % 2) == 0, "tr_rope_kv: bad shape");
+  if (tokens == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 grid((unsigned)heads, (unsigned)tokens);
+  TR_ACT_DISPATCH(act,
+                  (launch_pdl(k_rope_kv<__half>, grid, dim3(64), 0, st, (const __half*)qkv, pos, (const __half*)cos_t,
+                                                          (const __half*)sin_t, (__half*)q, (__half*)k_cache,
+                                                          (__half*)v_cache, (int)heads, (int)head_dim, (int)max_seq)),
+                  (launch_pdl(k_rope_kv<__nv_bfloat16>, grid, dim3(64), 0, st, 
+                      (const __nv_bfloat16*)qkv, pos, (const __nv_bfloat16*)cos_t, (const __nv_bfloat16*)sin_t,
+                      (__nv_bfloat16*)q, (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, (int)heads,
+                      (int)head_dim, (int)max_seq)));
+  return check_launch("tr_rope_kv");
+}
+
+int tr_attn_decode(int act, const void* qkv, const int64_t* pos, const void* cos_t, const void* sin_t,
+                   void* k_cache, void* v_cache, void* out, int64_t heads, int64_t head_dim, int64_t max_seq,
+                   float scale, void* stream) {
+  TR_REQUIRE(head_dim == 128, "tr_attn_decode: head_dim must be 128");
+  TR_REQUIRE(heads >= 1 && max_seq >= 1 && max_seq <= 128, "tr_attn_decode: 1 <= max_seq <= 128");
+  cudaStream_t st = (cudaStream_t)stream;
+  TR_ACT_DISPATCH(act,
+                  (launch_pdl(k_attn_decode<__half, 128>, dim3((int)heads), dim3(128), 0, st, (const __half*)qkv,
+                              pos, (const __half*)cos_t, (const __half*)sin_t, (__half*)k_cache, (__half*)v_cache,
+                              (__half*)out, (int)heads, (int)max_seq, scale)),
+                  (launch_pdl(k_attn_decode<__nv_bfloat16, 128>, dim3((int)heads), dim3(128), 0, st,
+                              (const __nv_bfloat16*)qkv, pos, (const __nv_bfloat16*)cos_t,
+                              (const __nv_bfloat16*)sin_t, (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache,
+                              (__nv_bfloat16*)out, (int)heads, (int)max_seq, scale)));
+  return check_launch("tr_attn_decode");
+}
+
+int tr_silu_mul(int act, const void* gu, void* out, int64_t tokens, int64_t ff, void* stream) {
+  TR_REQUIRE(tokens >= 0 && ff >= 8 && (ff % 8) == 0, "tr_silu_mul: ff must be a multiple of 8");
+  const int64_t n8 = tokens * ff / 8;
+  if (n8 == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int grid = (int)(ceil_div(n8, 256) > 148 * 8 ? 148 * 8 : ceil_div(n8, 256));
+  TR_ACT_DISPATCH(act,
+                  (launch_pdl(k_silu_mul<__half>, dim3(grid), dim3(256), 0, st, (const __half*)gu, (__half*)out,
+                              (int)ff, n8)),
+                  (launch_pdl(k_silu_mul<__nv_bfloat16>, dim3(grid), dim3(256), 0, st, (const __nv_bfloat16*)gu,
+                              (__nv_bfloat16*)out, (int)ff, n8)));
+  return check_launch("tr_silu_mul");
+}
+
+}  // extern "C"

