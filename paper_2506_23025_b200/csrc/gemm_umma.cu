@@ -451,11 +451,22 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
         __threadfence();
         const float* base = a.ws + (int64_t)tile_mn * a.ks * (kRowsPerCta * N);
         if (row < a.rows)
-          for (int e = 0; e < NH; ++e) {
-            const int idx = (half_k * NH + e) * kRowsPerCta + r;
-            float v = 0.0f;
-            for (int q = 0; q < a.ks; ++q) v += __ldcg(base + (int64_t)q * kRowsPerCta * N + idx);
-            if (n0 + e < a.batch) y[(int64_t)(n0 + e) * a.ldy + row] = Act<T>::from_float(v);
+#pragma unroll
+          for (int e0 = 0; e0 < NH; e0 += 8) {   // 8 independent loads in flight per slice
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = 0.0f;
+            for (int q = 0; q < a.ks; ++q) {
+              const float* src = base + (int64_t)q * kRowsPerCta * N + (half_k * NH + e0) * kRowsPerCta + r;
+              float u[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) u[e] = __ldcg(src + e * kRowsPerCta);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[e] += u[e];
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (n0 + e0 + e < a.batch) y[(int64_t)(n0 + e0 + e) * a.ldy + row] = Act<T>::from_float(v[e]);
           }
         if (threadIdx.x == 0) a.counters[tile_mn] = 0;   // self-reset
       }
