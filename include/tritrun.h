@@ -104,6 +104,29 @@ TR_API int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t bat
                      int act_dtype, int64_t ldx, int64_t ldy, int flags, void* workspace, size_t ws_bytes,
                      void* stream);
 
+/* One product of a chain (tr_linear_chain): y[batch, rows] = x[batch, cols] @ W^T, TQ2 device layout. */
+typedef struct {
+  const void* w;
+  const void* x;
+  void* y;
+  int64_t ldx, ldy, rows, cols;
+} TrChainLayer;
+
+/* Bytes of caller-owned device workspace tr_linear_chain needs for n_layers (zero it once:
+ * the first 256 bytes hold the grid barrier, which the kernel leaves reset). */
+TR_API size_t tr_linear_chain_workspace_size(int64_t n_layers);
+/* Upload the chain's layer table into the workspace (synchronous; call once, outside any
+ * stream capture, and again whenever a pointer or shape changes). */
+TR_API int tr_linear_chain_prepare(const TrChainLayer* layers, int64_t n_layers, int64_t batch, void* workspace,
+                                   size_t ws_bytes);
+/* A dependent chain of TQ2 products (layer l's x is typically layer l-1's y) for batch 1..8
+ * in ONE persistent cooperative launch: a grid barrier between layers, and every warp's TMA
+ * weight ring prefetching the next layer's weights across the barrier (weights do not depend
+ * on x).  `layers` is the same HOST array given to tr_linear_chain_prepare (used for the
+ * launch plan only); graph-capturable. */
+TR_API int tr_linear_chain(int act_dtype, const TrChainLayer* layers, int64_t n_layers, int64_t batch, int flags,
+                           void* workspace, size_t ws_bytes, void* stream);
+
 /* ---- decoder-layer glue (configs[2] decode stack; no reference analogue) ---------- */
 
 /* h[r] += delta[r] (delta may be NULL); y[r] = h[r] * rsqrt(mean(h[r]^2) + eps) * w; rows x d */

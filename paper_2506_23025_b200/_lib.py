@@ -31,6 +31,13 @@ _c_p = ctypes.c_void_p
 _i64 = ctypes.c_int64
 _int = ctypes.c_int
 
+class TrChainLayer(ctypes.Structure):
+    """include/tritrun.h TrChainLayer: one product of a tr_linear_chain."""
+
+    _fields_ = [("w", ctypes.c_void_p), ("x", ctypes.c_void_p), ("y", ctypes.c_void_p), ("ldx", ctypes.c_int64),
+                ("ldy", ctypes.c_int64), ("rows", ctypes.c_int64), ("cols", ctypes.c_int64)]
+
+
 _SIGS = {
     "tr_last_error": ([], ctypes.c_char_p),
     "tr_version": ([], _int),
@@ -49,6 +56,9 @@ _SIGS = {
     "tr_linear_workspace_size": ([_int, _i64, _i64, _i64], ctypes.c_size_t),
     "tr_linear": ([_int, _c_p, _c_p, _c_p, _i64, _i64, _i64, _int, _i64, _i64, _int, _c_p, ctypes.c_size_t,
                    _c_p], _int),
+    "tr_linear_chain_workspace_size": ([_i64], ctypes.c_size_t),
+    "tr_linear_chain_prepare": ([ctypes.POINTER(TrChainLayer), _i64, _i64, _c_p, ctypes.c_size_t], _int),
+    "tr_linear_chain": ([_int, ctypes.POINTER(TrChainLayer), _i64, _i64, _int, _c_p, ctypes.c_size_t, _c_p], _int),
     "tr_add_rmsnorm": ([_int, _c_p, _c_p, _c_p, _c_p, _i64, _i64, ctypes.c_float, _c_p], _int),
     "tr_rope_kv": ([_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _i64, _i64, _i64, _i64, _c_p], _int),
     "tr_attn_decode": ([_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _i64, _i64, _i64, ctypes.c_float, _c_p],
@@ -89,6 +99,11 @@ def call(name: str, *args) -> int:
         msg = lib().tr_last_error().decode(errors="replace")
         raise TriRunError(f"{name} failed: {msg}")
     return rc
+
+
+def call_nostream(name: str, *args) -> int:
+    """Invoke a tr_* entry point that takes no stream argument."""
+    return call(name, *args)
 
 
 def stream_handle(stream=None) -> int:

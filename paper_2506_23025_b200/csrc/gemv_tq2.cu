@@ -25,6 +25,8 @@
 //  * a warp leaving a tile deposits its fragment in a shared slot; the last of
 //    the tile's warps sums the fragments in fixed warp order and stores y --
 //    deterministic, and no CTA-wide barrier in the main loop.
+#include <vector>
+
 #include "common.cuh"
 
 namespace tr {
@@ -72,16 +74,56 @@ template <> struct Frag<__nv_bfloat16> {
   }
 };
 
-struct GemvArgs {
+struct GemvLayer {    // one product y = x W^T (the C-ABI's TrStackLayer, plus derived sizes)
   const uint8_t* w;   // T16 units, tile-major
   const void* x;      // [batch][ldx]
   void* y;            // [batch][ldy]
   int64_t ldx, ldy;
-  int rows, cols, nb, n_tiles, batch;
+  int rows, cols, nb, n_tiles;
   int x_vec;          // x rows 16-byte aligned
-  int ns;             // ring slots per warp
-  int dbg;            // development probes: 1 = stream weights only, 2 = per-CTA timestamps into y
+  int pad_;
 };
+
+struct GemvArgs {
+  GemvLayer l0;                  // the layer (single product), or unused
+  const GemvLayer* layers;       // device layer table for a persistent chain (nullptr: just l0)
+  unsigned* bar;                 // grid barrier {count, generation} (chain only; zero-initialised)
+  int n_layers;
+  int nb_max;                    // shared-memory layout is sized for the widest layer
+  int batch;
+  int ns;                        // ring slots per warp
+  int dbg;                       // development probe: 2 = per-CTA timestamps into y
+};
+
+// Sense-reversal grid barrier for the persistent chain (all CTAs are co-resident: the
+// chain is launched cooperatively).  The counter self-resets; the generation only grows.
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <typename T>
+__device__ __forceinline__ uint4 ld_cg_x8(const T* row, int64_t k, int cols, int vec) {   // coherent (L2) path
+  if (vec && k + 8 <= cols) return __ldcg(reinterpret_cast<const uint4*>(row + k));
+  T tmp[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) tmp[e] = (k + e < cols) ? __ldcg(row + k + e) : Act<T>::from_float(0.0f);
+  return *reinterpret_cast<uint4*>(tmp);
+}
 
 // Shared-memory plan: [barriers, slot tags | reduction slots | C | staged x | per-warp weight rings].
 template <int NT> struct GemvCfg {
@@ -129,25 +171,29 @@ __global__ void __launch_bounds__(GemvCfg<NT>::kWarps * 32, 1) k_gemv_tq2(const 
   constexpr int kFrag = Cfg::kFrag, kWarps = Cfg::kWarps, kSlotBytes = Cfg::kSlotBytes, kSU = Cfg::kSU;
   const int NS = a.ns;
   extern __shared__ __align__(128) uint8_t smem[];
-  const int nb = a.nb;
   const int nrx = a.batch < 8 * NT ? a.batch : 8 * NT;
+  const bool chain = a.layers != nullptr;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                      // kWarps * NS (<= 64)
   int* slot_tile = reinterpret_cast<int*>(smem + 512);                      // 2 * kWarps
   float* red = reinterpret_cast<float*>(smem + Cfg::kRedOff);               // 2 * kWarps * kFrag
   float* csum = reinterpret_cast<float*>(smem + Cfg::kCsumOff);             // nb x 8NT
-  uint8_t* xs = smem + Cfg::xs_off(nb);                                     // XS: nrx x x_stride
-  uint8_t* ring = smem + Cfg::ring_off(nb, nrx, XS);
+  uint8_t* xs = smem + Cfg::xs_off(a.nb_max);                               // XS: nrx x x_stride
+  uint8_t* ring = smem + Cfg::ring_off(a.nb_max, nrx, XS);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, c = lane & 3;
-  // the CTA owns whole tiles [t0, t1): units [t0 nb, t1 nb) are one contiguous byte range
-  const int t0 = (int)((int64_t)blockIdx.x * a.n_tiles / gridDim.x);
-  const int t1 = (int)((int64_t)(blockIdx.x + 1) * a.n_tiles / gridDim.x);
-  const int cu0 = t0 * nb, L = (t1 - t0) * nb;
-  const int wu0 = cu0 + (int)((int64_t)warp * L / kWarps), wu1 = cu0 + (int)((int64_t)(warp + 1) * L / kWarps);
   uint64_t* mybar = bars + warp * NS;
   uint8_t* myring = ring + warp * NS * kSlotBytes;
-  uint64_t* trace = (a.dbg & 2) ? reinterpret_cast<uint64_t*>(a.y) + blockIdx.x * 8 : nullptr;
+  auto layer = [&](int l) -> GemvLayer { return chain ? a.layers[l] : a.l0; };
+  // the CTA owns whole tiles [t0, t1) of a layer; warp w a contiguous slice of its units
+  auto warp_range = [&](const GemvLayer& L_, int& u0, int& u1) {
+    const int t0 = (int)((int64_t)blockIdx.x * L_.n_tiles / gridDim.x);
+    const int t1 = (int)((int64_t)(blockIdx.x + 1) * L_.n_tiles / gridDim.x);
+    const int cu0 = t0 * L_.nb, LL = (t1 - t0) * L_.nb;
+    u0 = cu0 + (int)((int64_t)warp * LL / kWarps);
+    u1 = cu0 + (int)((int64_t)(warp + 1) * LL / kWarps);
+  };
+  uint64_t* trace = (a.dbg & 2) ? reinterpret_cast<uint64_t*>(a.l0.y) + blockIdx.x * 8 : nullptr;
   auto stamp = [&](int k) {
     if (trace && threadIdx.x == 0) {
       uint64_t t;
@@ -157,65 +203,48 @@ __global__ void __launch_bounds__(GemvCfg<NT>::kWarps * 32, 1) k_gemv_tq2(const 
   };
   stamp(0);
 
-  // ---- prologue (independent of the previous kernel): the warp's ring + its first NS copies
-  int iu = wu0;   // next unit to fetch (lane 0)
+  // ---- weight producer (lane 0): one op stream over every layer's range, so the ring keeps
+  // prefetching the next layer's weights (they do not depend on x) across layer boundaries
+  int pl = 0, pu = 0, pu1 = 0;   // producer: layer, next unit, end of this warp's range
+  const uint8_t* pw = nullptr;
   uint64_t pol = 0;
+  auto producer_seek = [&]() {     // advance to the next layer with a non-empty range
+    while (pu >= pu1 && pl < a.n_layers) {
+      if (++pl < a.n_layers) {
+        const GemvLayer L_ = layer(pl);
+        warp_range(L_, pu, pu1);
+        pw = L_.w;
+      }
+    }
+  };
+  auto issue = [&](int slot) -> bool {   // lane 0: next op into `slot`; false when the stream is done
+    if (pl >= a.n_layers) return false;
+    const int n = min(kSU, pu1 - pu);
+    mbar_expect_tx(&mybar[slot], n * kUnitBytes);
+    bulk_g2s(myring + slot * kSlotBytes, pw + (int64_t)pu * kUnitBytes, n * kUnitBytes, &mybar[slot], pol);
+    pu += n;
+    producer_seek();
+    return true;
+  };
   if (lane == 0) {
     pol = policy_evict_first();
     for (int s = 0; s < NS; ++s) mbar_init(&mybar[s], 1);
     mbar_fence_init();
-    slot_tile[2 * warp] = -1;
-    slot_tile[2 * warp + 1] = -1;
-    for (int s = 0; s < NS && iu < wu1; ++s) {
-      const int n = min(kSU, wu1 - iu);
-      mbar_expect_tx(&mybar[s], n * kUnitBytes);
-      bulk_g2s(myring + s * kSlotBytes, a.w + (int64_t)iu * kUnitBytes, n * kUnitBytes, &mybar[s], pol);
-      iu += n;
-    }
+    const GemvLayer L0 = layer(0);
+    warp_range(L0, pu, pu1);
+    pw = L0.w;
+    pl = 0;
+    producer_seek();   // (skips layers where this warp has no units)
+    for (int s = 0; s < NS; ++s)
+      if (!issue(s)) break;
   }
   __syncwarp();
   griddep_launch_dependents();
   griddep_wait();   // x belongs to the previous kernel until here
   stamp(1);
 
-  // ---- per-(block, row) correction C = sum_k x_k (1 + base / m_j(k)); stages x (XS) or warms L1
-  const T* xg = reinterpret_cast<const T*>(a.x);
-  const int rs = Cfg::x_stride(nb);
-  for (int item = warp; item < nb * nrx; item += kWarps) {
-    const int kb = item / nrx, n = item % nrx;
-    const uint4 v = load_x8(xg + n * a.ldx, (int64_t)kb * kBlock + lane * 8, a.cols, a.x_vec);
-    if (XS) *reinterpret_cast<uint4*>(xs + n * rs + kb * kXBlk + (lane >> 3) * kXChunk + (lane & 7) * 16) = v;
-    // chunk column (8 lane + e) % 64 has field class j = (col >> 2) & 3
-    const int ja = (2 * lane) & 3, jb = ja + 1;
-    const float fa = 1.0f + Frag<T>::kBase * Frag<T>::inv_f(ja), fb = 1.0f + Frag<T>::kBase * Frag<T>::inv_f(jb);
-    const float2 p0 = Frag<T>::to_f2(v.x), p1 = Frag<T>::to_f2(v.y), p2 = Frag<T>::to_f2(v.z),
-                 p3 = Frag<T>::to_f2(v.w);
-    float s = ((p0.x + p0.y) + (p1.x + p1.y)) * fa + ((p2.x + p2.y) + (p3.x + p3.y)) * fb;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) csum[kb * 8 * NT + n] = s;
-  }
-  __syncthreads();
-  stamp(2);
-
-  T* y = reinterpret_cast<T*>(a.y);
-  auto store_tile = [&](int tile, const float (&v)[NT][4]) {
-    if (trace) return;
-    const int r0 = tile * 16 + g, r1 = r0 + 8;
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const int n0 = 8 * t + 2 * c, n1 = n0 + 1;
-      if (n0 < a.batch) {
-        if (r0 < a.rows) y[n0 * a.ldy + r0] = Act<T>::from_float(v[t][0]);
-        if (r1 < a.rows) y[n0 * a.ldy + r1] = Act<T>::from_float(v[t][2]);
-      }
-      if (n1 < a.batch) {
-        if (r0 < a.rows) y[n1 * a.ldy + r0] = Act<T>::from_float(v[t][1]);
-        if (r1 < a.rows) y[n1 * a.ldy + r1] = Act<T>::from_float(v[t][3]);
-      }
-    }
-  };
-
+  int k = 0;   // consumer op counter (ring slot k % NS)
+  const int nslog = NS == 1 ? 0 : NS == 2 ? 1 : 2;   // NS is a power of two (host)
   float acc[NT][4];
   float P[4][NT][4];
 #pragma unroll
@@ -226,164 +255,210 @@ __global__ void __launch_bounds__(GemvCfg<NT>::kWarps * 32, 1) k_gemv_tq2(const 
 #pragma unroll
       for (int j = 0; j < 4; ++j) P[j][t][e] = 0.0f;
     }
-  const int first_tile = wu0 < wu1 ? wu0 / nb : -1;
-  int cur = first_tile;
-  // a tile wholly inside this warp's range is stored now; a boundary tile is parked
-  // in a reduction slot (0: the warp's first tile, 1: its last) and combined below
-  auto close_tile = [&](int tile) {
-    if (tile * nb >= wu0 && (tile + 1) * nb <= wu1) {
-      store_tile(tile, acc);
-      return;
+
+  for (int l = 0; l < a.n_layers; ++l) {
+    const GemvLayer Ly = layer(l);
+    const int nb = Ly.nb;
+    if (l > 0) grid_barrier(a.bar);   // every CTA has stored layer l-1's y (= this layer's x)
+    if (lane == 0) {
+      slot_tile[2 * warp] = -1;
+      slot_tile[2 * warp + 1] = -1;
     }
-    const int which = (tile == first_tile) ? 0 : 1;
-    float* dst = red + (2 * warp + which) * kFrag;
+    // ---- per-(block, row) correction C = sum_k x_k (1 + base / m_j(k)); stages x (XS) or warms L1
+    const T* xg = reinterpret_cast<const T*>(Ly.x);
+    const int rs = Cfg::x_stride(nb);
+    for (int item = warp; item < nb * nrx; item += kWarps) {
+      const int kb = item / nrx, n = item % nrx;
+      const int64_t kx = (int64_t)kb * kBlock + lane * 8;
+      const uint4 v = chain ? ld_cg_x8(xg + n * Ly.ldx, kx, Ly.cols, Ly.x_vec)
+                            : load_x8(xg + n * Ly.ldx, kx, Ly.cols, Ly.x_vec);
+      if (XS) *reinterpret_cast<uint4*>(xs + n * rs + kb * kXBlk + (lane >> 3) * kXChunk + (lane & 7) * 16) = v;
+      // chunk column (8 lane + e) % 64 has field class j = (col >> 2) & 3
+      const int ja = (2 * lane) & 3, jb = ja + 1;
+      const float fa = 1.0f + Frag<T>::kBase * Frag<T>::inv_f(ja), fb = 1.0f + Frag<T>::kBase * Frag<T>::inv_f(jb);
+      const float2 p0 = Frag<T>::to_f2(v.x), p1 = Frag<T>::to_f2(v.y), p2 = Frag<T>::to_f2(v.z),
+                   p3 = Frag<T>::to_f2(v.w);
+      float sm = ((p0.x + p0.y) + (p1.x + p1.y)) * fa + ((p2.x + p2.y) + (p3.x + p3.y)) * fb;
 #pragma unroll
-    for (int t = 0; t < NT; ++t)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) dst[(t * 4 + e) * 32 + lane] = acc[t][e];
-    if (lane == 0) slot_tile[2 * warp + which] = tile;
-  };
+      for (int o = 16; o; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+      if (lane == 0) csum[kb * 8 * NT + n] = sm;
+    }
+    __syncthreads();
+    stamp(2);
 
-  // B-fragment rows: lanes past the batch read row 0 -- their output columns are never stored
-  const uint8_t* xsrow[NT];
-  const T* xrow[NT];
+    int wu0, wu1;
+    warp_range(Ly, wu0, wu1);
+    T* y = reinterpret_cast<T*>(Ly.y);
+    auto store_tile = [&](int tile, const float (&v)[NT][4]) {
+      if (trace) return;
+      const int r0 = tile * 16 + g, r1 = r0 + 8;
 #pragma unroll
-  for (int t = 0; t < NT; ++t) {
-    const int n = min(8 * t + g, nrx - 1);
-    xrow[t] = xg + n * a.ldx;
-    xsrow[t] = xs + n * rs + c * kXChunk;
-  }
-
-  // one 16x256 unit: decode + 16 (x NT) mma.sync, then the block epilogue into acc
-  auto do_unit = [&](const uint4& wl, const uint4& wh, uint32_t sv, int kb) {
-    const int64_t kx = (int64_t)kb * kBlock + c * 64;
-#pragma unroll
-    for (int p = 0; p < 2; ++p) {
-      const uint32_t L0 = p ? wl.z : wl.x, L1 = p ? wl.w : wl.y;
-      const uint32_t H0 = p ? wh.z : wh.x, H1 = p ? wh.w : wh.y;
-      const uint32_t L08 = L0 >> 8, L18 = L1 >> 8, H08 = H0 >> 8, H18 = H1 >> 8;
-#pragma unroll
-      for (int hb = 0; hb < 2; ++hb) {
-        uint4 xv[NT][2];
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          if (XS) {
-            const uint8_t* xp = xsrow[t] + kb * kXBlk + 32 * (2 * p + hb);
-            xv[t][0] = lds128(xp);
-            xv[t][1] = lds128(xp + 16);
-          } else {
-            xv[t][0] = load_x8(xrow[t], kx + 16 * (2 * p + hb), a.cols, a.x_vec);
-            xv[t][1] = load_x8(xrow[t], kx + 16 * (2 * p + hb) + 8, a.cols, a.x_vec);
-          }
+      for (int t = 0; t < NT; ++t) {
+        const int n0 = 8 * t + 2 * c, n1 = n0 + 1;
+        if (n0 < a.batch) {
+          if (r0 < Ly.rows) y[n0 * Ly.ldy + r0] = Act<T>::from_float(v[t][0]);
+          if (r1 < Ly.rows) y[n0 * Ly.ldy + r1] = Act<T>::from_float(v[t][2]);
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t A[4] = {Frag<T>::field(L0, L08, hb, j), Frag<T>::field(H0, H08, hb, j),
-                                 Frag<T>::field(L1, L18, hb, j), Frag<T>::field(H1, H18, hb, j)};
-#pragma unroll
-          for (int t = 0; t < NT; ++t) {
-            const uint4& xx = xv[t][j >> 1];
-            Frag<T>::mma(P[j][t], A, (j & 1) ? xx.z : xx.x, (j & 1) ? xx.w : xx.y);
-          }
+        if (n1 < a.batch) {
+          if (r0 < Ly.rows) y[n1 * Ly.ldy + r0] = Act<T>::from_float(v[t][1]);
+          if (r1 < Ly.rows) y[n1 * Ly.ldy + r1] = Act<T>::from_float(v[t][3]);
         }
       }
-    }
-    // block epilogue: block sum in fp32, times the block scale, into the row accumulator
-    const float2 sc = __half22float2(*reinterpret_cast<const __half2*>(&sv));
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const float2 cv = *reinterpret_cast<const float2*>(csum + kb * 8 * NT + 8 * t + 2 * c);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float yb = fmaf(P[0][t][e], Frag<T>::inv_f(0), -((e & 1) ? cv.y : cv.x));
-        yb = fmaf(P[1][t][e], Frag<T>::inv_f(1), yb);
-        yb = fmaf(P[2][t][e], Frag<T>::inv_f(2), yb);
-        yb = fmaf(P[3][t][e], Frag<T>::inv_f(3), yb);
-        acc[t][e] = fmaf((e & 2) ? sc.y : sc.x, yb, acc[t][e]);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) P[j][t][e] = 0.0f;
+    };
+    const int first_tile = wu0 < wu1 ? wu0 / nb : -1;
+    int cur = first_tile;
+    // a tile wholly inside this warp's range is stored now; a boundary tile is parked
+    // in a reduction slot (0: the warp's first tile, 1: its last) and combined below
+    auto close_tile = [&](int tile) {
+      if (tile * nb >= wu0 && (tile + 1) * nb <= wu1) {
+        store_tile(tile, acc);
+        return;
       }
-    }
-  };
-
-  // x row pointer of the current unit (advanced incrementally; reset on a tile change)
-  int kb = wu0 - (wu0 < wu1 ? first_tile : 0) * nb;   // block of the next unit within tile `cur`
-  auto unit = [&](const uint4& wl, const uint4& wh, uint32_t sv) {
-    if (kb == nb) {   // next tile
-      close_tile(cur);
+      const int which = (tile == first_tile) ? 0 : 1;
+      float* dst = red + (2 * warp + which) * kFrag;
 #pragma unroll
       for (int t = 0; t < NT; ++t)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[t][e] = 0.0f;
-      ++cur;
-      kb = 0;
-    }
-    do_unit(wl, wh, sv, kb);
-    ++kb;
-  };
+        for (int e = 0; e < 4; ++e) dst[(t * 4 + e) * 32 + lane] = acc[t][e];
+      if (lane == 0) slot_tile[2 * warp + which] = tile;
+    };
 
-  const int nslog = NS == 1 ? 0 : NS == 2 ? 1 : 2;   // NS is a power of two (host)
-  int u = wu0;
+    // B-fragment rows: lanes past the batch read row 0 -- their output columns are never stored
+    const uint8_t* xsrow[NT];
+    const T* xrow[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int n = min(8 * t + g, nrx - 1);
+      xrow[t] = xg + n * Ly.ldx;
+      xsrow[t] = xs + n * rs + c * kXChunk;
+    }
+
+    // one 16x256 unit: decode + 16 (x NT) mma.sync, then the block epilogue into acc
+    auto do_unit = [&](const uint4& wl, const uint4& wh, uint32_t sv, int kb) {
+      const int64_t kx = (int64_t)kb * kBlock + c * 64;
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const uint32_t L0 = p ? wl.z : wl.x, L1 = p ? wl.w : wl.y;
+        const uint32_t H0 = p ? wh.z : wh.x, H1 = p ? wh.w : wh.y;
+        const uint32_t L08 = L0 >> 8, L18 = L1 >> 8, H08 = H0 >> 8, H18 = H1 >> 8;
+#pragma unroll
+        for (int hb = 0; hb < 2; ++hb) {
+          uint4 xv[NT][2];
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            if (XS) {
+              const uint8_t* xp = xsrow[t] + kb * kXBlk + 32 * (2 * p + hb);
+              xv[t][0] = lds128(xp);
+              xv[t][1] = lds128(xp + 16);
+            } else {
+              xv[t][0] = load_x8(xrow[t], kx + 16 * (2 * p + hb), Ly.cols, Ly.x_vec);
+              xv[t][1] = load_x8(xrow[t], kx + 16 * (2 * p + hb) + 8, Ly.cols, Ly.x_vec);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t A[4] = {Frag<T>::field(L0, L08, hb, j), Frag<T>::field(H0, H08, hb, j),
+                                   Frag<T>::field(L1, L18, hb, j), Frag<T>::field(H1, H18, hb, j)};
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+              const uint4& xx = xv[t][j >> 1];
+              Frag<T>::mma(P[j][t], A, (j & 1) ? xx.z : xx.x, (j & 1) ? xx.w : xx.y);
+            }
+          }
+        }
+      }
+      // block epilogue: block sum in fp32, times the block scale, into the row accumulator
+      const float2 sc = __half22float2(*reinterpret_cast<const __half2*>(&sv));
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const float2 cv = *reinterpret_cast<const float2*>(csum + kb * 8 * NT + 8 * t + 2 * c);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float yb = fmaf(P[0][t][e], Frag<T>::inv_f(0), -((e & 1) ? cv.y : cv.x));
+          yb = fmaf(P[1][t][e], Frag<T>::inv_f(1), yb);
+          yb = fmaf(P[2][t][e], Frag<T>::inv_f(2), yb);
+          yb = fmaf(P[3][t][e], Frag<T>::inv_f(3), yb);
+          acc[t][e] = fmaf((e & 2) ? sc.y : sc.x, yb, acc[t][e]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) P[j][t][e] = 0.0f;
+        }
+      }
+    };
+
+    int kb = wu0 - (wu0 < wu1 ? first_tile : 0) * nb;   // block of the next unit within tile `cur`
+    auto unit = [&](const uint4& wl, const uint4& wh, uint32_t sv) {
+      if (kb == nb) {   // next tile
+        close_tile(cur);
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[t][e] = 0.0f;
+        ++cur;
+        kb = 0;
+      }
+      do_unit(wl, wh, sv, kb);
+      ++kb;
+    };
+
+    int u = wu0;
 #pragma unroll 1
-  for (int k = 0; u < wu1; ++k) {
-    const int s = k & (NS - 1);
-    mbar_wait(&mybar[s], (k >> nslog) & 1);
-    if (k == 0) stamp(3);
-    const uint8_t* slot = myring + s * kSlotBytes + (c * 8 + g) * 16;
-    if (wu1 - u >= kSU) {   // full slot: read all units into registers, refill, compute
+    for (; u < wu1; ++k) {
+      const int s = k & (NS - 1);
+      const int n = min(kSU, wu1 - u);
+      mbar_wait(&mybar[s], (k >> nslog) & 1);
+      if (k == 0) stamp(3);
+      const uint8_t* slot = myring + s * kSlotBytes + (c * 8 + g) * 16;
       uint4 wl[kSU], wh[kSU];
       uint32_t sv[kSU];
 #pragma unroll
       for (int q = 0; q < kSU; ++q) {
-        wl[q] = lds128(slot + q * kUnitBytes);
-        wh[q] = lds128(slot + q * kUnitBytes + 512);
-        sv[q] = *reinterpret_cast<const uint32_t*>(slot - (c * 8 + g) * 16 + q * kUnitBytes + kTileBlockBytes + g * 4);
+        if (q < n) {
+          wl[q] = lds128(slot + q * kUnitBytes);
+          wh[q] = lds128(slot + q * kUnitBytes + 512);
+          sv[q] = *reinterpret_cast<const uint32_t*>(slot - (c * 8 + g) * 16 + q * kUnitBytes + kTileBlockBytes + g * 4);
+        }
       }
-      __syncwarp();
-      if (lane == 0 && iu < wu1) {
-        const int nn = min(kSU, wu1 - iu);
+      __syncwarp();   // slot fully read into registers: refill it with the next op of the stream
+      if (lane == 0) {
         fence_proxy_async_smem();
-        mbar_expect_tx(&mybar[s], nn * kUnitBytes);
-        bulk_g2s(myring + s * kSlotBytes, a.w + (int64_t)iu * kUnitBytes, nn * kUnitBytes, &mybar[s], pol);
-        iu += nn;
+        issue(s);
       }
 #pragma unroll
-      for (int q = 0; q < kSU; ++q) unit(wl[q], wh[q], sv[q]);
-      u += kSU;
-    } else {                // the range's last, partial slot (no refill needed)
-#pragma unroll 1
-      for (; u < wu1; ++u, slot += kUnitBytes) {
-        const uint4 wl = lds128(slot), wh = lds128(slot + 512);
-        const uint32_t sv = *reinterpret_cast<const uint32_t*>(slot - (c * 8 + g) * 16 + kTileBlockBytes + g * 4);
-        unit(wl, wh, sv);
-      }
+      for (int q = 0; q < kSU; ++q)
+        if (q < n) unit(wl[q], wh[q], sv[q]);
+      u += n;
     }
-  }
-  stamp(4);
-  if (cur >= 0) close_tile(cur);
-
-  // ---- boundary tiles: combine the parked fragments in fixed (warp, slot) order and store
-  __syncthreads();
-  for (int i = warp; i < 2 * kWarps; i += kWarps) {
-    const int tile = slot_tile[i];
-    if (tile < 0) continue;
-    bool owner = true;   // the lowest slot holding this tile does the reduction
-    for (int q = 0; q < i; ++q) owner &= (slot_tile[q] != tile);
-    if (!owner) continue;
-    float v[NT][4];
+    stamp(4);
+    if (cur >= 0) close_tile(cur);
 #pragma unroll
     for (int t = 0; t < NT; ++t)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) v[t][e] = 0.0f;
-    for (int q = i; q < 2 * kWarps; ++q) {
-      if (slot_tile[q] != tile) continue;
-      const float* src = red + q * kFrag;
+      for (int e = 0; e < 4; ++e) acc[t][e] = 0.0f;
+
+    // ---- boundary tiles: combine the parked fragments in fixed (warp, slot) order and store
+    __syncthreads();
+    for (int i = warp; i < 2 * kWarps; i += kWarps) {
+      const int tile = slot_tile[i];
+      if (tile < 0) continue;
+      bool owner = true;   // the lowest slot holding this tile does the reduction
+      for (int q = 0; q < i; ++q) owner &= (slot_tile[q] != tile);
+      if (!owner) continue;
+      float v[NT][4];
 #pragma unroll
       for (int t = 0; t < NT; ++t)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) v[t][e] += src[(t * 4 + e) * 32 + lane];
+        for (int e = 0; e < 4; ++e) v[t][e] = 0.0f;
+      for (int q = i; q < 2 * kWarps; ++q) {
+        if (slot_tile[q] != tile) continue;
+        const float* src = red + q * kFrag;
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) v[t][e] += src[(t * 4 + e) * 32 + lane];
+      }
+      store_tile(tile, v);
     }
-    store_tile(tile, v);
+    __syncthreads();   // slot_tile / red / csum / xs are reused by the next layer
   }
   stamp(5);
 }
@@ -403,10 +478,19 @@ int sm_count() {
 
 size_t gemv_workspace_bytes(int, int, int) { return 0; }   // the GEMV needs no global workspace
 
-constexpr size_t kXsBudget = 96 * 1024;   // stage activations in smem up to this size
+constexpr size_t kXsBudget = 128 * 1024;  // stage activations in smem up to this size (if the whole plan fits)
+
+template <int NT>
+static int gemv_ns(int n_tiles, int nb, int grid) {
+  using Cfg = GemvCfg<NT>;
+  const int tiles_max = (int)ceil_div(n_tiles, grid);
+  const int ops = (int)ceil_div(ceil_div((int64_t)tiles_max * nb, Cfg::kWarps), Cfg::kSU);
+  const int ns_max = kNSMax * 2 / Cfg::kSU;   // <= 8 units (8.4 KB) in flight per warp
+  return ops >= ns_max ? ns_max : ops > 1 ? 2 : 1;
+}
 
 template <typename T, int NT, bool XS>
-static int launch_gemv_x(const GemvArgs& a, int grid, int pdl, cudaStream_t st) {
+static int launch_gemv_x(const GemvArgs& a, int grid, int pdl, bool coop, cudaStream_t st) {
   auto kern = k_gemv_tq2<T, NT, XS>;
   static int configured_dev = -1;
   int dev = 0;
@@ -417,15 +501,9 @@ static int launch_gemv_x(const GemvArgs& a, int grid, int pdl, cudaStream_t st) 
   }
   using Cfg = GemvCfg<NT>;
   const int nrx = a.batch < 8 * NT ? a.batch : 8 * NT;
-  GemvArgs b = a;
-  const int tiles_max = (int)ceil_div(a.n_tiles, grid);
-  const int per_warp = (int)ceil_div((int64_t)tiles_max * a.nb, Cfg::kWarps);
-  const int ops = (int)ceil_div(per_warp, Cfg::kSU);
-  const int ns_max = kNSMax * 2 / Cfg::kSU;   // <= 8 units (8.4 KB) in flight per warp
-  b.ns = ops >= ns_max ? ns_max : ops > 1 ? 2 : 1;
-  const size_t smem = Cfg::smem(a.nb, nrx, XS, b.ns);
+  const size_t smem = Cfg::smem(a.nb_max, nrx, XS, a.ns);
   if (smem > 227 * 1024) {
-    set_error("tr_linear(gemv): %d blocks per row need %zu B of shared memory", a.nb, smem);
+    set_error("tr_linear(gemv): %d blocks per row need %zu B of shared memory", a.nb_max, smem);
     return -1;
   }
   cudaLaunchConfig_t cfg = {};
@@ -433,16 +511,21 @@ static int launch_gemv_x(const GemvArgs& a, int grid, int pdl, cudaStream_t st) 
   cfg.blockDim = dim3(Cfg::kWarps * 32, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attrs[1];
+  cudaLaunchAttribute attrs[2];
   int na = 0;
   if (pdl) {
     attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attrs[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
+  if (coop) {   // the persistent chain's grid barrier needs every CTA resident
+    attrs[na].id = cudaLaunchAttributeCooperative;
+    attrs[na].val.cooperative = 1;
+    ++na;
+  }
   cfg.attrs = attrs;
   cfg.numAttrs = na;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, b);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
   if (e != cudaSuccess) {
     set_error("tr_linear(gemv): launch failed: %s (grid %d, smem %zu)", cudaGetErrorString(e), grid, smem);
     return -1;
@@ -451,63 +534,113 @@ static int launch_gemv_x(const GemvArgs& a, int grid, int pdl, cudaStream_t st) 
 }
 
 template <int NT>
-static size_t gemv_smem(const GemvArgs& a, int grid, bool xs) {
-  using Cfg = GemvCfg<NT>;
-  const int nrx = a.batch < 8 * NT ? a.batch : 8 * NT;
-  const int tiles_max = (int)ceil_div(a.n_tiles, grid);
-  const int ops = (int)ceil_div(ceil_div((int64_t)tiles_max * a.nb, Cfg::kWarps), Cfg::kSU);
-  const int ns_max = kNSMax * 2 / Cfg::kSU;
-  const int ns = ops >= ns_max ? ns_max : ops > 1 ? 2 : 1;
-  return Cfg::smem(a.nb, nrx, xs, ns);
+static bool xs_fits(int batch, int nb_max, int ns) {
+  const int nrx = batch < 8 * NT ? batch : 8 * NT;
+  return (size_t)nrx * GemvCfg<NT>::x_stride(nb_max) <= kXsBudget &&
+         GemvCfg<NT>::smem(nb_max, nrx, true, ns) <= 227 * 1024;
 }
 
 template <typename T, int NT>
-static int launch_gemv(const GemvArgs& a, int grid, int pdl, cudaStream_t st) {
-  const int nrx = a.batch < 8 * NT ? a.batch : 8 * NT;
-  if ((size_t)nrx * GemvCfg<NT>::x_stride(a.nb) <= kXsBudget && gemv_smem<NT>(a, grid, true) <= 227 * 1024)
-    return launch_gemv_x<T, NT, true>(a, grid, pdl, st);
-  return launch_gemv_x<T, NT, false>(a, grid, pdl, st);
+static int launch_gemv(GemvArgs& a, int grid, int pdl, bool coop, cudaStream_t st) {
+  if (xs_fits<NT>(a.batch, a.nb_max, a.ns)) return launch_gemv_x<T, NT, true>(a, grid, pdl, coop, st);
+  if (coop) {
+    set_error("tr_linear_chain: activations of %d blocks x batch %d do not fit in shared memory", a.nb_max, a.batch);
+    return -1;
+  }
+  return launch_gemv_x<T, NT, false>(a, grid, pdl, coop, st);
 }
 
 // true when the GEMV can stage this batch's activations in shared memory (its fast path)
 bool gemv_stages_x(int batch, int rows, int cols) {
-  GemvArgs a = {};
-  a.nb = (int)ceil_div(cols, kBlock);
-  a.n_tiles = (int)ceil_div(rows, 16);
-  a.batch = batch;
-  int grid = sm_count() < a.n_tiles ? sm_count() : a.n_tiles;
-  if (batch <= 8)
-    return (size_t)batch * GemvCfg<1>::x_stride(a.nb) <= kXsBudget && gemv_smem<1>(a, grid, true) <= 227 * 1024;
-  return false;
+  if (batch > 8) return false;
+  const int nb = (int)ceil_div(cols, kBlock), n_tiles = (int)ceil_div(rows, 16);
+  const int grid = sm_count() < n_tiles ? sm_count() : n_tiles;
+  return xs_fits<1>(batch, nb, gemv_ns<1>(n_tiles, nb, grid));
+}
+
+static GemvLayer make_layer(const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int rows, int cols) {
+  GemvLayer L;
+  L.w = (const uint8_t*)w;
+  L.x = x;
+  L.y = y;
+  L.ldx = ldx;
+  L.ldy = ldy;
+  L.rows = rows;
+  L.cols = cols;
+  L.nb = (int)ceil_div(cols, kBlock);
+  L.n_tiles = (int)ceil_div(rows, 16);
+  L.x_vec = ((ldx % 8) == 0 && ((uintptr_t)x % 16) == 0) ? 1 : 0;
+  L.pad_ = 0;
+  return L;
 }
 
 int gemv_tq2(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
              int cols, int ctas, int pdl, cudaStream_t st) {
-  GemvArgs a;
+  GemvArgs a = {};
   a.dbg = (ctas >> 12) & 0xF;
   ctas &= 0xFFF;
-  a.w = (const uint8_t*)w;
-  a.x = x;
-  a.y = y;
-  a.ldx = ldx;
-  a.ldy = ldy;
-  a.rows = rows;
-  a.cols = cols;
-  a.nb = (int)ceil_div(cols, kBlock);
-  a.n_tiles = (int)ceil_div(rows, 16);
+  a.l0 = make_layer(w, x, y, ldx, ldy, rows, cols);
+  a.layers = nullptr;
+  a.bar = nullptr;
+  a.n_layers = 1;
+  a.nb_max = a.l0.nb;
   a.batch = batch;
-  a.x_vec = ((ldx % 8) == 0 && ((uintptr_t)x % 16) == 0) ? 1 : 0;
   int grid = ctas > 0 ? ctas : sm_count();
-  if (grid > a.n_tiles) grid = a.n_tiles;
+  if (grid > a.l0.n_tiles) grid = a.l0.n_tiles;
   const int nt = batch <= 8 ? 1 : (batch <= 16 ? 2 : 4);
+  if (nt == 1) a.ns = gemv_ns<1>(a.l0.n_tiles, a.l0.nb, grid);
+  else if (nt == 2) a.ns = gemv_ns<2>(a.l0.n_tiles, a.l0.nb, grid);
+  else a.ns = gemv_ns<4>(a.l0.n_tiles, a.l0.nb, grid);
   if (act == kActF16) {
-    if (nt == 1) return launch_gemv<__half, 1>(a, grid, pdl, st);
-    if (nt == 2) return launch_gemv<__half, 2>(a, grid, pdl, st);
-    return launch_gemv<__half, 4>(a, grid, pdl, st);
+    if (nt == 1) return launch_gemv<__half, 1>(a, grid, pdl, false, st);
+    if (nt == 2) return launch_gemv<__half, 2>(a, grid, pdl, false, st);
+    return launch_gemv<__half, 4>(a, grid, pdl, false, st);
   }
-  if (nt == 1) return launch_gemv<__nv_bfloat16, 1>(a, grid, pdl, st);
-  if (nt == 2) return launch_gemv<__nv_bfloat16, 2>(a, grid, pdl, st);
-  return launch_gemv<__nv_bfloat16, 4>(a, grid, pdl, st);
+  if (nt == 1) return launch_gemv<__nv_bfloat16, 1>(a, grid, pdl, false, st);
+  if (nt == 2) return launch_gemv<__nv_bfloat16, 2>(a, grid, pdl, false, st);
+  return launch_gemv<__nv_bfloat16, 4>(a, grid, pdl, false, st);
 }
+
+// A chain of products y_l = x_l W_l^T in ONE persistent cooperative launch (batch <= 8):
+// grid barriers between layers, weight prefetch running ahead across them.
+int gemv_chain(int act, const TrChainLayer* host_layers, void* dev_table, int n_layers, int batch, unsigned* bar,
+               int pdl, cudaStream_t st, bool upload) {
+  if (n_layers < 1 || batch < 1 || batch > 8) {
+    set_error("tr_linear_chain: need 1 <= batch <= 8 and at least one layer");
+    return -1;
+  }
+  GemvArgs a = {};
+  a.layers = (const GemvLayer*)dev_table;
+  a.bar = bar;
+  a.n_layers = n_layers;
+  a.batch = batch;
+  a.nb_max = 0;
+  int tiles_min = 1 << 30, ns = 4;
+  std::vector<GemvLayer> tab((size_t)n_layers);
+  const int grid = sm_count();
+  for (int l = 0; l < n_layers; ++l) {
+    const TrChainLayer& h = host_layers[l];
+    tab[l] = make_layer(h.w, h.x, h.y, h.ldx, h.ldy, (int)h.rows, (int)h.cols);
+    if (tab[l].nb > a.nb_max) a.nb_max = tab[l].nb;
+    if (tab[l].n_tiles < tiles_min) tiles_min = tab[l].n_tiles;
+    const int n = gemv_ns<1>(tab[l].n_tiles, tab[l].nb, grid);
+    if (n < ns) ns = n;
+  }
+  a.ns = ns < 2 ? 2 : ns;
+  if (!xs_fits<1>(batch, a.nb_max, a.ns)) a.ns = 1;   // wide activations: a shallower weight ring
+  a.l0 = tab[0];
+  if (upload) {   // synchronous, outside any stream capture (tr_linear_chain_prepare)
+    cudaError_t e = cudaMemcpy(dev_table, tab.data(), sizeof(GemvLayer) * n_layers, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      set_error("tr_linear_chain_prepare: table upload failed: %s", cudaGetErrorString(e));
+      return -1;
+    }
+    return 0;
+  }
+  if (act == kActF16) return launch_gemv<__half, 1>(a, grid, pdl, true, st);
+  return launch_gemv<__nv_bfloat16, 1>(a, grid, pdl, true, st);
+}
+
+size_t gemv_chain_table_bytes(int n_layers) { return sizeof(GemvLayer) * (size_t)n_layers; }
 
 }  // namespace tr
