@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--replicas", type=int, default=32)
     p.add_argument("--sweep", default="1,2,4,8,16,32,64,128")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--extras", default="decode,tq1,tp70b",
+                   help="extra sections on rank 0 at N=1: decode (configs[2]), tq1 (configs[3]), tp70b (configs[4])")
     return p.parse_args()
 
 
@@ -245,6 +247,106 @@ def dense_stack(weights, batch):
     return g, dws
 
 
+def _time_layers(ws, x, path="auto", reps=10):
+    """Per-layer device time of independent products over rotating weights (graph + PDL)."""
+    import torch
+    import paper_2506_23025_b200 as tp
+
+    ys = [torch.empty((x.shape[0], w.rows), dtype=x.dtype, device=x.device) for w in ws]
+    s, g = torch.cuda.Stream(), torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        for w, y in zip(ws, ys):
+            tp.linear(x, w, out=y, pdl=True, path=path)
+        s.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            for w, y in zip(ws, ys):
+                tp.linear(x, w, out=y, pdl=True, path=path)
+    return timed_graph(g.replay, reps, 3, None) / reps / len(ws)
+
+
+def run_extras(args, stack_ws):
+    """configs[2] decode tokens/s, configs[3] TQ1 8192^2, configs[4] 70B layer shapes (1 GPU + TP shards)."""
+    import torch
+    import paper_2506_23025_b200 as tp
+
+    out = {}
+    want = set(args.extras.split(","))
+    del stack_ws
+    torch.cuda.empty_cache()
+    if "tq1" in want:   # 1.6-bit weights decoded on the fly (tcgen05 path), next to TQ2 on the same trits
+        res = []
+        for fmt, bpb in ((tp.DType.TQ1, 54), (tp.DType.TQ2, 66)):
+            g = torch.Generator(device="cuda").manual_seed(7)
+            ws = []
+            for _ in range(12):
+                T = torch.randint(0, 3, (8192, 8192), generator=g, device="cuda", dtype=torch.int8).float() - 1
+                gam = (0.02 * (1 + torch.rand((8192, 1), generator=g, device="cuda"))).half().float()
+                ws.append(tp.TernaryWeight.from_float(gam * T, fmt))
+            for b in (1, 8):
+                x = (torch.rand(b, 8192, device="cuda") * 2 - 1).half()
+                ms = _time_layers(ws, x)
+                nbytes = 8192 * 32 * bpb + b * 16384 * 2
+                res.append({"format": fmt.name, "batch": b, "us": round(ms * 1e3, 2),
+                            "gbs": round(nbytes / ms / 1e6, 1)})
+            del ws
+            torch.cuda.empty_cache()
+        out["tq1_8192x8192"] = res
+    if "tp70b" in want:   # 70B up (rows 28672 x cols 8192) / down (8192 x 28672); shard times at TP 1/2/4/8
+        from paper_2506_23025_b200.parallel import shard_bounds
+
+        res = []
+        g = torch.Generator(device="cuda").manual_seed(9)
+        for name, rows, cols, kind in (("up", 28672, 8192, "column"), ("down", 8192, 28672, "row")):
+            for tpn in (1, 2, 4, 8):
+                r = rows // tpn if kind == "column" else rows
+                c = cols if kind == "column" else cols // tpn
+                ws = []
+                for _ in range(max(3, min(16, (3 * 126 * 2**20) // (r * c // 256 * 66) + 1))):
+                    T = torch.randint(0, 3, (r, c), generator=g, device="cuda", dtype=torch.int8).float() - 1
+                    ws.append(tp.TernaryWeight.from_float(0.02 * T))
+                for b in (1, 16):
+                    x = (torch.rand(b, c, device="cuda") * 2 - 1).half()
+                    ms = _time_layers(ws, x)
+                    res.append({"layer": name, "tp": tpn, "shard": f"{r}x{c}", "batch": b,
+                                "us_per_gpu": round(ms * 1e3, 2),
+                                "gbs_per_gpu": round((r * (c // 256) * 66 + b * (r + c) * 2) / ms / 1e6, 1),
+                                "collective": "none" if kind == "column" else f"all-reduce {b * rows * 2} B"})
+                del ws
+                torch.cuda.empty_cache()
+        out["tp70b_shards"] = res
+    if "decode" in want:  # configs[2]: TriLM-3.9B-shaped decoder, 64 prompt + 64 greedy tokens
+        from paper_2506_23025_b200.decoder import DecoderConfig, TernaryDecoder
+
+        cfg = DecoderConfig(max_seq=128)
+        prompt = torch.randint(0, cfg.vocab, (64,), device="cuda", generator=torch.Generator(device="cuda").manual_seed(1))
+
+        def measure(m):
+            m.reset(); m.prefill(prompt); m.capture()
+            best = None
+            for _ in range(3):
+                m.reset()
+                torch.cuda.synchronize()
+                e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                e[0].record(); m.prefill(prompt); e[1].record(); m.decode(64); e[2].record(); e[2].synchronize()
+                cur = (e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]))
+                best = cur if best is None or cur[1] < best[1] else best
+            return best
+
+        tern = TernaryDecoder(cfg)
+        t_ttft, t_dec = measure(tern)
+        dense = TernaryDecoder(cfg, dense=True, weights=tern.weights)
+        d_ttft, d_dec = measure(dense)
+        out["decode_3p9b"] = {"params": cfg.n_params(), "prompt": 64, "generated": 64,
+                              "ternary_tokens_per_s": round(64 / t_dec * 1e3, 1),
+                              "fp16_cublas_tokens_per_s": round(64 / d_dec * 1e3, 1),
+                              "decode_speedup_vs_fp16": round(d_dec / t_dec, 3),
+                              "ternary_ttft_ms": round(t_ttft, 3), "fp16_cublas_ttft_ms": round(d_ttft, 3),
+                              "ternary_bytes_per_token": cfg.ternary_bytes() + cfg.vocab * cfg.d_model * 2}
+        del tern, dense
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, rank, world, dist):
     import torch
     import paper_2506_23025_b200 as tp
@@ -291,6 +393,8 @@ def run_ours(args, rank, world, dist):
             del st, g, dws
             torch.cuda.empty_cache()
 
+    extras = run_extras(args, ws) if (rank == 0 and world == 1 and args.extras) else {}
+
     line = None
     if rank == 0:
         cpu = CpuReference(os.cpu_count() or 1).sample(args.cpu_seconds)
@@ -319,6 +423,7 @@ def run_ours(args, rank, world, dist):
             "gpu_launches": stack.launches * args.steps,
             "clocks": clk.summary(),
             "sweep": sweep,
+            **extras,
         }
         print(json.dumps(line), flush=True)
     return line
