@@ -445,3 +445,21 @@ def test_linear_chain_matches_per_layer(tp, batch, dtype):
     torch.cuda.synchronize()
     assert torch.isfinite(ref).all()
     assert torch.equal(st.out, ref)   # same kernel math, same fixed reduction order
+
+
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
+@pytest.mark.parametrize("rows,cols", [(37, 1500), (640, 11008), (4096, 4096)])
+@pytest.mark.parametrize("batch", [1, 2, 8])
+@pytest.mark.parametrize("ctas", [0, 5])
+def test_gemv_uniform_scale_vs_oracle(tp, dtype, rows, cols, batch, ctas):
+    # per-channel gamma (one scale per row): the GEMV applies the scale once per tile
+    tdt = getattr(torch, dtype)
+    rng = np.random.default_rng(rows + cols + batch + ctas)
+    payload, scales = _rand_packed(rng, rows, cols, per_block=False)
+    pm = tp.PackedMatrix(rows=rows, cols=cols, fmt=tp.DType.TQ2, payload=payload, scales=scales)
+    w = pm.to_device()
+    assert w.uniform_scale
+    x = torch.from_numpy(rng.uniform(-1, 1, size=(batch, cols)).astype(np.float32)).to(tdt).cuda()
+    y = tp.linear(x, w, path="gemv", ctas=ctas).float().cpu().numpy()
+    ref = _oracle_ref(payload, scales, cols, 2, x.float().cpu().numpy())
+    assert rel_err(y, ref) <= (2e-3 if dtype == "float16" else 6e-3)
