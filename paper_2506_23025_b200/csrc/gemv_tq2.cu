@@ -429,6 +429,11 @@ __global__ void __launch_bounds__(GemvCfg<NT>::kWarps * 32, 1) k_gemv_tq2(const 
       u += n;
     }
     stamp(4);
+    if (trace && lane == 0) {   // per-warp loop end (development trace)
+      uint64_t t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      reinterpret_cast<uint64_t*>(a.l0.y)[148 * 8 + blockIdx.x * 32 + warp] = t;
+    }
     if (cur >= 0) close_tile(cur);
 #pragma unroll
     for (int t = 0; t < NT; ++t)
@@ -437,19 +442,23 @@ __global__ void __launch_bounds__(GemvCfg<NT>::kWarps * 32, 1) k_gemv_tq2(const 
 
     // ---- boundary tiles: combine the parked fragments in fixed (warp, slot) order and store
     __syncthreads();
+    stamp(6);
+    // slot tags in registers (lane q holds slot q): owner search and matching by ballot, and
+    // the fragment loads issued together -- a serial walk over shared memory cost ~2 us here
+    const int my_tag = lane < 2 * kWarps ? slot_tile[lane] : -1;
     for (int i = warp; i < 2 * kWarps; i += kWarps) {
-      const int tile = slot_tile[i];
+      const int tile = __shfl_sync(0xffffffffu, my_tag, i);
       if (tile < 0) continue;
-      bool owner = true;   // the lowest slot holding this tile does the reduction
-      for (int q = 0; q < i; ++q) owner &= (slot_tile[q] != tile);
-      if (!owner) continue;
+      const unsigned match = __ballot_sync(0xffffffffu, my_tag == tile);
+      if (match & ((1u << i) - 1u)) continue;   // a lower slot holds this tile: it reduces
       float v[NT][4];
 #pragma unroll
       for (int t = 0; t < NT; ++t)
 #pragma unroll
         for (int e = 0; e < 4; ++e) v[t][e] = 0.0f;
-      for (int q = i; q < 2 * kWarps; ++q) {
-        if (slot_tile[q] != tile) continue;
+#pragma unroll
+      for (int q = 0; q < 2 * kWarps; ++q) {   // fixed slot order: deterministic
+        if (!((match >> q) & 1u)) continue;
         const float* src = red + q * kFrag;
 #pragma unroll
         for (int t = 0; t < NT; ++t)
