@@ -126,8 +126,11 @@ __device__ __forceinline__ uint4 ld_cg_x8(const T* row, int64_t k, int cols, int
 }
 
 // Shared-memory plan: [barriers, slot tags | reduction slots | C | staged x | per-warp weight rings].
-template <int NT> struct GemvCfg {
-  static constexpr int kWarps = NT >= 4 ? 8 : 16;      // warps per CTA
+// NW warps per CTA: 16 (one CTA per SM) for long per-CTA ranges; 8 with <= 128 registers
+// so that two CTAs fit per SM and a PDL-chained next layer starts (and prefetches its
+// weights) while this one computes -- the better trade for small layers.
+template <int NT, int NW> struct GemvCfg {
+  static constexpr int kWarps = NW;     // warps per CTA
   static constexpr int kSU = NT == 1 ? 4 : 2;          // units (1056 B) per bulk copy = one ring slot
   static constexpr int kFrag = NT * 4 * 32;            // floats of one warp's tile fragment
   static constexpr int kSlotBytes = kSU * kUnitBytes;
@@ -165,9 +168,9 @@ __device__ __forceinline__ uint4 load_x8(const T* row, int64_t k, int cols, int 
 }
 
 // XS: activations staged in shared memory (when they fit), else read through L1
-template <typename T, int NT, bool XS>
-__global__ void __launch_bounds__(GemvCfg<NT>::kWarps * 32, 1) k_gemv_tq2(const GemvArgs a) {
-  using Cfg = GemvCfg<NT>;
+template <typename T, int NT, bool XS, int NW>
+__global__ void __launch_bounds__(NW * 32, (NW == 8 && NT == 1) ? 2 : 1) k_gemv_tq2(const GemvArgs a) {
+  using Cfg = GemvCfg<NT, NW>;
   constexpr int kFrag = Cfg::kFrag, kWarps = Cfg::kWarps, kSlotBytes = Cfg::kSlotBytes, kSU = Cfg::kSU;
   const int NS = a.ns;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -489,18 +492,18 @@ size_t gemv_workspace_bytes(int, int, int) { return 0; }   // the GEMV needs no 
 
 constexpr size_t kXsBudget = 128 * 1024;  // stage activations in smem up to this size (if the whole plan fits)
 
-template <int NT>
+template <int NT, int NW>
 static int gemv_ns(int n_tiles, int nb, int grid) {
-  using Cfg = GemvCfg<NT>;
+  using Cfg = GemvCfg<NT, NW>;
   const int tiles_max = (int)ceil_div(n_tiles, grid);
   const int ops = (int)ceil_div(ceil_div((int64_t)tiles_max * nb, Cfg::kWarps), Cfg::kSU);
   const int ns_max = kNSMax * 2 / Cfg::kSU;   // <= 8 units (8.4 KB) in flight per warp
   return ops >= ns_max ? ns_max : ops > 1 ? 2 : 1;
 }
 
-template <typename T, int NT, bool XS>
+template <typename T, int NT, bool XS, int NW>
 static int launch_gemv_x(const GemvArgs& a, int grid, int pdl, bool coop, cudaStream_t st) {
-  auto kern = k_gemv_tq2<T, NT, XS>;
+  auto kern = k_gemv_tq2<T, NT, XS, NW>;
   static int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -508,7 +511,7 @@ static int launch_gemv_x(const GemvArgs& a, int grid, int pdl, bool coop, cudaSt
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured_dev = dev;
   }
-  using Cfg = GemvCfg<NT>;
+  using Cfg = GemvCfg<NT, NW>;
   const int nrx = a.batch < 8 * NT ? a.batch : 8 * NT;
   const size_t smem = Cfg::smem(a.nb_max, nrx, XS, a.ns);
   if (smem > 227 * 1024) {
@@ -542,29 +545,34 @@ static int launch_gemv_x(const GemvArgs& a, int grid, int pdl, bool coop, cudaSt
   return 0;
 }
 
-template <int NT>
+template <int NT, int NW>
 static bool xs_fits(int batch, int nb_max, int ns) {
   const int nrx = batch < 8 * NT ? batch : 8 * NT;
-  return (size_t)nrx * GemvCfg<NT>::x_stride(nb_max) <= kXsBudget &&
-         GemvCfg<NT>::smem(nb_max, nrx, true, ns) <= 227 * 1024;
+  return (size_t)nrx * GemvCfg<NT, NW>::x_stride(nb_max) <= kXsBudget &&
+         GemvCfg<NT, NW>::smem(nb_max, nrx, true, ns) <= 227 * 1024;
 }
 
-template <typename T, int NT>
+template <typename T, int NT, int NW>
 static int launch_gemv(GemvArgs& a, int grid, int pdl, bool coop, cudaStream_t st) {
-  if (xs_fits<NT>(a.batch, a.nb_max, a.ns)) return launch_gemv_x<T, NT, true>(a, grid, pdl, coop, st);
+  if (xs_fits<NT, NW>(a.batch, a.nb_max, a.ns)) return launch_gemv_x<T, NT, true, NW>(a, grid, pdl, coop, st);
   if (coop) {
     set_error("tr_linear_chain: activations of %d blocks x batch %d do not fit in shared memory", a.nb_max, a.batch);
     return -1;
   }
-  return launch_gemv_x<T, NT, false>(a, grid, pdl, coop, st);
+  return launch_gemv_x<T, NT, false, NW>(a, grid, pdl, coop, st);
 }
+
+// units per CTA at or below which the 8-warp, two-CTAs-per-SM variant wins (measured)
+constexpr int kSmallCtaUnits = 48;
+static bool small_variant(int n_tiles, int nb, int grid) { return (int64_t)ceil_div(n_tiles, grid) * nb <= kSmallCtaUnits; }
 
 // true when the GEMV can stage this batch's activations in shared memory (its fast path)
 bool gemv_stages_x(int batch, int rows, int cols) {
   if (batch > 8) return false;
   const int nb = (int)ceil_div(cols, kBlock), n_tiles = (int)ceil_div(rows, 16);
   const int grid = sm_count() < n_tiles ? sm_count() : n_tiles;
-  return xs_fits<1>(batch, nb, gemv_ns<1>(n_tiles, nb, grid));
+  if (small_variant(n_tiles, nb, grid)) return xs_fits<1, 8>(batch, nb, gemv_ns<1, 8>(n_tiles, nb, grid));
+  return xs_fits<1, 16>(batch, nb, gemv_ns<1, 16>(n_tiles, nb, grid));
 }
 
 static GemvLayer make_layer(const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int rows, int cols) {
@@ -597,17 +605,24 @@ int gemv_tq2(int act, const void* w, const void* x, void* y, int64_t ldx, int64_
   int grid = ctas > 0 ? ctas : sm_count();
   if (grid > a.l0.n_tiles) grid = a.l0.n_tiles;
   const int nt = batch <= 8 ? 1 : (batch <= 16 ? 2 : 4);
-  if (nt == 1) a.ns = gemv_ns<1>(a.l0.n_tiles, a.l0.nb, grid);
-  else if (nt == 2) a.ns = gemv_ns<2>(a.l0.n_tiles, a.l0.nb, grid);
-  else a.ns = gemv_ns<4>(a.l0.n_tiles, a.l0.nb, grid);
-  if (act == kActF16) {
-    if (nt == 1) return launch_gemv<__half, 1>(a, grid, pdl, false, st);
-    if (nt == 2) return launch_gemv<__half, 2>(a, grid, pdl, false, st);
-    return launch_gemv<__half, 4>(a, grid, pdl, false, st);
+  const bool small = small_variant(a.l0.n_tiles, a.l0.nb, grid);
+  const bool bf = act != kActF16;
+  if (nt == 1 && small) {
+    a.ns = gemv_ns<1, 8>(a.l0.n_tiles, a.l0.nb, grid);
+    return bf ? launch_gemv<__nv_bfloat16, 1, 8>(a, grid, pdl, false, st) : launch_gemv<__half, 1, 8>(a, grid, pdl, false, st);
   }
-  if (nt == 1) return launch_gemv<__nv_bfloat16, 1>(a, grid, pdl, false, st);
-  if (nt == 2) return launch_gemv<__nv_bfloat16, 2>(a, grid, pdl, false, st);
-  return launch_gemv<__nv_bfloat16, 4>(a, grid, pdl, false, st);
+  if (nt == 1) {
+    a.ns = gemv_ns<1, 16>(a.l0.n_tiles, a.l0.nb, grid);
+    return bf ? launch_gemv<__nv_bfloat16, 1, 16>(a, grid, pdl, false, st)
+              : launch_gemv<__half, 1, 16>(a, grid, pdl, false, st);
+  }
+  if (nt == 2) {
+    a.ns = gemv_ns<2, 16>(a.l0.n_tiles, a.l0.nb, grid);
+    return bf ? launch_gemv<__nv_bfloat16, 2, 16>(a, grid, pdl, false, st)
+              : launch_gemv<__half, 2, 16>(a, grid, pdl, false, st);
+  }
+  a.ns = gemv_ns<4, 8>(a.l0.n_tiles, a.l0.nb, grid);
+  return bf ? launch_gemv<__nv_bfloat16, 4, 8>(a, grid, pdl, false, st) : launch_gemv<__half, 4, 8>(a, grid, pdl, false, st);
 }
 
 // A chain of products y_l = x_l W_l^T in ONE persistent cooperative launch (batch <= 8):
@@ -632,11 +647,11 @@ int gemv_chain(int act, const TrChainLayer* host_layers, void* dev_table, int n_
     tab[l] = make_layer(h.w, h.x, h.y, h.ldx, h.ldy, (int)h.rows, (int)h.cols);
     if (tab[l].nb > a.nb_max) a.nb_max = tab[l].nb;
     if (tab[l].n_tiles < tiles_min) tiles_min = tab[l].n_tiles;
-    const int n = gemv_ns<1>(tab[l].n_tiles, tab[l].nb, grid);
+    const int n = gemv_ns<1, 16>(tab[l].n_tiles, tab[l].nb, grid);
     if (n < ns) ns = n;
   }
   a.ns = ns < 2 ? 2 : ns;
-  if (!xs_fits<1>(batch, a.nb_max, a.ns)) a.ns = 1;   // wide activations: a shallower weight ring
+  if (!xs_fits<1, 16>(batch, a.nb_max, a.ns)) a.ns = 1;   // wide activations: a shallower weight ring
   a.l0 = tab[0];
   if (upload) {   // synchronous, outside any stream capture (tr_linear_chain_prepare)
     cudaError_t e = cudaMemcpy(dev_table, tab.data(), sizeof(GemvLayer) * n_layers, cudaMemcpyHostToDevice);
@@ -646,8 +661,8 @@ int gemv_chain(int act, const TrChainLayer* host_layers, void* dev_table, int n_
     }
     return 0;
   }
-  if (act == kActF16) return launch_gemv<__half, 1>(a, grid, pdl, true, st);
-  return launch_gemv<__nv_bfloat16, 1>(a, grid, pdl, true, st);
+  if (act == kActF16) return launch_gemv<__half, 1, 16>(a, grid, pdl, true, st);
+  return launch_gemv<__nv_bfloat16, 1, 16>(a, grid, pdl, true, st);
 }
 
 size_t gemv_chain_table_bytes(int n_layers) { return sizeof(GemvLayer) * (size_t)n_layers; }
