@@ -104,6 +104,18 @@ TR_API int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t bat
                      int act_dtype, int64_t ldx, int64_t ldy, int flags, void* workspace, size_t ws_bytes,
                      void* stream);
 
+/* tr_linear with the producer of x fused into the GEMV's activation staging (decode glue;
+ * batch 1..8, TQ2, activations that fit in shared memory -- else -1):
+ *  TR_PRE_ADD_RMSNORM: x_eff = rmsnorm(x + delta) * gamma (delta may be NULL); x + delta
+ *     (rounded) is also stored to x_out [batch, cols] (stride ldx) -- must not alias x;
+ *  TR_PRE_SILU_MUL:    x_eff = silu(x[:, :cols]) * x[:, cols:2 cols]  (x = gate|up, ldx >= 2 cols).
+ * Same arithmetic and roundings as tr_add_rmsnorm / tr_silu_mul followed by tr_linear. */
+#define TR_PRE_ADD_RMSNORM 1
+#define TR_PRE_SILU_MUL 2
+TR_API int tr_linear_pre(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
+                         int act_dtype, int64_t ldx, int64_t ldy, int flags, int pre_op, const void* delta,
+                         const void* gamma, void* x_out, float eps, void* stream);
+
 /* One product of a chain (tr_linear_chain): y[batch, rows] = x[batch, cols] @ W^T, TQ2 device layout. */
 typedef struct {
   const void* w;

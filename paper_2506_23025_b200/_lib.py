@@ -23,6 +23,8 @@ LINEAR_PDL = 1
 LINEAR_UNIFORM_SCALE = 2
 LINEAR_FORCE_UMMA = 4
 LINEAR_FORCE_GEMV = 8
+PRE_ADD_RMSNORM = 1
+PRE_SILU_MUL = 2
 
 _lock = threading.Lock()
 _lib = None
@@ -56,6 +58,8 @@ _SIGS = {
     "tr_linear_workspace_size": ([_int, _i64, _i64, _i64], ctypes.c_size_t),
     "tr_linear": ([_int, _c_p, _c_p, _c_p, _i64, _i64, _i64, _int, _i64, _i64, _int, _c_p, ctypes.c_size_t,
                    _c_p], _int),
+    "tr_linear_pre": ([_int, _c_p, _c_p, _c_p, _i64, _i64, _i64, _int, _i64, _i64, _int, _int, _c_p, _c_p, _c_p,
+                       ctypes.c_float, _c_p], _int),
     "tr_linear_chain_workspace_size": ([_i64], ctypes.c_size_t),
     "tr_linear_chain_prepare": ([ctypes.POINTER(TrChainLayer), _i64, _i64, _c_p, ctypes.c_size_t], _int),
     "tr_linear_chain": ([_int, ctypes.POINTER(TrChainLayer), _i64, _i64, _int, _c_p, ctypes.c_size_t, _c_p], _int),

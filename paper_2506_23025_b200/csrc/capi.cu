@@ -28,7 +28,8 @@ int check_launch(const char* what) {
 }
 
 int gemv_tq2(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
-             int cols, int ctas, int pdl, cudaStream_t st);
+             int cols, int ctas, int pdl, cudaStream_t st, int pre, const void* pre_delta, const void* pre_gamma,
+             void* pre_out, float eps);
 size_t gemv_workspace_bytes(int batch, int rows, int cols);
 int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
               int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg);
@@ -94,10 +95,24 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
   for (int64_t n0 = 0; n0 < batch; n0 += 32) {
     const int nb_ = (int)(batch - n0 < 32 ? batch - n0 : 32);
     int rc = gemv_tq2(act_dtype, w, (const uint8_t*)x + n0 * ldx * esz, (uint8_t*)y + n0 * ldy * esz, ldx, ldy, nb_,
-                      (int)rows, (int)cols, knob, pdl, st);
+                      (int)rows, (int)cols, knob, pdl, st, 0, nullptr, nullptr, nullptr, 0.0f);
     if (rc) return rc;
   }
   return 0;
+}
+
+int tr_linear_pre(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
+                  int act_dtype, int64_t ldx, int64_t ldy, int flags, int pre_op, const void* delta, const void* gamma,
+                  void* x_out, float eps, void* stream) {
+  TR_REQUIRE(fmt == kFmtTq2, "tr_linear_pre: TQ2 only");
+  TR_REQUIRE(act_dtype == kActF16 || act_dtype == kActBf16, "tr_linear_pre: act_dtype must be F16(1) or BF16(2)");
+  TR_REQUIRE(pre_op == TR_PRE_ADD_RMSNORM || pre_op == TR_PRE_SILU_MUL, "tr_linear_pre: bad pre_op %d", pre_op);
+  TR_REQUIRE(pre_op != TR_PRE_ADD_RMSNORM || gamma != nullptr, "tr_linear_pre: RMSNorm needs gamma");
+  TR_REQUIRE(batch >= 1 && batch <= 8 && rows >= 1 && cols >= 1, "tr_linear_pre: 1 <= batch <= 8");
+  TR_REQUIRE(ldx >= (pre_op == TR_PRE_SILU_MUL ? 2 * cols : cols) && ldy >= rows, "tr_linear_pre: leading dimensions");
+  TR_REQUIRE(((uintptr_t)w & 15) == 0, "tr_linear_pre: weight buffer must be 16-byte aligned");
+  return gemv_tq2(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, (flags >> 8) & 0xFFFF,
+                  flags & TR_LINEAR_PDL, (cudaStream_t)stream, pre_op, delta, gamma, x_out, eps);
 }
 
 size_t tr_linear_chain_workspace_size(int64_t n_layers) {

@@ -93,6 +93,14 @@ struct GemvArgs {
   int batch;
   int ns;                        // ring slots per warp
   int dbg;                       // development probe: 2 = per-CTA timestamps into y
+  // fused producer of x (decode glue folded into the staging, single layer + XS only):
+  // 1: x = rmsnorm(x + delta) * gamma, CTA 0 also stores x + delta to x_out (the residual);
+  // 2: x = silu(x[:, :cols]) * x[:, cols:2 cols] (SwiGLU of a gate|up product)
+  int pre;
+  const void* pre_delta;
+  const void* pre_gamma;
+  void* pre_out;
+  float eps;
 };
 
 // Sense-reversal grid barrier for the persistent chain (all CTAs are co-resident: the
@@ -168,6 +176,98 @@ __device__ __forceinline__ uint4 load_x8(const T* row, int64_t k, int cols, int 
 }
 
 // XS: activations staged in shared memory (when they fit), else read through L1
+__device__ __forceinline__ float tof(__half v) { return __half2float(v); }
+__device__ __forceinline__ float tof(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T>
+__device__ __forceinline__ void f8_from(const uint4& v, float (&f)[8]) {
+  const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = tof(e[i]);
+}
+template <typename T>
+__device__ __forceinline__ uint4 f8_to(const float (&f)[8]) {
+  uint4 v;
+  T* e = reinterpret_cast<T*>(&v);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) e[i] = Act<T>::from_float(f[i]);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ float rnd(float v) { return tof(Act<T>::from_float(v)); }   // round through T
+
+// Fused decode glue (GemvArgs::pre): writes the producer's output straight into the
+// staged-activation buffer xs (same arithmetic and roundings as tr_add_rmsnorm /
+// tr_silu_mul).  scratch: >= nb * 8 floats (the boundary-reduction buffer, free here).
+template <typename T, typename Ly_t>
+__device__ void stage_pre(const GemvArgs& a, const Ly_t& Ly, uint8_t* xs, int rs, float* scratch, int nrx) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nb = Ly.nb, cols = Ly.cols;
+  const T* xg = reinterpret_cast<const T*>(Ly.x);
+  auto at = [&](int n, int kb) { return xs + n * rs + kb * kXBlk + (lane >> 3) * kXChunk + (lane & 7) * 16; };
+  for (int item = warp; item < nb * nrx; item += nw) {
+    const int kb = item / nrx, n = item % nrx;
+    const int64_t kx = (int64_t)kb * kBlock + lane * 8;
+    float f[8];
+    if (a.pre == 2) {   // silu(gate) * up
+      float g[8], u[8];
+      f8_from<T>(load_x8(xg + n * Ly.ldx, kx, cols, Ly.x_vec), g);
+      f8_from<T>(load_x8(xg + n * Ly.ldx + cols, kx, cols, Ly.x_vec), u);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) f[e] = kx + e < cols ? rnd<T>(g[e] / (1.0f + __expf(-g[e]))) * u[e] : 0.0f;
+      *reinterpret_cast<uint4*>(at(n, kb)) = f8_to<T>(f);
+    } else {            // residual add, stored rounded; sum of squares per (block, row)
+      f8_from<T>(load_x8(xg + n * Ly.ldx, kx, cols, Ly.x_vec), f);
+      if (a.pre_delta) {
+        float d[8];
+        f8_from<T>(load_x8(reinterpret_cast<const T*>(a.pre_delta) + n * Ly.ldx, kx, cols, Ly.x_vec), d);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] = rnd<T>(f[e] + d[e]);
+      }
+      const uint4 hv = f8_to<T>(f);
+      *reinterpret_cast<uint4*>(at(n, kb)) = hv;
+      if (blockIdx.x == 0 && a.pre_out && kx < cols) {
+        T* o = reinterpret_cast<T*>(a.pre_out) + n * Ly.ldx + kx;
+        if (kx + 8 <= cols && Ly.x_vec) {
+          *reinterpret_cast<uint4*>(o) = hv;
+        } else {
+          const T* he = reinterpret_cast<const T*>(&hv);
+          for (int e = 0; e < 8 && kx + e < cols; ++e) o[e] = he[e];
+        }
+      }
+      float ss = 0.0f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ss += f[e] * f[e];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) scratch[kb * 8 + n] = ss;
+    }
+  }
+  __syncthreads();
+  if (a.pre != 1) return;
+  float* inv = scratch + nb * 8;   // per row: rsqrt(mean(h^2) + eps), fixed-order sums
+  for (int n = warp; n < nrx; n += nw) {
+    float ss = 0.0f;
+    for (int kb = lane; kb < nb; kb += 32) ss += scratch[kb * 8 + n];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) inv[n] = rsqrtf(ss / cols + a.eps);
+  }
+  __syncthreads();
+  const T* gam = reinterpret_cast<const T*>(a.pre_gamma);
+  for (int item = warp; item < nb * nrx; item += nw) {
+    const int kb = item / nrx, n = item % nrx;
+    const int64_t kx = (int64_t)kb * kBlock + lane * 8;
+    float f[8], g[8];
+    f8_from<T>(*reinterpret_cast<const uint4*>(at(n, kb)), f);
+    f8_from<T>(load_x8(gam, kx, cols, Ly.x_vec), g);
+    const float iv = inv[n];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = rnd<T>(f[e] * iv) * g[e];
+    *reinterpret_cast<uint4*>(at(n, kb)) = f8_to<T>(f);
+  }
+  __syncthreads();
+}
+
 template <typename T, int NT, bool XS, int NW>
 __global__ void __launch_bounds__(NW * 32, (NW == 8 && NT == 1) ? 2 : 1) k_gemv_tq2(const GemvArgs a) {
   using Cfg = GemvCfg<NT, NW>;
@@ -270,12 +370,18 @@ __global__ void __launch_bounds__(NW * 32, (NW == 8 && NT == 1) ? 2 : 1) k_gemv_
     // ---- per-(block, row) correction C = sum_k x_k (1 + base / m_j(k)); stages x (XS) or warms L1
     const T* xg = reinterpret_cast<const T*>(Ly.x);
     const int rs = Cfg::x_stride(nb);
+    if (XS && a.pre) stage_pre<T>(a, Ly, xs, rs, red, nrx);   // fused glue: xs already holds x
     for (int item = warp; item < nb * nrx; item += kWarps) {
       const int kb = item / nrx, n = item % nrx;
       const int64_t kx = (int64_t)kb * kBlock + lane * 8;
-      const uint4 v = chain ? ld_cg_x8(xg + n * Ly.ldx, kx, Ly.cols, Ly.x_vec)
-                            : load_x8(xg + n * Ly.ldx, kx, Ly.cols, Ly.x_vec);
-      if (XS) *reinterpret_cast<uint4*>(xs + n * rs + kb * kXBlk + (lane >> 3) * kXChunk + (lane & 7) * 16) = v;
+      uint4 v;
+      uint8_t* xsp = xs + n * rs + kb * kXBlk + (lane >> 3) * kXChunk + (lane & 7) * 16;
+      if (XS && a.pre) {
+        v = *reinterpret_cast<const uint4*>(xsp);
+      } else {
+        v = chain ? ld_cg_x8(xg + n * Ly.ldx, kx, Ly.cols, Ly.x_vec) : load_x8(xg + n * Ly.ldx, kx, Ly.cols, Ly.x_vec);
+        if (XS) *reinterpret_cast<uint4*>(xsp) = v;
+      }
       // chunk column (8 lane + e) % 64 has field class j = (col >> 2) & 3
       const int ja = (2 * lane) & 3, jb = ja + 1;
       const float fa = 1.0f + Frag<T>::kBase * Frag<T>::inv_f(ja), fb = 1.0f + Frag<T>::kBase * Frag<T>::inv_f(jb);
@@ -592,8 +698,18 @@ static GemvLayer make_layer(const void* w, const void* x, void* y, int64_t ldx, 
 }
 
 int gemv_tq2(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
-             int cols, int ctas, int pdl, cudaStream_t st) {
+             int cols, int ctas, int pdl, cudaStream_t st, int pre, const void* pre_delta, const void* pre_gamma,
+             void* pre_out, float eps) {
   GemvArgs a = {};
+  a.pre = pre;
+  a.pre_delta = pre_delta;
+  a.pre_gamma = pre_gamma;
+  a.pre_out = pre_out;
+  a.eps = eps;
+  if (pre && (batch > 8 || !gemv_stages_x(batch, rows, cols))) {
+    set_error("tr_linear_pre: fused producers need batch <= 8 and activations that fit in shared memory");
+    return -1;
+  }
   a.dbg = (ctas >> 12) & 0xF;
   ctas &= 0xFFF;
   a.l0 = make_layer(w, x, y, ldx, ldy, rows, cols);

@@ -28,7 +28,7 @@ import torch
 import torch.nn.functional as F
 
 from . import _lib
-from .device import _ACT, TernaryWeight, linear
+from .device import _ACT, TernaryWeight, linear, linear_pre
 
 
 @dataclass(frozen=True)
@@ -141,10 +141,13 @@ class TernaryDecoder:
         return F.linear(h, self.weights["lm_head"])[0]
 
     def _forward_fused(self, tokens, pos):
-        """Same computation with the glue as single kernels (tr_add_rmsnorm / tr_attn_decode /
-        tr_silu_mul; tr_rope_kv for the prompt): 7 launches per layer at decode."""
+        """Same computation with the glue as single kernels.  Decode (T = 1) of the ternary
+        model folds residual-add + RMSNorm into the QKV / gate|up GEMVs and SwiGLU into the
+        down GEMV (tr_linear_pre): 5 launches per layer."""
         cfg, act, st = self.cfg, _ACT[self.dtype], _lib.stream_handle()
         T, d, H, D, S = tokens.shape[0], cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.max_seq
+        if T == 1 and not self.dense:
+            return self._decode_step_fused(tokens, pos)
         h = self.weights["embed"][tokens].contiguous()
         xn = torch.empty_like(h)
         q = torch.empty((T, H, D), device=self.device, dtype=self.dtype)
@@ -177,6 +180,30 @@ class TernaryDecoder:
         _lib.call("tr_add_rmsnorm", act, h.data_ptr(), delta.data_ptr(), self.norm_out.data_ptr(), xn.data_ptr(),
                   T, d, cfg.eps, st)
         return F.linear(xn[-1:], self.weights["lm_head"])[0]
+
+    def _decode_step_fused(self, tokens, pos):
+        cfg, act, st = self.cfg, _ACT[self.dtype], _lib.stream_handle()
+        d, H, D, S = cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.max_seq
+        hs = [self.weights["embed"][tokens].contiguous(), torch.empty((1, d), device=self.device, dtype=self.dtype)]
+        cur, delta = 0, None
+        for i in range(cfg.n_layers):
+            lw = self.lin[i]
+            # residual stream ping-pongs: the GEMV reads hs[cur] and stores hs[cur] + delta to hs[1 - cur]
+            qkv = linear_pre(hs[cur], lw["qkv"], _lib.PRE_ADD_RMSNORM, delta, self.norm_attn[i], hs[1 - cur],
+                             cfg.eps, pdl=True)
+            cur = 1 - cur
+            att = torch.empty((1, d), device=self.device, dtype=self.dtype)
+            _lib.call("tr_attn_decode", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(), self.sin.data_ptr(),
+                      self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(), H, D, S, D ** -0.5, st)
+            o = linear(att, lw["o"], pdl=True)
+            gu = linear_pre(hs[cur], lw["gate_up"], _lib.PRE_ADD_RMSNORM, o, self.norm_mlp[i], hs[1 - cur],
+                            cfg.eps, pdl=True)
+            cur = 1 - cur
+            delta = linear_pre(gu, lw["down"], _lib.PRE_SILU_MUL, pdl=True)
+        xn = torch.empty((1, d), device=self.device, dtype=self.dtype)
+        _lib.call("tr_add_rmsnorm", act, hs[cur].data_ptr(), delta.data_ptr(), self.norm_out.data_ptr(), xn.data_ptr(),
+                  1, d, cfg.eps, st)
+        return F.linear(xn, self.weights["lm_head"])[0]
 
     # -- serving --------------------------------------------------------------------------
     def prefill(self, prompt: torch.Tensor) -> None:

@@ -158,6 +158,26 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
     return out
 
 
+def linear_pre(x: torch.Tensor, w: TernaryWeight, pre: int, delta: torch.Tensor | None = None,
+               gamma: torch.Tensor | None = None, x_out: torch.Tensor | None = None, eps: float = 1e-5,
+               out: torch.Tensor | None = None, pdl: bool = False) -> torch.Tensor:
+    """``linear`` with the producer of its input fused into the GEMV's activation staging.
+
+    pre = _lib.PRE_ADD_RMSNORM: y = rmsnorm(x + delta) * gamma @ W^T, and x + delta is
+    written to ``x_out`` (the residual stream; must not alias x).  pre = _lib.PRE_SILU_MUL:
+    y = (silu(x[:, :cols]) * x[:, cols:]) @ W^T for a gate|up product x.  Batch 1..8.
+    """
+    x2 = x.reshape(-1, x.shape[-1])
+    batch = x2.shape[0]
+    if out is None:
+        out = torch.empty((batch, w.rows), dtype=x.dtype, device=x.device)
+    ptr = lambda t: 0 if t is None else t.data_ptr()
+    _lib.call("tr_linear_pre", int(w.fmt), w.data.data_ptr(), x2.data_ptr(), out.data_ptr(), batch, w.rows, w.cols,
+              _ACT[x.dtype], x2.stride(0), out.stride(0), _lib.LINEAR_PDL if pdl else 0, int(pre), ptr(delta),
+              ptr(gamma), ptr(x_out), float(eps), _lib.stream_handle())
+    return out
+
+
 class TernaryLinear(torch.nn.Module):
     """nn.Linear-shaped module over a TernaryWeight (no bias, like the paper's BitLinear layers)."""
 

@@ -466,3 +466,37 @@ def test_gemv_uniform_scale_vs_oracle(tp, dtype, rows, cols, batch, ctas):
     y = tp.linear(x, w, path="gemv", ctas=ctas).float().cpu().numpy()
     ref = _oracle_ref(payload, scales, cols, 2, x.float().cpu().numpy())
     assert rel_err(y, ref) <= (2e-3 if dtype == "float16" else 6e-3)
+
+
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
+@pytest.mark.parametrize("batch", [1, 3])
+def test_linear_pre_fused_producers(tp, dtype, batch):
+    # tr_linear_pre == standalone glue kernel followed by tr_linear (same roundings)
+    from paper_2506_23025_b200 import _lib
+    from paper_2506_23025_b200.device import _ACT, linear_pre
+
+    tdt = getattr(torch, dtype)
+    g = torch.Generator(device="cuda").manual_seed(batch)
+    d, f = 3072, 9216
+    w_qkv = tp.TernaryWeight.from_float(torch.randn(3 * d, d, generator=g, device="cuda"))
+    w_down = tp.TernaryWeight.from_float(torch.randn(d, f, generator=g, device="cuda"))
+    h = (torch.randn(batch, d, generator=g, device="cuda")).to(tdt)
+    delta = (torch.randn(batch, d, generator=g, device="cuda")).to(tdt)
+    gamma = (torch.rand(d, generator=g, device="cuda") + 0.5).to(tdt)
+    st = _lib.stream_handle()
+    # reference: add + rmsnorm kernel, then the plain linear
+    h_ref, xn = h.clone(), torch.empty_like(h)
+    _lib.call("tr_add_rmsnorm", _ACT[tdt], h_ref.data_ptr(), delta.data_ptr(), gamma.data_ptr(), xn.data_ptr(),
+              batch, d, 1e-5, st)
+    ref = tp.linear(xn, w_qkv).float()
+    h_out = torch.empty_like(h)
+    y = linear_pre(h, w_qkv, _lib.PRE_ADD_RMSNORM, delta, gamma, h_out).float()
+    assert torch.equal(h_out, h_ref)   # the residual stream, bit for bit
+    assert ((y - ref).abs().amax(1) / ref.abs().amax(1)).max().item() <= 3e-3
+    # SwiGLU producer
+    gu = (torch.randn(batch, 2 * f, generator=g, device="cuda")).to(tdt)
+    a = torch.empty((batch, f), dtype=tdt, device="cuda")
+    _lib.call("tr_silu_mul", _ACT[tdt], gu.data_ptr(), a.data_ptr(), batch, f, st)
+    ref2 = tp.linear(a, w_down)
+    y2 = linear_pre(gu, w_down, _lib.PRE_SILU_MUL)
+    assert torch.equal(y2, ref2)   # identical staged activations -> identical product
