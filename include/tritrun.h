@@ -45,6 +45,7 @@ extern "C" {
 #define TR_LINEAR_UNIFORM_SCALE 2  /* bit 1: caller asserts each row has one scale for all its blocks */
 #define TR_LINEAR_FORCE_UMMA 4     /* bit 2: force the tcgen05 tensor-core GEMM */
 #define TR_LINEAR_FORCE_GEMV 8     /* bit 3: force the mma.sync GEMV */
+#define TR_LINEAR_GEMV_F16 16      /* bit 4: batch 1-2 on the fp16 GEMV instead of the int8-slice one */
 
 TR_API const char* tr_last_error(void);
 TR_API int tr_version(void);
@@ -98,7 +99,9 @@ TR_API size_t tr_linear_workspace_size(int fmt, int64_t batch, int64_t rows, int
 /* y[batch, rows] = x[batch, cols] @ W^T  (linear.py:137-166 gemm semantics with the
  * paper's fp16/bf16 activations, fp32 accumulation, RNE output).  w is the device
  * layout from tr_repack; x has leading dimension ldx, y has ldy (elements).
- * Batches >= 9 run the tcgen05 GEMM (K5), smaller ones the GEMV (K3).
+ * Batches >= 9 run the tcgen05 GEMM (K5), 3-8 the fp16 mma.sync GEMV (K3), 1-2 the
+ * int8-slice GEMV (K3-S8: exact integer block sums over activations put on a 2^-24 grid
+ * of each 256-column block's maximum).
  * flags: TR_LINEAR_* bits | (knob << 8): GEMV CTA count / GEMM K split (0 = automatic). */
 TR_API int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
                      int act_dtype, int64_t ldx, int64_t ldy, int flags, void* workspace, size_t ws_bytes,

@@ -13,7 +13,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtritrun.so")
+LIB_PATH = os.environ.get("TRITRUN_LIB") or os.path.join(HERE, "libtritrun.so")   # override: dev A/B builds
 
 FMT_TQ2 = 2   # blocks.DType.TQ2 (reference blocks.py:49-52)
 FMT_TQ1 = 3
@@ -23,6 +23,7 @@ LINEAR_PDL = 1
 LINEAR_UNIFORM_SCALE = 2
 LINEAR_FORCE_UMMA = 4
 LINEAR_FORCE_GEMV = 8
+LINEAR_GEMV_F16 = 16
 PRE_ADD_RMSNORM = 1
 PRE_SILU_MUL = 2
 

@@ -30,8 +30,10 @@ constexpr int kActF32 = 3;
 // cut into 16-row tiles t and 256-column blocks b; unit (t, b) is 1056 contiguous
 // bytes at offset (t * nb + b) * 1056 (tile-major, so a tile's K range is one
 // contiguous run that a single TMA bulk copy can fetch):
-//   bytes [0, 1024): 64 16-byte words; word u = half*32 + c*8 + g is chunk c
-//     (block columns 64c..64c+63) of row 16t + 8*half + g, encoded so that
+//   bytes [0, 1024): 64 16-byte words; word u = half*32 + c*8 + (g ^ 2c) is chunk c
+//     (block columns 64c..64c+63) of row 16t + 8*half + g (the XOR puts the 8 words an
+//     MMA quarter-warp reads -- rows g, g^1 of all 4 chunks -- in 8 distinct bank groups),
+//     encoded so that
 //     32-bit word w (0..3), bits 16h + 8hb + 2j (+1), hold the digit of chunk
 //     column 32*(w>>1) + 16hb + 4j + 2*(w&1) + h;
 //   bytes [1024, 1056): 8 half2 scale pairs (s[16t+g], s[16t+8+g]).
@@ -39,6 +41,7 @@ constexpr int kRowPad = 128;
 constexpr int kTileBlockBytes = 1024;
 constexpr int kTileScaleBytes = 32;
 constexpr int kUnitBytes = kTileBlockBytes + kTileScaleBytes;   // 1056
+__host__ __device__ inline int t16_word(int half, int c, int g) { return half * 32 + c * 8 + (g ^ (2 * c)); }
 
 // ---- T16-Q1 device layout for TQ1 (1.6 bit, 5 trits per byte) -------------------
 // Same tiling (16-row tiles x 256-column blocks, tile-major units, rows padded to 128),
@@ -149,10 +152,12 @@ template <typename T> struct Act;
 template <> struct Act<__half> {
   static constexpr int kId = kActF16;
   __device__ static __half from_float(float v) { return __float2half_rn(v); }
+  __device__ static float to_float(__half v) { return __half2float(v); }
 };
 template <> struct Act<__nv_bfloat16> {
   static constexpr int kId = kActBf16;
   __device__ static __nv_bfloat16 from_float(float v) { return __float2bfloat16_rn(v); }
+  __device__ static float to_float(__nv_bfloat16 v) { return __bfloat162float(v); }
 };
 
 }  // namespace tr

@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
         for (int m = 0; m < 7; ++m) wq[m] = ld_shared_u32(unit + rt * kQ1RowBytes + (half_k * 6 + m) * 4);
       } else {
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) wv[cc] = ld_shared_v4(unit + (hrow * 32 + (2 * half_k + cc) * 8 + g) * 16);
+        for (int cc = 0; cc < 2; ++cc) wv[cc] = ld_shared_v4(unit + t16_word(hrow, 2 * half_k + cc, g) * 16);
       }
       const uint32_t sv = ld_shared_u32(unit + Cfg::TBB + g * 4);
       const float s_cur = __half2float(hrow ? __high2half(*reinterpret_cast<const __half2*>(&sv))

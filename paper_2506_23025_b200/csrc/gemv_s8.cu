@@ -1,0 +1,588 @@
+// K3-S8: decode GEMV for batch 1-2 on the int8 tensor-core MMA, TQ2 weights.
+//
+// Semantics are K3's (reference linear.py:137-166, _kernels.pyx:136-168, paper App. F):
+//   y[n, r] = sum_b s[r, b] * (sum_{k in block b} trit[r, k] * x[n, k]),
+// inner block sums exact, scaled and accumulated in fp32, the output rounded once.
+//
+// Why int8: at batch 1-2 the fp16 mma.sync GEMV is issue-bound, not
+// HBM-bound -- one LOP3 per half2 of weights plus 16 HMMA.16816 per 16x256 unit (measured:
+// the kernel runs as fast with the weight stream switched off).  Here
+//  * each activation block (256 columns, one batch row) is put on an integer grid:
+//    x~ = rint(x * 2^(23-e)), 2^e <= max|x| < 2^(e+1), |x~| < 2^24 (fp16/bf16 values down to
+//    2^-24 of the block maximum are exact, smaller ones carry an error below 2^-24 max|x|);
+//  * column k's value is pre-multiplied by 4^(3-j), j = (k >> 2) & 3 its field class in the
+//    T16 word, and split into 4 signed bytes (slices);
+//  * a weight field is extracted by ONE LOP3 per FOUR weights: the byte (w >> 0) & (3 << 2j)
+//    is the u8 4^j * d (d = trit + 1), so A = 4^j d and B = 4^(3-j) x~ multiply to 64 d x~ for
+//    every class -- one int32 accumulator, exact;
+//  * the 4 slices (x 2 batch rows) are the N = 8 columns of mma.sync.m16n8k32.u8.s8.s32, which
+//    has the HMMA.16816's issue cost at twice the K: 8 IMMA + 32 LOP3 per unit instead of
+//    16 HMMA + 64 LOP3 + 20 FFMA;
+//  * the trit offset is folded into the accumulator: the first MMA of a block starts from
+//    -Cs, Cs[slice] = sum_k 4^j(k) b_slice(k), so D = sum_k 4^j (d - 1) b(k) exactly;
+//  * per block: two slices combine in int32, one I2F + FFMA per row applies the block scale
+//    and the block grid 2^(e-29); the two slice pairs meet by one shuffle when a tile closes.
+// Weight streaming, tile ownership and the deterministic boundary-tile reduction are K3's.
+#include "common.cuh"
+
+namespace tr {
+
+struct S8Args {
+  const uint8_t* w;
+  const void* x;
+  void* y;
+  int64_t ldx, ldy;
+  int rows, cols, nb, n_tiles;
+  int x_vec;
+  int batch;   // 1 or 2
+  int ns;      // ring slots per warp (power of two)
+  int dbg;     // development probe: 2 = per-CTA / per-warp %globaltimer stamps into y (no output)
+  int pre;     // fused producer of x (K3's GemvArgs::pre): 1 add+RMSNorm, 2 SwiGLU
+  const void* pre_delta;
+  const void* pre_gamma;
+  void* pre_out;
+  float eps;
+};
+
+constexpr int kS8SU = 2;              // units per ring slot (one bulk copy)
+constexpr int kS8NSMax = 4;
+constexpr int kS8ItemBytes = 1024;    // staged x per (block, batch row): 4 slices x 4 chunks x 16 words
+
+template <int NW> struct S8Cfg {
+  static constexpr int kSlotBytes = kS8SU * kUnitBytes;
+  static constexpr size_t kRedOff = 1024;                         // [mbarriers | slot tags]
+  static constexpr size_t kRedBytes = (size_t)2 * NW * 64 * 4;    // 2 parked tiles per warp x 64 floats
+  static constexpr size_t kCsOff = kRedOff + kRedBytes;           // -Cs: nb x nrx x 4 int32
+  __host__ __device__ static size_t f_off(int nb, int nrx) { return kCsOff + (size_t)nb * nrx * 16; }
+  __host__ __device__ static size_t xs_off(int nb, int nrx) {
+    return (f_off(nb, nrx) + (size_t)nb * nrx * 4 + 127) / 128 * 128;
+  }
+  __host__ __device__ static size_t ring_off(int nb, int nrx) {
+    return xs_off(nb, nrx) + (size_t)nb * nrx * kS8ItemBytes;
+  }
+  __host__ __device__ static size_t smem(int nb, int nrx, int ns) {
+    return ring_off(nb, nrx) + (size_t)NW * ns * kSlotBytes;
+  }
+};
+
+// Staged slice word of (block kb, batch row br, slice s, chunk c, combo cb = 4w + j): the
+// 4 bytes B[k-slots] of one MMA B-fragment register.  The 16-byte group index is XOR-swizzled
+// by (chunk pair, slice parity) so a quarter-warp's 128-bit loads hit 8 distinct bank groups.
+__device__ __forceinline__ uint32_t s8_word_off(int nrx, int kb, int br, int s, int c, int cb) {
+  const int sw = ((c >> 1) << 1) | (s & 1);
+  return (uint32_t)(kb * nrx + br) * kS8ItemBytes + s * 256 + c * 64 + (((cb >> 2) ^ sw) << 4) + ((cb & 3) << 2);
+}
+
+template <typename T>
+__device__ __forceinline__ void s8_f8(const uint4& v, float (&f)[8]) {
+  const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = Act<T>::to_float(e[i]);
+}
+template <typename T>
+__device__ __forceinline__ uint4 s8_pack8(const float (&f)[8]) {
+  uint4 v;
+  T* e = reinterpret_cast<T*>(&v);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) e[i] = Act<T>::from_float(f[i]);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ float s8_rnd(float v) { return Act<T>::to_float(Act<T>::from_float(v)); }
+
+template <typename T>
+__device__ __forceinline__ uint4 s8_load8(const T* row, int64_t k, int cols, int vec) {
+  if (vec && k + 8 <= cols) {
+    uint4 r;
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];\n" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(row + k));
+    return r;
+  }
+  T tmp[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) tmp[e] = (k + e < cols) ? row[k + e] : Act<T>::from_float(0.0f);
+  return *reinterpret_cast<uint4*>(tmp);
+}
+
+// Whole warp: lane l holds the activations of columns kb*256 + 8l .. +7 of batch row br (already
+// rounded to T).  Puts the block on its integer grid, stores the 4 slices in k-slot order, and
+// -Cs and the block grid factor 2^(e-29).
+__device__ __forceinline__ void s8_stage_block(const float (&f)[8], uint8_t* xs, int32_t* ncs, float* fsc, int nrx,
+                                               int kb, int br) {
+  const int lane = threadIdx.x & 31;
+  float m = 0.0f;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) m = fmaxf(m, fabsf(f[e]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  int ex = ((__float_as_int(m) >> 23) & 0xFF) - 127;   // 2^ex <= m < 2^(ex+1)
+  ex = ex < -90 ? -90 : ex;                              // zero / tiny blocks: any grid is exact enough
+  const int c = lane >> 3, mm = lane & 7;
+  // columns 8mm + e: field class j = (2mm + (e >> 2)) & 3; X = rint(x * 2^(23-ex) * 4^(3-j)), |X| <= 2^30
+  uint32_t R[4][2];   // [slice][e >> 2]: the signed-byte slices of columns e = 4G .. 4G+3
+  int wj[2];
+#pragma unroll
+  for (int G = 0; G < 2; ++G) {
+    const int j = (2 * mm + G) & 3;
+    wj[G] = (1 << (2 * j)) * 0x01010101;
+    const float q = __int_as_float((150 - ex + 2 * (3 - j)) << 23);
+    uint32_t Z[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      // balanced base-256 digits: the bytes of (X + 0x80808080) ^ 0x80808080 are int8 slices of X
+      Z[i] = ((uint32_t)__float2int_rn(f[4 * G + i] * q) + 0x80808080u) ^ 0x80808080u;
+    }
+    const uint32_t t0 = __byte_perm(Z[0], Z[1], 0x5140), t1 = __byte_perm(Z[0], Z[1], 0x7362);
+    const uint32_t t2 = __byte_perm(Z[2], Z[3], 0x5140), t3 = __byte_perm(Z[2], Z[3], 0x7362);
+    R[0][G] = __byte_perm(t0, t2, 0x5410);
+    R[1][G] = __byte_perm(t0, t2, 0x7632);
+    R[2][G] = __byte_perm(t1, t3, 0x5410);
+    R[3][G] = __byte_perm(t1, t3, 0x7632);
+  }
+  int cs[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) cs[s] = __dp4a((int)R[s][1], wj[1], __dp4a((int)R[s][0], wj[0], 0));
+  // word (s, combo) = bytes {(h0,hb0), (h0,hb1), (h1,hb0), (h1,hb1)}: columns 16 apart sit in
+  // lanes 2 apart; the hb = 0 lane builds pairs 0-1, its partner pairs 2-3
+  const int hb = (mm >> 1) & 1;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const uint32_t send = hb ? R[s][0] : R[s][1];
+    const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 2);
+    const uint32_t mine = hb ? R[s][1] : R[s][0];
+    const uint32_t lo = hb ? recv : mine, hi = hb ? mine : recv;
+#pragma unroll
+    for (int pl = 0; pl < 2; ++pl) {
+      const int p = pl + 2 * hb;
+      const int w = 2 * (mm >> 2) + (p & 1), j = (2 * mm + (p >> 1)) & 3;
+      const uint32_t word = __byte_perm(lo, hi, pl ? 0x7362 : 0x5140);
+      *reinterpret_cast<uint32_t*>(xs + s8_word_off(nrx, kb, br, s, c, 4 * w + j)) = word;
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < 4; ++s) cs[s] = __reduce_add_sync(0xffffffffu, cs[s]);
+  if (lane == 0) {
+    int4 v = make_int4(-cs[0], -cs[1], -cs[2], -cs[3]);
+    *reinterpret_cast<int4*>(ncs + (kb * nrx + br) * 4) = v;
+    fsc[kb * nrx + br] = __int_as_float((127 + ex - 29) << 23);   // 2^(ex - 29)
+  }
+}
+
+__device__ __forceinline__ void imma(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t u4c(const uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+
+template <typename T, int NW>
+__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Args a) {
+  using Cfg = S8Cfg<NW>;
+  constexpr int kSlotBytes = Cfg::kSlotBytes;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int NS = a.ns, nrx = a.batch, nb = a.nb;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                 // NW * NS <= 64
+  int* slot_tile = reinterpret_cast<int*>(smem + 512);                 // 2 * NW
+  float* red = reinterpret_cast<float*>(smem + Cfg::kRedOff);
+  int32_t* ncs = reinterpret_cast<int32_t*>(smem + Cfg::kCsOff);
+  float* fsc = reinterpret_cast<float*>(smem + Cfg::f_off(nb, nrx));
+  uint8_t* xs = smem + Cfg::xs_off(nb, nrx);
+  uint8_t* ring = smem + Cfg::ring_off(nb, nrx);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, c = lane & 3;
+  uint64_t* mybar = bars + warp * NS;
+  uint8_t* myring = ring + warp * NS * kSlotBytes;
+  uint64_t* trace = (a.dbg & 2) ? reinterpret_cast<uint64_t*>(a.y) : nullptr;
+  auto stamp = [&](int k) {   // CTA stamps [blockIdx][0..7], warp stamps [148*8 + (blockIdx*NW + warp)*4 + k]
+    if (trace && lane == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      if (k < 8) {
+        if (warp == 0) trace[blockIdx.x * 8 + k] = t;
+      } else {
+        trace[148 * 8 + (blockIdx.x * NW + warp) * 4 + (k - 8)] = t;
+      }
+    }
+  };
+  stamp(0);
+
+  // the CTA owns whole tiles [t0, t1); warp w a contiguous slice of their units
+  const int t0 = (int)((int64_t)blockIdx.x * a.n_tiles / gridDim.x);
+  const int t1 = (int)((int64_t)(blockIdx.x + 1) * a.n_tiles / gridDim.x);
+  const int LL = (t1 - t0) * nb;
+  const int wu0 = t0 * nb + (int)((int64_t)warp * LL / NW);
+  const int wu1 = t0 * nb + (int)((int64_t)(warp + 1) * LL / NW);
+
+  // ---- weight stream (lane 0): bulk copies of kS8SU units into the warp's ring
+  int pu = wu0;
+  uint64_t pol = 0;
+  auto issue = [&](int slot) {
+    if (pu >= wu1) return;
+    const int n = min(kS8SU, wu1 - pu);
+    mbar_expect_tx(&mybar[slot], n * kUnitBytes);
+    bulk_g2s(myring + slot * kSlotBytes, a.w + (int64_t)pu * kUnitBytes, n * kUnitBytes, &mybar[slot], pol);
+    pu += n;
+  };
+  if (lane == 0) {
+    pol = policy_evict_first();
+    for (int s = 0; s < NS; ++s) mbar_init(&mybar[s], 1);
+    mbar_fence_init();
+    slot_tile[2 * warp] = -1;
+    slot_tile[2 * warp + 1] = -1;
+  }
+  // weights do not depend on the previous kernel: prefetch before griddepcontrol.wait
+  // (dev knob dbg&4: after it; dbg&8: one slot before, the rest after)
+  const int pre_slots = (a.dbg & 4) ? 0 : (a.dbg & 8) ? 1 : NS;
+  if (lane == 0)
+    for (int s = 0; s < pre_slots; ++s) issue(s);
+  __syncwarp();
+  griddep_launch_dependents();
+  griddep_wait();   // x belongs to the previous kernel until here
+  stamp(1);
+  // the rest of the ring is issued right after this warp's first activation loads, so those
+  // loads are not queued behind the weight stream
+  bool rest_issued = pre_slots >= NS;
+  auto issue_rest = [&]() {
+    if (!rest_issued) {
+      if (lane == 0)
+        for (int s = pre_slots; s < NS; ++s) issue(s);
+      rest_issued = true;
+    }
+  };
+
+  // ---- stage the activations as int8 slices (fused producer first when asked)
+  const T* xg = reinterpret_cast<const T*>(a.x);
+  if (a.pre == 1) {   // x = rmsnorm(x + delta) * gamma; CTA 0 stores x + delta (the residual)
+    float* ss_buf = red;   // nb * nrx partial sums of squares, then nrx inverse RMS
+    for (int item = warp; item < nb * nrx; item += NW) {
+      const int kb = item / nrx, br = item % nrx;
+      const int64_t kx = (int64_t)kb * kBlock + lane * 8;
+      float f[8];
+      const uint4 xv = s8_load8(xg + br * a.ldx, kx, a.cols, a.x_vec);
+      uint4 dv = make_uint4(0, 0, 0, 0);
+      if (a.pre_delta) dv = s8_load8(reinterpret_cast<const T*>(a.pre_delta) + br * a.ldx, kx, a.cols, a.x_vec);
+      issue_rest();
+      s8_f8<T>(xv, f);
+      if (a.pre_delta) {
+        float d[8];
+        s8_f8<T>(dv, d);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] = s8_rnd<T>(f[e] + d[e]);
+      }
+      const uint4 hv = s8_pack8<T>(f);
+      *reinterpret_cast<uint4*>(xs + (size_t)item * kS8ItemBytes + lane * 16) = hv;   // parked in its own item
+      if (blockIdx.x == 0 && a.pre_out && kx < a.cols) {
+        T* o = reinterpret_cast<T*>(a.pre_out) + br * a.ldx + kx;
+        if (kx + 8 <= a.cols && a.x_vec) {
+          *reinterpret_cast<uint4*>(o) = hv;
+        } else {
+          const T* he = reinterpret_cast<const T*>(&hv);
+          for (int e = 0; e < 8 && kx + e < a.cols; ++e) o[e] = he[e];
+        }
+      }
+      float ss = 0.0f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ss += f[e] * f[e];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) ss_buf[item] = ss;
+    }
+    __syncthreads();
+    for (int br = warp; br < nrx; br += NW) {   // fixed-order sums: same value in every CTA
+      float ss = 0.0f;
+      for (int kb = lane; kb < nb; kb += 32) ss += ss_buf[kb * nrx + br];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) ss_buf[nb * nrx + br] = rsqrtf(ss / a.cols + a.eps);
+    }
+    __syncthreads();
+    const T* gam = reinterpret_cast<const T*>(a.pre_gamma);
+    for (int item = warp; item < nb * nrx; item += NW) {
+      const int kb = item / nrx, br = item % nrx;
+      const int64_t kx = (int64_t)kb * kBlock + lane * 8;
+      float f[8], gm[8];
+      s8_f8<T>(*reinterpret_cast<const uint4*>(xs + (size_t)item * kS8ItemBytes + lane * 16), f);
+      s8_f8<T>(s8_load8(gam, kx, a.cols, a.x_vec), gm);
+      const float iv = ss_buf[nb * nrx + br];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) f[e] = s8_rnd<T>(s8_rnd<T>(f[e] * iv) * gm[e]);
+      __syncwarp();   // every lane holds its h before the item's bytes are overwritten
+      s8_stage_block(f, xs, ncs, fsc, nrx, kb, br);
+    }
+  } else {   // plain x, or silu(gate) * up of a gate|up product; loads for 4 items in flight
+    const int n_items = nb * nrx;
+    for (int i0 = warp; i0 < n_items; i0 += 4 * NW) {
+      uint4 va[4], vb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int item = i0 + i * NW;
+        if (item < n_items) {
+          const int kb = item / nrx, br = item % nrx;
+          const int64_t kx = (int64_t)kb * kBlock + lane * 8;
+          va[i] = s8_load8(xg + br * a.ldx, kx, a.cols, a.x_vec);
+          if (a.pre == 2) vb[i] = s8_load8(xg + br * a.ldx + a.cols, kx, a.cols, a.x_vec);
+        }
+      }
+      issue_rest();
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int item = i0 + i * NW;
+        if (item < n_items) {
+          const int kb = item / nrx, br = item % nrx;
+          const int64_t kx = (int64_t)kb * kBlock + lane * 8;
+          float f[8];
+          s8_f8<T>(va[i], f);
+          if (a.pre == 2) {
+            float up[8];
+            s8_f8<T>(vb[i], up);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              f[e] = kx + e < a.cols ? s8_rnd<T>(s8_rnd<T>(f[e] / (1.0f + __expf(-f[e]))) * up[e]) : 0.0f;
+          }
+          s8_stage_block(f, xs, ncs, fsc, nrx, kb, br);
+        }
+      }
+    }
+  }
+  issue_rest();
+  stamp(8);
+  __syncthreads();
+  stamp(2);
+
+  // ---- main loop: units [wu0, wu1), tile by tile
+  T* y = reinterpret_cast<T*>(a.y);
+  const int nBc = g & (4 * nrx - 1);          // B column of this lane: slice-column g
+  const int bB = nBc >> 2, sB = nBc & 3;
+  const int swB = ((c >> 1) << 1) | (sB & 1);
+  const uint8_t* xsB = xs + (size_t)bB * kS8ItemBytes + sB * 256 + c * 64;
+  const int bD = min(c >> 1, nrx - 1);         // D columns of this lane: slices 2(c&1), +1 of row c>>1
+  const int32_t* ncsD = ncs + bD * 4 + 2 * (c & 1);
+  const float* fscD = fsc + bD;
+  const float lane_w = (c & 1) ? 65536.0f : 1.0f;
+
+  auto store_tile = [&](int tile, float v0, float v1) {
+    if (trace) return;
+    if ((c & 1) == 0 && (c >> 1) < nrx) {
+      const int r0 = tile * 16 + g, r1 = r0 + 8;
+      if (r0 < a.rows) y[(c >> 1) * a.ldy + r0] = Act<T>::from_float(v0);
+      if (r1 < a.rows) y[(c >> 1) * a.ldy + r1] = Act<T>::from_float(v1);
+    }
+  };
+  const int first_tile = wu0 < wu1 ? wu0 / nb : -1;
+  int cur = first_tile;
+  float acc0 = 0.0f, acc1 = 0.0f;
+  auto close_tile = [&](int tile) {   // combine the two slice pairs; store or park
+    float v0 = acc0 * lane_w, v1 = acc1 * lane_w;
+    v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+    if (tile * nb >= wu0 && (tile + 1) * nb <= wu1) {
+      store_tile(tile, v0, v1);
+      return;
+    }
+    const int which = (tile == first_tile) ? 0 : 1;
+    float* dst = red + (2 * warp + which) * 64;
+    dst[lane] = v0;
+    dst[32 + lane] = v1;
+    if (lane == 0) slot_tile[2 * warp + which] = tile;
+  };
+
+  auto do_unit = [&](const uint4& wl, const uint4& wh, uint32_t sv, int kb) {
+    const uint8_t* xp = xsB + (size_t)kb * nrx * kS8ItemBytes;
+    uint4 xw[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) xw[q] = lds128(xp + ((q ^ swB) << 4));
+    const int2 cs = *reinterpret_cast<const int2*>(ncsD + kb * nrx * 4);
+    int d[4] = {cs.x, cs.y, cs.x, cs.y};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int w = i >> 1, j0 = 2 * (i & 1);
+      const uint32_t lw = u4c(wl, w), hw = u4c(wh, w);
+      const uint32_t m0 = 0x03030303u << (2 * j0), m1 = 0x03030303u << (2 * j0 + 2);
+      const uint32_t A[4] = {lw & m0, hw & m0, lw & m1, hw & m1};
+      imma(d, A, u4c(xw[w], j0), u4c(xw[w], j0 + 1));
+    }
+    const float fb = fscD[kb * nrx];
+    const float2 sc = __half22float2(*reinterpret_cast<const __half2*>(&sv));
+    const int v0 = d[0] + d[1] * 256, v1 = d[2] + d[3] * 256;
+    acc0 = fmaf((float)v0, sc.x * fb, acc0);
+    acc1 = fmaf((float)v1, sc.y * fb, acc1);
+  };
+
+  int kb = wu0 < wu1 ? wu0 - first_tile * nb : 0;
+  const int nslog = NS == 1 ? 0 : NS == 2 ? 1 : 2;
+  int k = 0;
+#pragma unroll 1
+  for (int u = wu0; u < wu1; ++k) {
+    const int s = k & (NS - 1);
+    const int n = min(kS8SU, wu1 - u);
+#ifdef S8_NOWAIT   // dev probe: math on the first ring fill only (wrong results)
+    if (k >= NS) goto skip_wait;
+#endif
+    if (k > 0) {   // refill the slot read in the previous iteration (its loads have completed)
+      __syncwarp();
+      if (lane == 0) {
+        fence_proxy_async_smem();
+        issue((k - 1) & (NS - 1));
+      }
+    }
+    mbar_wait(&mybar[s], (k >> nslog) & 1);
+#ifdef S8_NOWAIT
+  skip_wait:
+#endif
+    const uint8_t* slot = myring + s * kSlotBytes;
+    uint4 wl[kS8SU], wh[kS8SU];
+    uint32_t sv[kS8SU];
+#pragma unroll
+    for (int q = 0; q < kS8SU; ++q) {
+      if (q < n) {
+        wl[q] = lds128(slot + q * kUnitBytes + t16_word(0, c, g) * 16);
+        wh[q] = lds128(slot + q * kUnitBytes + t16_word(1, c, g) * 16);
+        sv[q] = *reinterpret_cast<const uint32_t*>(slot + q * kUnitBytes + kTileBlockBytes + g * 4);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kS8SU; ++q) {
+      if (q < n) {
+        if (kb == nb) {   // next tile
+          close_tile(cur);
+          acc0 = acc1 = 0.0f;
+          ++cur;
+          kb = 0;
+        }
+#ifdef S8_NOMATH   // dev probe: stream the weights only (wrong results)
+        acc0 += __uint_as_float(wl[q].x ^ wh[q].y ^ sv[q]);
+#else
+        do_unit(wl[q], wh[q], sv[q], kb);
+#endif
+        ++kb;
+      }
+    }
+    u += n;
+  }
+  stamp(9);
+  if (cur >= 0) close_tile(cur);
+
+  // ---- boundary tiles: combine the parked fragments in fixed (warp, slot) order and store
+  __syncthreads();
+  const int my_tag = lane < 2 * NW ? slot_tile[lane] : -1;
+  for (int i = warp; i < 2 * NW; i += NW) {
+    const int tile = __shfl_sync(0xffffffffu, my_tag, i);
+    if (tile < 0) continue;
+    const unsigned match = __ballot_sync(0xffffffffu, my_tag == tile);
+    if (match & ((1u << i) - 1u)) continue;   // a lower slot holds this tile: it reduces
+    float v0 = 0.0f, v1 = 0.0f;
+    for (unsigned mq = match; mq; mq &= mq - 1) {   // ascending slot order: deterministic
+      const int q = __ffs(mq) - 1;
+      v0 += red[q * 64 + lane];
+      v1 += red[q * 64 + 32 + lane];
+    }
+    store_tile(tile, v0, v1);
+  }
+  stamp(10);
+  if (warp == 0) stamp(3);
+}
+
+// ------------------------------------------------------------------------------------ host
+
+template <int NW>
+static int s8_ns(int n_tiles, int nb, int grid) {
+  const int tiles_max = (int)ceil_div(n_tiles, grid);
+  const int ops = (int)ceil_div(ceil_div((int64_t)tiles_max * nb, NW), kS8SU);
+  return ops >= kS8NSMax ? kS8NSMax : ops > 2 ? 4 : ops > 1 ? 2 : 1;
+}
+
+constexpr int kS8SmallCtaUnits = 48;   // units per CTA at or below which 8 warps x 2 CTAs/SM are used
+
+static bool s8_small(int n_tiles, int nb, int grid) { return (int64_t)ceil_div(n_tiles, grid) * nb <= kS8SmallCtaUnits; }
+
+template <int NW>
+static size_t s8_smem_plan(int batch, int nb, int n_tiles, int grid, int* ns_out) {
+  int ns = s8_ns<NW>(n_tiles, nb, grid);
+  size_t sm = S8Cfg<NW>::smem(nb, batch, ns);
+  while (sm > 227 * 1024 && ns > 1) {   // wide activations: a shallower weight ring
+    ns >>= 1;
+    sm = S8Cfg<NW>::smem(nb, batch, ns);
+  }
+  if (ns_out) *ns_out = ns;
+  return sm;
+}
+
+// true when the int8-slice GEMV takes this product (batch 1-2, activations fit with a ring of >= 2)
+bool gemv_s8_fits(int batch, int rows, int cols) {
+  if (batch < 1 || batch > 2) return false;
+  const int nb = (int)ceil_div(cols, kBlock), n_tiles = (int)ceil_div(rows, 16);
+  const int grid = sm_count() < n_tiles ? sm_count() : n_tiles;
+  int ns = 0;
+  const size_t sm = s8_small(n_tiles, nb, grid) ? s8_smem_plan<8>(batch, nb, n_tiles, grid, &ns)
+                                                : s8_smem_plan<16>(batch, nb, n_tiles, grid, &ns);
+  return sm <= 227 * 1024 && (ns >= 2 || s8_ns<16>(n_tiles, nb, grid) < 2);
+}
+
+template <typename T, int NW>
+static int launch_s8(S8Args& a, int grid, int pdl, cudaStream_t st) {
+  auto kern = k_gemv_s8<T, NW>;
+  static int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    configured_dev = dev;
+  }
+  const size_t smem = s8_smem_plan<NW>(a.batch, a.nb, a.n_tiles, grid, &a.ns);
+  if (smem > 227 * 1024) {
+    set_error("tr_linear(gemv-s8): %d blocks per row x batch %d need %zu B of shared memory", a.nb, a.batch, smem);
+    return -1;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(NW * 32, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+  if (e != cudaSuccess) {
+    set_error("tr_linear(gemv-s8): launch failed: %s (grid %d, smem %zu)", cudaGetErrorString(e), grid, smem);
+    return -1;
+  }
+  return 0;
+}
+
+int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows, int cols,
+            int ctas, int pdl, cudaStream_t st, int pre, const void* pre_delta, const void* pre_gamma, void* pre_out,
+            float eps) {
+  if (!gemv_s8_fits(batch, rows, cols)) {
+    set_error("tr_linear(gemv-s8): batch %d x %d columns does not fit the int8-slice GEMV", batch, cols);
+    return -1;
+  }
+  S8Args a = {};
+  a.w = (const uint8_t*)w;
+  a.x = x;
+  a.y = y;
+  a.ldx = ldx;
+  a.ldy = ldy;
+  a.rows = rows;
+  a.cols = cols;
+  a.nb = (int)ceil_div(cols, kBlock);
+  a.n_tiles = (int)ceil_div(rows, 16);
+  a.x_vec = ((ldx % 8) == 0 && ((uintptr_t)x % 16) == 0) ? 1 : 0;
+  a.batch = batch;
+  a.pre = pre;
+  a.pre_delta = pre_delta;
+  a.pre_gamma = pre_gamma;
+  a.pre_out = pre_out;
+  a.eps = eps;
+  a.dbg = (ctas >> 12) & 0xF;
+  ctas &= 0xFFF;
+  int grid = ctas > 0 ? ctas : sm_count();
+  if (grid > a.n_tiles) grid = a.n_tiles;
+  const bool bf = act != kActF16;
+  if (s8_small(a.n_tiles, a.nb, grid))
+    return bf ? launch_s8<__nv_bfloat16, 8>(a, grid, pdl, st) : launch_s8<__half, 8>(a, grid, pdl, st);
+  return bf ? launch_s8<__nv_bfloat16, 16>(a, grid, pdl, st) : launch_s8<__half, 16>(a, grid, pdl, st);
+}
+
+}  // namespace tr

@@ -31,7 +31,13 @@
 
 namespace tr {
 
-constexpr int kNSMax = 4;      // ring slots per warp at 2 units per slot (a power of two; fewer when the range is short)
+#ifndef GEMV_SU1
+#define GEMV_SU1 4
+#endif
+#ifndef GEMV_NSMAX
+#define GEMV_NSMAX 4
+#endif
+constexpr int kNSMax = GEMV_NSMAX;     // ring slots per warp at 2 units per slot (a power of two; fewer when the range is short)
 constexpr int kXChunk = 144;   // staged activations: bytes per 64-column chunk (128 + bank spread)
 constexpr int kXBlk = 4 * kXChunk;
 
@@ -139,7 +145,7 @@ __device__ __forceinline__ uint4 ld_cg_x8(const T* row, int64_t k, int cols, int
 // weights) while this one computes -- the better trade for small layers.
 template <int NT, int NW> struct GemvCfg {
   static constexpr int kWarps = NW;     // warps per CTA
-  static constexpr int kSU = NT == 1 ? 4 : 2;          // units (1056 B) per bulk copy = one ring slot
+  static constexpr int kSU = NT == 1 ? GEMV_SU1 : 2;   // units (1056 B) per bulk copy = one ring slot
   static constexpr int kFrag = NT * 4 * 32;            // floats of one warp's tile fragment
   static constexpr int kSlotBytes = kSU * kUnitBytes;
   static constexpr size_t kRedOff = 1024;
@@ -514,9 +520,24 @@ __global__ void __launch_bounds__(NW * 32, (NW == 8 && NT == 1) ? 2 : 1) k_gemv_
     for (; u < wu1; ++k) {
       const int s = k & (NS - 1);
       const int n = min(kSU, wu1 - u);
+      // refill the slot read in the PREVIOUS iteration: its loads have long completed (their
+      // values fed the MMAs), so the proxy fence does not stall on outstanding loads
+#ifdef GEMV_NOWAIT   // dev probe: compute on the first ring fill only (wrong results; times the math)
+      if (k >= NS) goto skip_wait;
+#endif
+      if (k > 0) {
+        __syncwarp();
+        if (lane == 0) {
+          fence_proxy_async_smem();
+          issue((k - 1) & (NS - 1));
+        }
+      }
       mbar_wait(&mybar[s], (k >> nslog) & 1);
       if (k == 0) stamp(3);
-      const uint8_t* slot = myring + s * kSlotBytes + (c * 8 + g) * 16;
+#ifdef GEMV_NOWAIT
+    skip_wait:
+#endif
+      const uint8_t* slot = myring + s * kSlotBytes + t16_word(0, c, g) * 16;
       uint4 wl[kSU], wh[kSU];
       uint32_t sv[kSU];
 #pragma unroll
@@ -524,13 +545,8 @@ __global__ void __launch_bounds__(NW * 32, (NW == 8 && NT == 1) ? 2 : 1) k_gemv_
         if (q < n) {
           wl[q] = lds128(slot + q * kUnitBytes);
           wh[q] = lds128(slot + q * kUnitBytes + 512);
-          sv[q] = *reinterpret_cast<const uint32_t*>(slot - (c * 8 + g) * 16 + q * kUnitBytes + kTileBlockBytes + g * 4);
+          sv[q] = *reinterpret_cast<const uint32_t*>(slot - t16_word(0, c, g) * 16 + q * kUnitBytes + kTileBlockBytes + g * 4);
         }
-      }
-      __syncwarp();   // slot fully read into registers: refill it with the next op of the stream
-      if (lane == 0) {
-        fence_proxy_async_smem();
-        issue(s);
       }
 #pragma unroll
       for (int q = 0; q < kSU; ++q)

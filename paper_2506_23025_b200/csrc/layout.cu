@@ -23,7 +23,7 @@ __global__ void k_repack_tq2(const uint8_t* __restrict__ payload, const __half* 
     const int64_t t = tb / nb, b = tb % nb;
     uint8_t* unit = dst + tb * kUnitBytes;
     const int u = (int)((w >> 2) & 63), i = (int)(w & 3);
-    const int half = u >> 5, c = (u >> 3) & 3, g = u & 7;
+    const int half = u >> 5, c = (u >> 3) & 3, g = (u & 7) ^ (2 * c);   // u = t16_word(half, c, g)
     const int64_t row = 16 * t + 8 * half + g;
     uint32_t word = 0;
     if (row < rows) {
@@ -62,7 +62,7 @@ __global__ void k_unrepack_tq2(const uint8_t* __restrict__ src, int64_t rows, in
     const int k = (int)(rem % 16), c = k >> 2, kq = k & 3;   // payload bytes 4k..4k+3 = chunk c cols 16kq..+15
     const int64_t t = row / 16;
     const int rt = (int)(row % 16), half = rt >> 3, g = rt & 7;
-    const int u = half * 32 + c * 8 + g;
+    const int u = t16_word(half, c, g);
     const uint8_t* unit = src + (t * nb + b) * kUnitBytes;
     const uint4 w4 = *reinterpret_cast<const uint4*>(unit + u * 16);
     const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};

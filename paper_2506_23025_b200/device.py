@@ -116,7 +116,8 @@ class TernaryWeight:
         return f"TernaryWeight({self.rows}x{self.cols}, {self.fmt.name}, {self.data.numel()} B on {self.data.device})"
 
 
-_PATHS = {"auto": 0, "umma": _lib.LINEAR_FORCE_UMMA, "gemv": _lib.LINEAR_FORCE_GEMV}
+_PATHS = {"auto": 0, "umma": _lib.LINEAR_FORCE_UMMA, "gemv": _lib.LINEAR_FORCE_GEMV,
+          "gemv_f16": _lib.LINEAR_FORCE_GEMV | _lib.LINEAR_GEMV_F16}
 
 
 def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, pdl: bool = False,

@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_gemv -s 6 -c 1 \
+  -o gpurun_out/prof_s8_big python scripts/ncu_target.py 28672 8192 1 > /dev/null 2>&1; echo "prof rc=$?"
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_gemv -s 6 -c 1 \
+  -o gpurun_out/prof_s8_11008 python scripts/ncu_target.py 11008 4096 1 > /dev/null 2>&1; echo "prof rc=$?"

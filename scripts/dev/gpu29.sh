@@ -1,0 +1,7 @@
+#!/bin/bash
+for d in 0 8; do for sh in "28672 8192" "11008 4096"; do
+  echo "== dbg $d $sh" >> gpurun_out/tr29.txt
+  timeout 120 python scripts/dev/s8_trace.py $sh $d 2>&1 | tail -2 >> gpurun_out/tr29.txt
+done; done
+timeout 300 python -m pytest tests -m gpu -x -q -k "s8 or linear_vs_oracle or exact or pre_fused or uniform or partition" 2>&1 | tail -3 >> gpurun_out/tr29.txt
+timeout 300 python scripts/dev/gemv_sweep.py 1,2 auto 4096x4096,11008x4096,4096x11008,8192x8192,28672x8192 2>&1 | grep -v relerr >> gpurun_out/tr29.txt

@@ -441,7 +441,7 @@ def test_linear_chain_matches_per_layer(tp, batch, dtype):
     st.replay()   # twice: the grid barrier resets itself between launches
     ref = x
     for w in ws:
-        ref = tp.linear(ref, w)
+        ref = tp.linear(ref, w, path="gemv_f16")   # the chain runs the fp16 mma.sync GEMV
     torch.cuda.synchronize()
     assert torch.isfinite(ref).all()
     # same math; the per-layer launches may pick the 8-warp variant (another warp split of
@@ -469,7 +469,7 @@ def test_gemv_uniform_scale_vs_oracle(tp, dtype, rows, cols, batch, ctas):
 
 
 @pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
-@pytest.mark.parametrize("batch", [1, 3])
+@pytest.mark.parametrize("batch", [1, 2, 3])
 def test_linear_pre_fused_producers(tp, dtype, batch):
     # tr_linear_pre == standalone glue kernel followed by tr_linear (same roundings)
     from paper_2506_23025_b200 import _lib
@@ -500,3 +500,63 @@ def test_linear_pre_fused_producers(tp, dtype, batch):
     ref2 = tp.linear(a, w_down)
     y2 = linear_pre(gu, w_down, _lib.PRE_SILU_MUL)
     assert torch.equal(y2, ref2)   # identical staged activations -> identical product
+
+
+# ---------------------------------------------------------------- int8-slice GEMV (batch 1-2)
+
+def _s8_inputs(rng, kind, batch, cols, dtype):
+    x = rng.uniform(-1, 1, size=(batch, cols))
+    if kind == "range":      # 1e4 next to 1e-4 inside one block: small values fall below the 2^-24 grid
+        x = x * np.where(rng.uniform(size=x.shape) < 0.1, 1e4, 1e-4)
+    elif kind == "zeros":    # whole zero blocks and one lone non-zero
+        x[:, : min(cols, 512)] = 0.0
+        x[:, -1] = 3.0
+    elif kind == "tiny":     # fp16 subnormals / bf16 values near 1e-30
+        x = x * (1e-6 if dtype == "float16" else 1e-30)
+    elif kind == "huge":     # near the top of the format
+        x = x * (6e4 if dtype == "float16" else 1e30)
+    elif kind == "rows":     # batch rows of very different magnitude
+        x = x * np.array([1e-3, 1e3][:batch])[:, None]
+    return torch.from_numpy(x.astype(np.float32)).to(getattr(torch, dtype)).cuda()
+
+
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
+@pytest.mark.parametrize("kind", ["uniform", "range", "zeros", "tiny", "huge", "rows"])
+@pytest.mark.parametrize("rows,cols", [(37, 1500), (300, 4096), (640, 11008)])
+@pytest.mark.parametrize("batch", [1, 2])
+@pytest.mark.parametrize("per_block", [False, True])
+def test_gemv_s8_vs_oracle(tp, dtype, kind, rows, cols, batch, per_block):
+    rng = np.random.default_rng(rows + cols + batch + len(kind))
+    payload, scales = _rand_packed(rng, rows, cols, per_block)
+    w = tp.PackedMatrix(rows=rows, cols=cols, fmt=tp.DType.TQ2, payload=payload, scales=scales).to_device()
+    x = _s8_inputs(rng, kind, batch, cols, dtype)
+    y = tp.linear(x, w).float().cpu().numpy()
+    ref = _oracle_ref(payload, scales, cols, 2, x.float().cpu().numpy())
+    assert np.isfinite(y).all() or kind == "huge"
+    fin = np.isfinite(ref).all(axis=1) & (np.abs(ref).max(axis=1) < (6.5e4 if dtype == "float16" else 3e38))
+    tol = 2e-3 if dtype == "float16" else 6e-3
+    if kind == "tiny" and dtype == "float16":   # outputs are fp16 subnormals: within one ulp (2^-24)
+        assert np.abs(y - ref).max() <= 2.0 ** -24
+    else:
+        err = rel_err(y[fin], ref[fin]) if fin.any() else 0.0
+        assert err <= tol, f"rel err {err:.3e}"
+    # the fp16 mma.sync GEMV computes the same product
+    y16 = tp.linear(x, w, path="gemv_f16").float().cpu().numpy()
+    if kind == "tiny" and dtype == "float16":
+        assert np.abs(y16 - ref).max() <= 2.0 ** -24
+    elif fin.any():
+        assert rel_err(y16[fin], ref[fin]) <= tol
+
+
+def test_gemv_s8_exact_integer_cases(tp):
+    # integer activations and +-1 weights with scale 1: every block sum is exact -> bitwise results
+    rng = np.random.default_rng(5)
+    rows, cols = 256, 4096
+    W = (rng.integers(0, 3, size=(rows, cols)) - 1).astype(np.float32)
+    w = tp.pack_matrix(W, tp.DType.TQ2).to_device()
+    x = torch.from_numpy(rng.integers(-8, 9, size=(2, cols)).astype(np.float32)).half().cuda()
+    y = tp.linear(x, w).float().cpu().numpy()
+    ref = (x.float().cpu().numpy().astype(np.float64) @ W.T.astype(np.float64))
+    np.testing.assert_array_equal(y, ref.astype(np.float16).astype(np.float32))
+    for ctas in (1, 7, 148):   # exact sums: any partition gives the same bits
+        np.testing.assert_array_equal(tp.linear(x, w, ctas=ctas).float().cpu().numpy(), y)
