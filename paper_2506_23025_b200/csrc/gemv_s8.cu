@@ -91,16 +91,20 @@ template <typename T>
 __device__ __forceinline__ float s8_rnd(float v) { return Act<T>::to_float(Act<T>::from_float(v)); }
 
 template <typename T>
+__device__ __noinline__ uint4 s8_load8_slow(const T* row, int64_t k, int cols) {   // ragged / unaligned rows
+  T tmp[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) tmp[e] = (k + e < cols) ? row[k + e] : Act<T>::from_float(0.0f);
+  return *reinterpret_cast<uint4*>(tmp);
+}
+template <typename T>
 __device__ __forceinline__ uint4 s8_load8(const T* row, int64_t k, int cols, int vec) {
   if (vec && k + 8 <= cols) {
     uint4 r;
     asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];\n" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(row + k));
     return r;
   }
-  T tmp[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) tmp[e] = (k + e < cols) ? row[k + e] : Act<T>::from_float(0.0f);
-  return *reinterpret_cast<uint4*>(tmp);
+  return s8_load8_slow(row, k, cols);
 }
 
 // Whole warp: lane l holds the activations of columns kb*256 + 8l .. +7 of batch row br (already
@@ -112,9 +116,8 @@ __device__ __forceinline__ void s8_stage_block(const float (&f)[8], uint8_t* xs,
   float m = 0.0f;
 #pragma unroll
   for (int e = 0; e < 8; ++e) m = fmaxf(m, fabsf(f[e]));
-#pragma unroll
-  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  int ex = ((__float_as_int(m) >> 23) & 0xFF) - 127;   // 2^ex <= m < 2^(ex+1)
+  const unsigned mb = __reduce_max_sync(0xffffffffu, __float_as_uint(m));   // |x| >= 0: bits order as floats
+  int ex = (int)((mb >> 23) & 0xFF) - 127;               // 2^ex <= max|x| < 2^(ex+1)
   ex = ex < -90 ? -90 : ex;                              // zero / tiny blocks: any grid is exact enough
   const int c = lane >> 3, mm = lane & 7;
   // columns 8mm + e: field class j = (2mm + (e >> 2)) & 3; X = rint(x * 2^(23-ex) * 4^(3-j)), |X| <= 2^30
@@ -168,14 +171,22 @@ __device__ __forceinline__ void s8_stage_block(const float (&f)[8], uint8_t* xs,
 }
 
 __device__ __forceinline__ void imma(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
+  asm(
       "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
       : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+// D = A B + C with C in separate registers (the first MMA of a chain starts from -Cs or 0)
+__device__ __forceinline__ void imma_c(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1, int c0, int c1,
+                                       int c2, int c3) {
+  asm(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%11,%12,%13};\n"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "r"(c0), "r"(c1), "r"(c2), "r"(c3));
+}
 __device__ __forceinline__ uint32_t u4c(const uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 
-template <typename T, int NW>
+template <typename T, int NW, int PRE>
 __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Args a) {
   using Cfg = S8Cfg<NW>;
   constexpr int kSlotBytes = Cfg::kSlotBytes;
@@ -233,15 +244,20 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   // weights do not depend on the previous kernel: prefetch before griddepcontrol.wait
   // (dev knob dbg&4: after it; dbg&8: one slot before, the rest after)
   const int pre_slots = (a.dbg & 4) ? 0 : (a.dbg & 8) ? 1 : NS;
+  const bool ring_after_staging = (a.dbg & 12) == 12;   // dev probe: the whole ring after x is staged
   if (lane == 0)
     for (int s = 0; s < pre_slots; ++s) issue(s);
   __syncwarp();
   griddep_launch_dependents();
+  if (!(a.dbg & 1)) {   // warm the instruction cache with the staging code while the previous kernel drains
+    float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    s8_stage_block(z, xs, ncs, fsc, nrx, 0, 0);   // (item 0 is restaged below)
+  }
   griddep_wait();   // x belongs to the previous kernel until here
   stamp(1);
   // the rest of the ring is issued right after this warp's first activation loads, so those
   // loads are not queued behind the weight stream
-  bool rest_issued = pre_slots >= NS;
+  bool rest_issued = pre_slots >= NS || ring_after_staging;
   auto issue_rest = [&]() {
     if (!rest_issued) {
       if (lane == 0)
@@ -252,10 +268,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
 
   // ---- stage the activations as int8 slices (fused producer first when asked)
   const T* xg = reinterpret_cast<const T*>(a.x);
-  if (a.pre == 1) {   // x = rmsnorm(x + delta) * gamma; CTA 0 stores x + delta (the residual)
+  if (PRE == 1) {   // x = rmsnorm(x + delta) * gamma; CTA 0 stores x + delta (the residual)
     float* ss_buf = red;   // nb * nrx partial sums of squares, then nrx inverse RMS
     for (int item = warp; item < nb * nrx; item += NW) {
-      const int kb = item / nrx, br = item % nrx;
+      const int kb = item >> (nrx - 1), br = item & (nrx - 1);   // nrx is 1 or 2
       const int64_t kx = (int64_t)kb * kBlock + lane * 8;
       float f[8];
       const uint4 xv = s8_load8(xg + br * a.ldx, kx, a.cols, a.x_vec);
@@ -298,7 +314,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
     __syncthreads();
     const T* gam = reinterpret_cast<const T*>(a.pre_gamma);
     for (int item = warp; item < nb * nrx; item += NW) {
-      const int kb = item / nrx, br = item % nrx;
+      const int kb = item >> (nrx - 1), br = item & (nrx - 1);   // nrx is 1 or 2
       const int64_t kx = (int64_t)kb * kBlock + lane * 8;
       float f[8], gm[8];
       s8_f8<T>(*reinterpret_cast<const uint4*>(xs + (size_t)item * kS8ItemBytes + lane * 16), f);
@@ -317,29 +333,41 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
       for (int i = 0; i < 4; ++i) {
         const int item = i0 + i * NW;
         if (item < n_items) {
-          const int kb = item / nrx, br = item % nrx;
+          const int kb = item >> (nrx - 1), br = item & (nrx - 1);   // nrx is 1 or 2
           const int64_t kx = (int64_t)kb * kBlock + lane * 8;
           va[i] = s8_load8(xg + br * a.ldx, kx, a.cols, a.x_vec);
-          if (a.pre == 2) vb[i] = s8_load8(xg + br * a.ldx + a.cols, kx, a.cols, a.x_vec);
+          if (PRE == 2) vb[i] = s8_load8(xg + br * a.ldx + a.cols, kx, a.cols, a.x_vec);
         }
       }
       issue_rest();
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
+#pragma unroll 1
+      for (int i = 0; i < 4; ++i) {   // one copy of the staging code; the loaded rows rotate down
         const int item = i0 + i * NW;
         if (item < n_items) {
-          const int kb = item / nrx, br = item % nrx;
+          const int kb = item >> (nrx - 1), br = item & (nrx - 1);   // nrx is 1 or 2
           const int64_t kx = (int64_t)kb * kBlock + lane * 8;
           float f[8];
-          s8_f8<T>(va[i], f);
-          if (a.pre == 2) {
+          s8_f8<T>(va[0], f);
+          if (i == 0 && i0 == warp) {   // dev trace: when the first activation load has landed
+            __syncwarp();
+            if (trace && lane == 0 && f[0] != 12345.0f) stamp(11);
+          }
+          if (PRE == 2) {
             float up[8];
-            s8_f8<T>(vb[i], up);
+            s8_f8<T>(vb[0], up);
 #pragma unroll
             for (int e = 0; e < 8; ++e)
               f[e] = kx + e < a.cols ? s8_rnd<T>(s8_rnd<T>(f[e] / (1.0f + __expf(-f[e]))) * up[e]) : 0.0f;
           }
           s8_stage_block(f, xs, ncs, fsc, nrx, kb, br);
+        }
+        va[0] = va[1];
+        va[1] = va[2];
+        va[2] = va[3];
+        if (PRE == 2) {
+          vb[0] = vb[1];
+          vb[1] = vb[2];
+          vb[2] = vb[3];
         }
       }
     }
@@ -347,6 +375,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   issue_rest();
   stamp(8);
   __syncthreads();
+  if (ring_after_staging && lane == 0)
+    for (int s = 0; s < NS; ++s) issue(s);
   stamp(2);
 
   // ---- main loop: units [wu0, wu1), tile by tile
@@ -354,7 +384,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   const int nBc = g & (4 * nrx - 1);          // B column of this lane: slice-column g
   const int bB = nBc >> 2, sB = nBc & 3;
   const int swB = ((c >> 1) << 1) | (sB & 1);
-  const uint8_t* xsB = xs + (size_t)bB * kS8ItemBytes + sB * 256 + c * 64;
+  // B fragment base in shared space: the group swizzle (q ^ swB) becomes an XOR on bits 4-5
+  const uint32_t xsB32 = smem_u32(xs + (size_t)bB * kS8ItemBytes + sB * 256 + c * 64) ^ (uint32_t)(swB << 4);
+  const int kb_shift = 9 + nrx;                // log2(nrx * kS8ItemBytes)
   const int bD = min(c >> 1, nrx - 1);         // D columns of this lane: slices 2(c&1), +1 of row c>>1
   const int32_t* ncsD = ncs + bD * 4 + 2 * (c & 1);
   const float* fscD = fsc + bD;
@@ -386,22 +418,44 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
     if (lane == 0) slot_tile[2 * warp + which] = tile;
   };
 
-  auto do_unit = [&](const uint4& wl, const uint4& wh, uint32_t sv, int kb) {
-    const uint8_t* xp = xsB + (size_t)kb * nrx * kS8ItemBytes;
-    uint4 xw[4];
+  // The two units of a ring slot: their 16 IMMAs run as four independent accumulator
+  // chains (even / odd MMAs of each unit) so the tensor pipe sees 4-deep chains, not 8+8.
+  auto mma_pair = [&](const uint4 (&wl)[kS8SU], const uint4 (&wh)[kS8SU], const int (&kbq)[kS8SU],
+                      int (&D)[kS8SU][4]) {
+    uint4 xw[kS8SU][4];
+    int2 cs[kS8SU];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) xw[q] = lds128(xp + ((q ^ swB) << 4));
-    const int2 cs = *reinterpret_cast<const int2*>(ncsD + kb * nrx * 4);
-    int d[4] = {cs.x, cs.y, cs.x, cs.y};
+    for (int q = 0; q < kS8SU; ++q) {
+      const uint32_t xp = xsB32 + ((uint32_t)kbq[q] << kb_shift);
+#pragma unroll
+      for (int i4 = 0; i4 < 4; ++i4) xw[q][i4] = ld_shared_v4u(xp ^ (i4 << 4));
+      cs[q] = *reinterpret_cast<const int2*>(ncsD + (kbq[q] << (nrx + 1)));
+    }
+    int da[kS8SU][4], db[kS8SU][4];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int w = i >> 1, j0 = 2 * (i & 1);
-      const uint32_t lw = u4c(wl, w), hw = u4c(wh, w);
       const uint32_t m0 = 0x03030303u << (2 * j0), m1 = 0x03030303u << (2 * j0 + 2);
-      const uint32_t A[4] = {lw & m0, hw & m0, lw & m1, hw & m1};
-      imma(d, A, u4c(xw[w], j0), u4c(xw[w], j0 + 1));
+#pragma unroll
+      for (int q = 0; q < kS8SU; ++q) {
+        const uint32_t lw = u4c(wl[q], w), hw = u4c(wh[q], w);
+        const uint32_t A[4] = {lw & m0, hw & m0, lw & m1, hw & m1};
+        const uint32_t b0 = u4c(xw[q][w], j0), b1 = u4c(xw[q][w], j0 + 1);
+        if (i == 0)
+          imma_c(da[q], A, b0, b1, cs[q].x, cs[q].y, cs[q].x, cs[q].y);
+        else if (i == 1)
+          imma_c(db[q], A, b0, b1, 0, 0, 0, 0);
+        else
+          imma((i & 1) ? db[q] : da[q], A, b0, b1);
+      }
     }
-    const float fb = fscD[kb * nrx];
+#pragma unroll
+    for (int q = 0; q < kS8SU; ++q)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) D[q][e] = da[q][e] + db[q][e];
+  };
+  auto epilogue = [&](const int (&d)[4], uint32_t sv, int kbq) {   // block scale x grid, into the row sums
+    const float fb = fscD[kbq * nrx];
     const float2 sc = __half22float2(*reinterpret_cast<const __half2*>(&sv));
     const int v0 = d[0] + d[1] * 256, v1 = d[2] + d[3] * 256;
     acc0 = fmaf((float)v0, sc.x * fb, acc0);
@@ -440,23 +494,37 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
         sv[q] = *reinterpret_cast<const uint32_t*>(slot + q * kUnitBytes + kTileBlockBytes + g * 4);
       }
     }
+    // blocks of the slot's units (a partial last slot recomputes unit 0 and drops it)
+    int kbq[kS8SU];
+    bool wrap[kS8SU];
+#pragma unroll
+    for (int q = 0; q < kS8SU; ++q) {
+      wrap[q] = q < n && kb == nb;
+      if (wrap[q]) kb = 0;
+      kbq[q] = q < n ? kb : kbq[0];
+      if (q < n) ++kb;
+      if (q >= n) {
+        wl[q] = wl[0];
+        wh[q] = wh[0];
+      }
+    }
+#ifdef S8_NOMATH   // dev probe: stream the weights only (wrong results)
+    acc0 += __uint_as_float(wl[0].x ^ wh[1].y ^ sv[0]);
+#else
+    int D[kS8SU][4];
+    mma_pair(wl, wh, kbq, D);
 #pragma unroll
     for (int q = 0; q < kS8SU; ++q) {
       if (q < n) {
-        if (kb == nb) {   // next tile
+        if (wrap[q]) {   // next tile
           close_tile(cur);
           acc0 = acc1 = 0.0f;
           ++cur;
-          kb = 0;
         }
-#ifdef S8_NOMATH   // dev probe: stream the weights only (wrong results)
-        acc0 += __uint_as_float(wl[q].x ^ wh[q].y ^ sv[q]);
-#else
-        do_unit(wl[q], wh[q], sv[q], kb);
-#endif
-        ++kb;
+        epilogue(D[q], sv[q], kbq[q]);
       }
     }
+#endif
     u += n;
   }
   stamp(9);
@@ -491,7 +559,10 @@ static int s8_ns(int n_tiles, int nb, int grid) {
   return ops >= kS8NSMax ? kS8NSMax : ops > 2 ? 4 : ops > 1 ? 2 : 1;
 }
 
-constexpr int kS8SmallCtaUnits = 48;   // units per CTA at or below which 8 warps x 2 CTAs/SM are used
+#ifndef S8_SMALL_UNITS
+#define S8_SMALL_UNITS 48
+#endif
+constexpr int kS8SmallCtaUnits = S8_SMALL_UNITS;   // units per CTA at or below which 8 warps x 2 CTAs/SM are used
 
 static bool s8_small(int n_tiles, int nb, int grid) { return (int64_t)ceil_div(n_tiles, grid) * nb <= kS8SmallCtaUnits; }
 
@@ -518,9 +589,9 @@ bool gemv_s8_fits(int batch, int rows, int cols) {
   return sm <= 227 * 1024 && (ns >= 2 || s8_ns<16>(n_tiles, nb, grid) < 2);
 }
 
-template <typename T, int NW>
-static int launch_s8(S8Args& a, int grid, int pdl, cudaStream_t st) {
-  auto kern = k_gemv_s8<T, NW>;
+template <typename T, int NW, int PRE>
+static int launch_s8_k(S8Args& a, int grid, int pdl, cudaStream_t st) {
+  auto kern = k_gemv_s8<T, NW, PRE>;
   static int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -549,6 +620,12 @@ static int launch_s8(S8Args& a, int grid, int pdl, cudaStream_t st) {
     return -1;
   }
   return 0;
+}
+template <typename T, int NW>
+static int launch_s8(S8Args& a, int grid, int pdl, cudaStream_t st) {   // one kernel per fused producer
+  if (a.pre == 1) return launch_s8_k<T, NW, 1>(a, grid, pdl, st);
+  if (a.pre == 2) return launch_s8_k<T, NW, 2>(a, grid, pdl, st);
+  return launch_s8_k<T, NW, 0>(a, grid, pdl, st);
 }
 
 int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows, int cols,

@@ -29,4 +29,4 @@ for i in (2, 3, 4):
     wt = raw[i][148 * 8: 148 * 8 + 148 * NW * 4].reshape(148, NW, 4)
     med = lambda v: np.median(v - t0) / 1e3
     print(f"layer {i}: start {med(cta[:,0]):.2f} waited {med(cta[:,1]):.2f} staged {med(cta[:,2]):.2f} end {med(cta[:,3]):.2f}/{(cta[:,3]-t0).max()/1e3:.2f}"
-          f" | warp staged {med(wt[:,:,0]):.2f} loopend med {med(wt[:,:,1]):.2f} max {(wt[:,:,1]-t0).max()/1e3:.2f} done {med(wt[:,:,2]):.2f}")
+          f" | warp x-landed {med(wt[:,:,3]):.2f} staged {med(wt[:,:,0]):.2f} loopend med {med(wt[:,:,1]):.2f} max {(wt[:,:,1]-t0).max()/1e3:.2f} done {med(wt[:,:,2]):.2f}")
