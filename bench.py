@@ -399,9 +399,12 @@ def run_ours(args, rank, world, dist):
     if rank == 0:
         cpu = CpuReference(os.cpu_count() or 1).sample(args.cpu_seconds)
         traffic = None
+        kernel_name = "k_gemv_s8"
         prof = os.path.join(ROOT, "profiles", "r01_ncu_full_summary.json")
         if os.path.exists(prof):   # one `ncu --set full` capture of the GEMV (scripts/profile_round.sh)
-            g = json.load(open(prof)).get("k_gemv_tq2", {})
+            summ = json.load(open(prof))
+            g = summ.get("gemv") or summ.get("k_gemv_tq2", {})
+            kernel_name = g.get("kernel") or "k_gemv_tq2"
             if g.get("dram__bytes_read.sum"):
                 traffic = {"bytes_per_launch": round((float(g["dram__bytes_read.sum"]) +
                                                       float(g.get("dram__bytes_write.sum") or 0)) * 1e6),
@@ -417,7 +420,7 @@ def run_ours(args, rank, world, dist):
                        "launches_per_step": stack.launches, "graph": "CUDA graph, PDL-chained"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "k_gemv_tq2", "avg_launch_us": round(per_launch_us, 3)},
+                         "kernel": kernel_name, "avg_launch_us": round(per_launch_us, 3)},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": stack.launches * args.steps,

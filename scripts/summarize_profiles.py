@@ -35,10 +35,11 @@ keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 summ = {}
-for name, rep, shape in [("k_gemv_tq2", "gpurun_out/prof_gemv.ncu-rep", "rows 11008 x cols 4096, batch 1, fp16"),
-                         ("k_gemm_umma", "gpurun_out/prof_umma.ncu-rep", "rows 11008 x cols 4096, batch 128, fp16")]:
+for name, rep, shape in [("gemv", "gpurun_out/prof_gemv.ncu-rep", "rows 11008 x cols 4096, batch 1, fp16"),
+                         ("umma", "gpurun_out/prof_umma.ncu-rep", "rows 11008 x cols 4096, batch 128, fp16")]:
     m = raw(rep)
-    e = {k: m.get(k) for k in keys}
+    e = {"kernel": (m.get("Kernel Name") or m.get("Function Name") or "").split("(")[0]}
+    e.update({k: m.get(k) for k in keys})
     e["shape"] = shape
     e["units"] = "time us, dram bytes MB, smem KB (ncu --set full, one launch, cold, --clock-control none)"
     summ[name] = e
