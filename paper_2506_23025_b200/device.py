@@ -20,6 +20,9 @@ _ACT = {torch.float16: _lib.ACT_F16, torch.bfloat16: _lib.ACT_BF16}
 _WORKSPACES: dict = {}
 
 
+_RETIRED_WORKSPACES: list = []
+
+
 def workspace(nbytes: int, device=None, stream=None) -> torch.Tensor:
     """Per-(device, stream) zero-initialised workspace for tr_linear, grown on demand.
 
@@ -32,6 +35,8 @@ def workspace(nbytes: int, device=None, stream=None) -> torch.Tensor:
     buf = _WORKSPACES.get(key)
     if buf is None or buf.numel() < nbytes:
         size = max(nbytes, 1 << 20, 0 if buf is None else 2 * buf.numel())
+        if buf is not None:   # a captured CUDA graph may still point at it: never free
+            _RETIRED_WORKSPACES.append(buf)
         buf = torch.zeros(size, dtype=torch.uint8, device=dev)
         _WORKSPACES[key] = buf
     return buf
