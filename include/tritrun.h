@@ -158,6 +158,10 @@ TR_API int tr_attn_decode(int act_dtype, const void* qkv, const int64_t* pos, co
                           float scale, void* stream);
 /* gu [T, 2F] = (gate | up) -> out [T, F] = silu(gate) * up */
 TR_API int tr_silu_mul(int act_dtype, const void* gu, void* out, int64_t tokens, int64_t ff, void* stream);
+/* greedy decode step: idx = argmax(logits [vocab]) (lowest index among ties); out_tokens[pos[0]] = idx
+ * (if pos[0] < max_pos); tok[0] = idx; pos[0] += 1; h_next [d] = embed [vocab, d] row idx.  int64 on device. */
+TR_API int tr_greedy_next(int act_dtype, const void* logits, int64_t vocab, int64_t* out_tokens, int64_t max_pos,
+                          int64_t* tok, int64_t* pos, const void* embed, int64_t d, void* h_next, void* stream);
 
 #ifdef __cplusplus
 }

@@ -66,6 +66,7 @@ _SIGS = {
     "tr_linear_chain": ([_int, ctypes.POINTER(TrChainLayer), _i64, _i64, _int, _c_p, ctypes.c_size_t, _c_p], _int),
     "tr_add_rmsnorm": ([_int, _c_p, _c_p, _c_p, _c_p, _i64, _i64, ctypes.c_float, _c_p], _int),
     "tr_rope_kv": ([_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _i64, _i64, _i64, _i64, _c_p], _int),
+    "tr_greedy_next": ([_int, _c_p, _i64, _c_p, _i64, _c_p, _c_p, _c_p, _i64, _c_p, _c_p], _int),
     "tr_attn_decode": ([_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _i64, _i64, _i64, ctypes.c_float, _c_p],
                        _int),
     "tr_silu_mul": ([_int, _c_p, _c_p, _i64, _i64, _c_p], _int),

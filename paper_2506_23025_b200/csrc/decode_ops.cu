@@ -126,8 +126,14 @@ __global__ void k_rope_kv(const T* __restrict__ qkv, const int64_t* __restrict__
 
 // One decode token, fused: rotary q/k of head hh from qkv [3, H, D], k/v appended to the
 // caches [H, S, D] at pos, then out[hh] = softmax(q k^T * scale over keys 0..pos) v.
-// One CTA (128 threads) per head; thread t scores key t with 16-byte loads issued up front,
-// the value sum is split over the 4 warps (lanes cover D) and combined in fixed order.
+// One CTA (128 threads) per head.  Right after griddepcontrol.wait every load is issued at
+// once -- this token's q/k/v, thread t's cached key t (16-byte loads into registers) and all
+// cached values (cp.async into shared memory) -- so the kernel pays one memory latency, not
+// three.  Thread t scores key t; the value sum is split over the 4 warps (lanes cover D) and
+// combined in fixed order.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 template <typename T, int D>
 __global__ void __launch_bounds__(128) k_attn_decode(const T* __restrict__ qkv, const int64_t* __restrict__ pos,
                                                      const T* __restrict__ cs, const T* __restrict__ sn,
@@ -136,35 +142,53 @@ __global__ void __launch_bounds__(128) k_attn_decode(const T* __restrict__ qkv, 
   griddep_wait();
   griddep_launch_dependents();
   static_assert(D == 128, "one key per thread, 4 dims per lane");
+  __shared__ __align__(16) T vs[128][D];   // values of keys 0..pos
+  __shared__ __align__(16) T kp[D];        // this token's rotated key
   __shared__ float qs[D];
   __shared__ float sc[128];
   __shared__ float part[4][D];
   __shared__ float red[32];
   const int hh = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int p = (int)pos[0], n = p + 1;
-  // rotary embedding of this token's q and k; k and v into the caches
+  const T* kb = kc + (int64_t)hh * S * D;
+  const T* vb = vc + (int64_t)hh * S * D;
+  // cached values -> shared memory (asynchronous), cached key tid -> registers
+  for (int c = tid; c < p * (D / 8); c += 128) cp_async16(&vs[c / (D / 8)][(c % (D / 8)) * 8], vb + (int64_t)c * 8);
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  uint4 kv[D / 8];
+  if (tid < p) {
+    const uint4* kr = reinterpret_cast<const uint4*>(kb + (int64_t)tid * D);
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) kv[j] = kr[j];
+  }
+  // rotary embedding of this token's q and k; k and v into the caches (and shared memory)
   if (tid < D / 2) {
     const float c = to_f(cs[(int64_t)p * (D / 2) + tid]), s = to_f(sn[(int64_t)p * (D / 2) + tid]);
     const float q1 = to_f(qkv[hh * D + 2 * tid]), q2 = to_f(qkv[hh * D + 2 * tid + 1]);
     const float k1 = to_f(qkv[(H + hh) * D + 2 * tid]), k2 = to_f(qkv[(H + hh) * D + 2 * tid + 1]);
+    const T v1 = qkv[(2 * H + hh) * D + 2 * tid], v2 = qkv[(2 * H + hh) * D + 2 * tid + 1];
     qs[2 * tid] = to_f(Act<T>::from_float(q1 * c - q2 * s));
     qs[2 * tid + 1] = to_f(Act<T>::from_float(q1 * s + q2 * c));
+    const T r1 = Act<T>::from_float(k1 * c - k2 * s), r2 = Act<T>::from_float(k1 * s + k2 * c);
+    kp[2 * tid] = r1;
+    kp[2 * tid + 1] = r2;
+    vs[p][2 * tid] = v1;
+    vs[p][2 * tid + 1] = v2;
     T* ko = kc + ((int64_t)hh * S + p) * D;
-    ko[2 * tid] = Act<T>::from_float(k1 * c - k2 * s);
-    ko[2 * tid + 1] = Act<T>::from_float(k1 * s + k2 * c);
+    ko[2 * tid] = r1;
+    ko[2 * tid + 1] = r2;
     T* vo = vc + ((int64_t)hh * S + p) * D;
-    vo[2 * tid] = qkv[(2 * H + hh) * D + 2 * tid];
-    vo[2 * tid + 1] = qkv[(2 * H + hh) * D + 2 * tid + 1];
+    vo[2 * tid] = v1;
+    vo[2 * tid + 1] = v2;
   }
-  __threadfence_block();
   __syncthreads();
-  // scores: thread tid <-> key tid
+  // scores: thread tid <-> key tid (this token's key from shared memory)
   float v = -INFINITY;
-  if (tid < n) {
-    const uint4* kr = reinterpret_cast<const uint4*>(kc + ((int64_t)hh * S + tid) * D);
-    uint4 kv[D / 8];
+  if (tid <= p) {
+    if (tid == p) {
 #pragma unroll
-    for (int j = 0; j < D / 8; ++j) kv[j] = kr[j];
+      for (int j = 0; j < D / 8; ++j) kv[j] = reinterpret_cast<const uint4*>(kp)[j];
+    }
     float acc = 0.0f;
 #pragma unroll
     for (int j = 0; j < D / 8; ++j) {
@@ -183,31 +207,100 @@ __global__ void __launch_bounds__(128) k_attn_decode(const T* __restrict__ qkv, 
   m = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
   const float e = tid < n ? __expf(v - m) : 0.0f;
   sc[tid] = e;
-  const float z = block_sum(e, red);   // (syncs; sc visible afterwards)
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");   // (block_sum syncs: values visible after it)
+  const float z = block_sum(e, red);
   // value sum: warp w takes keys w, w+4, ...; lane covers dims 4 lane .. 4 lane + 3
   float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-  for (int s0 = warp; s0 < n; s0 += 16) {
-    uint2 vv[4];
+  for (int s0 = warp; s0 < n; s0 += 4) {
+    const uint2 vv = *reinterpret_cast<const uint2*>(&vs[s0][4 * lane]);
+    const T* ve = reinterpret_cast<const T*>(&vv);
+    const float w = sc[s0];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int s = s0 + 4 * u;
-      vv[u] = s < n ? *reinterpret_cast<const uint2*>(vc + ((int64_t)hh * S + s) * D + 4 * lane) : make_uint2(0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int s = s0 + 4 * u;
-      if (s < n) {
-        const T* ve = reinterpret_cast<const T*>(&vv[u]);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[q] += sc[s] * to_f(ve[q]);
-      }
-    }
+    for (int q = 0; q < 4; ++q) acc[q] += w * to_f(ve[q]);
   }
 #pragma unroll
   for (int q = 0; q < 4; ++q) part[warp][4 * lane + q] = acc[q];
   __syncthreads();
   const float r = ((part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid])) / z;
   out[(int64_t)hh * D + tid] = Act<T>::from_float(r);
+}
+
+// Greedy decode bookkeeping in one kernel (one CTA of 1024 threads): idx = argmax(logits)
+// (lowest index among equal maxima), out_tokens[pos] = idx, tok = idx, pos += 1, and the next
+// token's embedding row h_next = embed[idx] -- replacing argmax + index_copy + add + the
+// embedding gather of the next step (four launches, ~30 us on B200) by one.
+template <typename T>
+__global__ void __launch_bounds__(1024) k_greedy_next(const T* __restrict__ logits, int vocab,
+                                                      int64_t* __restrict__ out_tokens, int max_pos,
+                                                      int64_t* __restrict__ tok, int64_t* __restrict__ pos,
+                                                      const T* __restrict__ embed, int d, T* __restrict__ h_next) {
+  griddep_wait();
+  griddep_launch_dependents();
+  __shared__ float bv[32];
+  __shared__ int bi[32];
+  __shared__ int best_idx;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float best = -INFINITY;
+  int idx = 0x7fffffff;
+  const bool vec = (vocab % 8) == 0 && ((uintptr_t)logits % 16) == 0;
+  if (vec) {
+    for (int i = tid * 8; i < vocab; i += 1024 * 8) {
+      float f[8];
+      unpack8<T>(*reinterpret_cast<const uint4*>(logits + i), f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (f[e] > best) {   // ascending indices per thread: strict > keeps the lowest
+          best = f[e];
+          idx = i + e;
+        }
+    }
+  } else {
+    for (int i = tid; i < vocab; i += 1024) {
+      const float f = to_f(logits[i]);
+      if (f > best) {
+        best = f;
+        idx = i;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > best || (ov == best && oi < idx)) {
+      best = ov;
+      idx = oi;
+    }
+  }
+  if (lane == 0) {
+    bv[warp] = best;
+    bi[warp] = idx;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    best = bv[lane];
+    idx = bi[lane];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (ov > best || (ov == best && oi < idx)) {
+        best = ov;
+        idx = oi;
+      }
+    }
+    if (lane == 0) {
+      if (idx >= vocab) idx = 0;   // all -inf / NaN logits
+      best_idx = idx;
+      const int64_t p = pos[0];
+      if (p < max_pos) out_tokens[p] = idx;
+      tok[0] = idx;
+      pos[0] = p + 1;
+    }
+  }
+  __syncthreads();
+  const T* row = embed + (int64_t)best_idx * d;
+  for (int j = tid; j < d; j += 1024) h_next[j] = row[j];
 }
 
 // gu [T, 2F] = (gate | up) -> out [T, F] = silu(gate) * up   (8 elements per thread)
@@ -331,6 +424,19 @@ int tr_silu_mul(int act, const void* gu, void* out, int64_t tokens, int64_t ff, 
                   (launch_pdl(k_silu_mul<__nv_bfloat16>, dim3(grid), dim3(256), 0, st, (const __nv_bfloat16*)gu,
                               (__nv_bfloat16*)out, (int)ff, n8)));
   return check_launch("tr_silu_mul");
+}
+
+int tr_greedy_next(int act, const void* logits, int64_t vocab, int64_t* out_tokens, int64_t max_pos, int64_t* tok,
+                   int64_t* pos, const void* embed, int64_t d, void* h_next, void* stream) {
+  TR_REQUIRE(vocab >= 1 && vocab < (1LL << 31) && d >= 1 && max_pos >= 0, "tr_greedy_next: bad sizes");
+  cudaStream_t st = (cudaStream_t)stream;
+  TR_ACT_DISPATCH(act,
+                  (launch_pdl(k_greedy_next<__half>, dim3(1), dim3(1024), 0, st, (const __half*)logits, (int)vocab,
+                              out_tokens, (int)max_pos, tok, pos, (const __half*)embed, (int)d, (__half*)h_next)),
+                  (launch_pdl(k_greedy_next<__nv_bfloat16>, dim3(1), dim3(1024), 0, st, (const __nv_bfloat16*)logits,
+                              (int)vocab, out_tokens, (int)max_pos, tok, pos, (const __nv_bfloat16*)embed, (int)d,
+                              (__nv_bfloat16*)h_next)));
+  return check_launch("tr_greedy_next");
 }
 
 }  // extern "C"

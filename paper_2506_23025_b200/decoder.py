@@ -97,6 +97,7 @@ class TernaryDecoder:
         self.tok = torch.zeros(1, dtype=torch.long, device=self.device)
         self.pos = torch.zeros(1, dtype=torch.long, device=self.device)
         self.out_tokens = torch.zeros(S, dtype=torch.long, device=self.device)
+        self.h0 = torch.zeros((1, d), device=self.device, dtype=dtype)   # embedding row of the next token
         self.graph = None
 
     # -- building blocks ----------------------------------------------------------------
@@ -129,10 +130,11 @@ class TernaryDecoder:
         g, u = gu[:, : cfg.d_ff], gu[:, cfg.d_ff:]
         return h + self._lin(F.silu(g) * u, lw["down"])
 
-    def forward(self, tokens, pos):
-        """tokens [T] at positions pos [T] -> logits of the last position [vocab] (fills the cache)."""
+    def forward(self, tokens, pos, h_in=None):
+        """tokens [T] at positions pos [T] -> logits of the last position [vocab] (fills the cache).
+        h_in: the tokens' embedding rows when already gathered (the fused decode step)."""
         if self.fused:
-            return self._forward_fused(tokens, pos)
+            return self._forward_fused(tokens, pos, h_in)
         T = tokens.shape[0]
         h = self.weights["embed"][tokens]
         for i in range(self.cfg.n_layers):
@@ -140,15 +142,17 @@ class TernaryDecoder:
         h = self._rms(h[-1:], self.norm_out)
         return F.linear(h, self.weights["lm_head"])[0]
 
-    def _forward_fused(self, tokens, pos):
+    def _forward_fused(self, tokens, pos, h_in=None):
         """Same computation with the glue as single kernels.  Decode (T = 1) of the ternary
         model folds residual-add + RMSNorm into the QKV / gate|up GEMVs and SwiGLU into the
         down GEMV (tr_linear_pre): 5 launches per layer."""
         cfg, act, st = self.cfg, _ACT[self.dtype], _lib.stream_handle()
-        T, d, H, D, S = tokens.shape[0], cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.max_seq
+        T = tokens.shape[0] if h_in is None else h_in.shape[0]
+        d, H, D, S = cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.max_seq
         if T == 1 and not self.dense:
-            return self._decode_step_fused(tokens, pos)
-        h = self.weights["embed"][tokens].contiguous()
+            return self._decode_step_fused(tokens, pos, h_in)
+        # (h_in, the fused decode step's embedding buffer, doubles as the residual stream)
+        h = (self.weights["embed"][tokens] if h_in is None else h_in).contiguous()
         xn = torch.empty_like(h)
         q = torch.empty((T, H, D), device=self.device, dtype=self.dtype)
         delta = None
@@ -181,10 +185,11 @@ class TernaryDecoder:
                   T, d, cfg.eps, st)
         return F.linear(xn[-1:], self.weights["lm_head"])[0]
 
-    def _decode_step_fused(self, tokens, pos):
+    def _decode_step_fused(self, tokens, pos, h_in=None):
         cfg, act, st = self.cfg, _ACT[self.dtype], _lib.stream_handle()
         d, H, D, S = cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.max_seq
-        hs = [self.weights["embed"][tokens].contiguous(), torch.empty((1, d), device=self.device, dtype=self.dtype)]
+        h0 = self.weights["embed"][tokens].contiguous() if h_in is None else h_in
+        hs = [h0, torch.empty((1, d), device=self.device, dtype=self.dtype)]
         cur, delta = 0, None
         for i in range(cfg.n_layers):
             lw = self.lin[i]
@@ -212,8 +217,15 @@ class TernaryDecoder:
         logits = self.forward(prompt, torch.arange(T, device=self.device))
         self.tok.copy_(logits.argmax().view(1))
         self.pos.fill_(T)
+        self.h0.copy_(self.weights["embed"][self.tok])
 
     def _decode_body(self):
+        if self.fused:   # embedding row gathered by the previous step; greedy bookkeeping in one kernel
+            logits = self.forward(self.tok, self.pos, self.h0)
+            _lib.call("tr_greedy_next", _ACT[self.dtype], logits.data_ptr(), logits.shape[-1],
+                      self.out_tokens.data_ptr(), self.out_tokens.shape[0], self.tok.data_ptr(), self.pos.data_ptr(),
+                      self.weights["embed"].data_ptr(), self.cfg.d_model, self.h0.data_ptr(), _lib.stream_handle())
+            return
         logits = self.forward(self.tok, self.pos)
         nxt = logits.argmax().view(1)
         self.out_tokens.index_copy_(0, self.pos, nxt)
@@ -223,7 +235,7 @@ class TernaryDecoder:
     def capture(self) -> None:
         """Capture one greedy decode step (state advanced on the device) as a CUDA graph."""
         s = torch.cuda.Stream(device=self.device)
-        saved = (self.tok.clone(), self.pos.clone(), self.k_cache.clone(), self.v_cache.clone())
+        saved = (self.tok.clone(), self.pos.clone(), self.k_cache.clone(), self.v_cache.clone(), self.h0.clone())
         with torch.cuda.stream(s):
             self._decode_body()   # warm-up (lazy kernel set-up) outside capture
             s.synchronize()
@@ -235,6 +247,7 @@ class TernaryDecoder:
         self.pos.copy_(saved[1])
         self.k_cache.copy_(saved[2])
         self.v_cache.copy_(saved[3])
+        self.h0.copy_(saved[4])
 
     def decode(self, n: int) -> None:
         """n greedy decode steps as n graph replays (no host synchronisation)."""

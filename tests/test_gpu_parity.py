@@ -371,6 +371,50 @@ def test_decoder_fused_glue_matches_torch_glue(tp, dtype):
     assert torch.equal(fused.k_cache[:, :, :10], ref.k_cache[:, :, :10]) or dtype == "bfloat16" or True
 
 
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
+def test_greedy_next_kernel(tp, dtype):
+    from paper_2506_23025_b200 import _lib
+    from paper_2506_23025_b200.device import _ACT
+
+    tdt = getattr(torch, dtype)
+    vocab, d = 32000, 3072
+    g = torch.Generator(device="cuda").manual_seed(2)
+    logits = torch.randn(vocab, generator=g, device="cuda").to(tdt)
+    logits[777] = logits[31111] = 50.0   # a tie: the lower index wins (torch.argmax semantics)
+    embed = torch.randn(vocab, d, generator=g, device="cuda").to(tdt)
+    out_tokens = torch.zeros(16, dtype=torch.long, device="cuda")
+    tok = torch.zeros(1, dtype=torch.long, device="cuda")
+    pos = torch.tensor([5], dtype=torch.long, device="cuda")
+    h = torch.empty(1, d, device="cuda", dtype=tdt)
+    _lib.call("tr_greedy_next", _ACT[tdt], logits.data_ptr(), vocab, out_tokens.data_ptr(), 16, tok.data_ptr(),
+              pos.data_ptr(), embed.data_ptr(), d, h.data_ptr(), _lib.stream_handle())
+    assert int(tok) == 777 == int(torch.argmax(logits)) and int(out_tokens[5]) == 777 and int(pos) == 6
+    assert torch.equal(h[0], embed[777])
+
+
+def test_decoder_graph_decode_matches_eager_greedy(tp):
+    # graph-captured steps (fused greedy bookkeeping) == eager steps with torch.argmax
+    from paper_2506_23025_b200.decoder import DecoderConfig, TernaryDecoder
+
+    cfg = DecoderConfig(d_model=512, n_layers=2, n_heads=4, d_ff=1536, vocab=1000, max_seq=32)
+    m = TernaryDecoder(cfg, seed=5)
+    prompt = torch.randint(0, cfg.vocab, (10,), device="cuda", generator=torch.Generator(device="cuda").manual_seed(3))
+    m.reset()
+    m.prefill(prompt)
+    m.decode(6)
+    graph_tokens = m.out_tokens[10:16].clone()
+    m.reset()
+    m.prefill(prompt)
+    eager = []
+    for _ in range(6):
+        logits = m.forward(m.tok, m.pos)
+        nxt = logits.argmax().view(1)
+        eager.append(int(nxt))
+        m.tok.copy_(nxt)
+        m.pos.add_(1)
+    assert graph_tokens.tolist() == eager
+
+
 # ---------------------------------------------------------------- TQ1 (1.6-bit) decoded on the fly (config 4)
 
 @pytest.mark.parametrize("rows,cols", [(1, 5), (37, 1500), (128, 256), (300, 1000), (8192, 8192)])
