@@ -249,10 +249,6 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
     for (int s = 0; s < pre_slots; ++s) issue(s);
   __syncwarp();
   griddep_launch_dependents();
-  if (!(a.dbg & 1)) {   // warm the instruction cache with the staging code while the previous kernel drains
-    float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    s8_stage_block(z, xs, ncs, fsc, nrx, 0, 0);   // (item 0 is restaged below)
-  }
   griddep_wait();   // x belongs to the previous kernel until here
   stamp(1);
   // the rest of the ring is issued right after this warp's first activation loads, so those
