@@ -98,6 +98,8 @@ class TernaryDecoder:
         self.pos = torch.zeros(1, dtype=torch.long, device=self.device)
         self.out_tokens = torch.zeros(S, dtype=torch.long, device=self.device)
         self.h0 = torch.zeros((1, d), device=self.device, dtype=dtype)   # embedding row of the next token
+        self._positions = torch.arange(S, device=self.device)
+        self._prefill_graphs = {}
         self.graph = None
 
     # -- building blocks ----------------------------------------------------------------
@@ -211,10 +213,34 @@ class TernaryDecoder:
         return F.linear(xn, self.weights["lm_head"])[0]
 
     # -- serving --------------------------------------------------------------------------
-    def prefill(self, prompt: torch.Tensor) -> None:
-        """Run the prompt (one batched pass: the tcgen05 GEMM path) and seed the decode state."""
+    def prefill(self, prompt: torch.Tensor, graph: bool = True) -> None:
+        """Run the prompt (one batched pass: the tcgen05 GEMM path) and seed the decode state.
+
+        With ``graph`` the pass is captured once per prompt length as a CUDA graph (the prompt
+        is copied into a static buffer) and replayed, so time-to-first-token is GPU time, not
+        ~12 host launches per layer."""
         T = prompt.shape[0]
-        logits = self.forward(prompt, torch.arange(T, device=self.device))
+        if not graph:
+            self._prefill_body(prompt)
+            return
+        if T not in self._prefill_graphs:
+            buf = prompt.to(device=self.device, dtype=torch.long).clone()
+            s = torch.cuda.Stream(device=self.device)
+            with torch.cuda.stream(s):
+                self._prefill_body(buf)   # warm-up outside capture (workspaces, lazy set-up)
+                s.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    self._prefill_body(buf)
+            torch.cuda.synchronize(self.device)
+            self._prefill_graphs[T] = (g, buf)
+        g, buf = self._prefill_graphs[T]
+        buf.copy_(prompt)
+        g.replay()
+
+    def _prefill_body(self, prompt: torch.Tensor) -> None:
+        T = prompt.shape[0]
+        logits = self.forward(prompt, self._positions[:T])
         self.tok.copy_(logits.argmax().view(1))
         self.pos.fill_(T)
         self.h0.copy_(self.weights["embed"][self.tok])
