@@ -110,64 +110,89 @@ __device__ __forceinline__ uint4 s8_load8(const T* row, int64_t k, int cols, int
 // Whole warp: lane l holds the activations of columns kb*256 + 8l .. +7 of batch row br (already
 // rounded to T).  Puts the block on its integer grid, stores the 4 slices in k-slot order, and
 // -Cs and the block grid factor 2^(e-29).
-__device__ __forceinline__ void s8_stage_block(const float (&f)[8], uint8_t* xs, int32_t* ncs, float* fsc, int nrx,
-                                               int kb, int br) {
+// NI blocks at once (independent latency chains interleave); items >= nvalid are computed
+// but not stored (nvalid is warp-uniform).
+template <int NI>
+__device__ __forceinline__ void s8_stage_blocks(const float (&f)[NI][8], uint8_t* xs, int32_t* ncs, float* fsc,
+                                                int nrx, const int (&kb)[NI], const int (&br)[NI], int nvalid) {
   const int lane = threadIdx.x & 31;
-  float m = 0.0f;
-#pragma unroll
-  for (int e = 0; e < 8; ++e) m = fmaxf(m, fabsf(f[e]));
-  const unsigned mb = __reduce_max_sync(0xffffffffu, __float_as_uint(m));   // |x| >= 0: bits order as floats
-  int ex = (int)((mb >> 23) & 0xFF) - 127;               // 2^ex <= max|x| < 2^(ex+1)
-  ex = ex < -90 ? -90 : ex;                              // zero / tiny blocks: any grid is exact enough
   const int c = lane >> 3, mm = lane & 7;
+  int ex[NI];
+#pragma unroll
+  for (int t = 0; t < NI; ++t) {
+    float m = 0.0f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) m = fmaxf(m, fabsf(f[t][e]));
+    const unsigned mb = __reduce_max_sync(0xffffffffu, __float_as_uint(m));   // |x| >= 0: bits order as floats
+    ex[t] = (int)((mb >> 23) & 0xFF) - 127;              // 2^ex <= max|x| < 2^(ex+1)
+    ex[t] = ex[t] < -90 ? -90 : ex[t];                   // zero / tiny blocks: any grid is exact enough
+  }
   // columns 8mm + e: field class j = (2mm + (e >> 2)) & 3; X = rint(x * 2^(23-ex) * 4^(3-j)), |X| <= 2^30
-  uint32_t R[4][2];   // [slice][e >> 2]: the signed-byte slices of columns e = 4G .. 4G+3
+  uint32_t R[NI][4][2];   // [item][slice][e >> 2]: the signed-byte slices of columns e = 4G .. 4G+3
   int wj[2];
 #pragma unroll
   for (int G = 0; G < 2; ++G) {
     const int j = (2 * mm + G) & 3;
     wj[G] = (1 << (2 * j)) * 0x01010101;
-    const float q = __int_as_float((150 - ex + 2 * (3 - j)) << 23);
-    uint32_t Z[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      // balanced base-256 digits: the bytes of (X + 0x80808080) ^ 0x80808080 are int8 slices of X
-      Z[i] = ((uint32_t)__float2int_rn(f[4 * G + i] * q) + 0x80808080u) ^ 0x80808080u;
+    for (int t = 0; t < NI; ++t) {
+      const float q = __int_as_float((150 - ex[t] + 2 * (3 - j)) << 23);
+      uint32_t Z[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        // balanced base-256 digits: the bytes of (X + 0x80808080) ^ 0x80808080 are int8 slices of X
+        Z[i] = ((uint32_t)__float2int_rn(f[t][4 * G + i] * q) + 0x80808080u) ^ 0x80808080u;
+      }
+      const uint32_t t0 = __byte_perm(Z[0], Z[1], 0x5140), t1 = __byte_perm(Z[0], Z[1], 0x7362);
+      const uint32_t t2 = __byte_perm(Z[2], Z[3], 0x5140), t3 = __byte_perm(Z[2], Z[3], 0x7362);
+      R[t][0][G] = __byte_perm(t0, t2, 0x5410);
+      R[t][1][G] = __byte_perm(t0, t2, 0x7632);
+      R[t][2][G] = __byte_perm(t1, t3, 0x5410);
+      R[t][3][G] = __byte_perm(t1, t3, 0x7632);
     }
-    const uint32_t t0 = __byte_perm(Z[0], Z[1], 0x5140), t1 = __byte_perm(Z[0], Z[1], 0x7362);
-    const uint32_t t2 = __byte_perm(Z[2], Z[3], 0x5140), t3 = __byte_perm(Z[2], Z[3], 0x7362);
-    R[0][G] = __byte_perm(t0, t2, 0x5410);
-    R[1][G] = __byte_perm(t0, t2, 0x7632);
-    R[2][G] = __byte_perm(t1, t3, 0x5410);
-    R[3][G] = __byte_perm(t1, t3, 0x7632);
   }
-  int cs[4];
+  int cs[NI][4];
 #pragma unroll
-  for (int s = 0; s < 4; ++s) cs[s] = __dp4a((int)R[s][1], wj[1], __dp4a((int)R[s][0], wj[0], 0));
+  for (int t = 0; t < NI; ++t)
+#pragma unroll
+    for (int s = 0; s < 4; ++s) cs[t][s] = __dp4a((int)R[t][s][1], wj[1], __dp4a((int)R[t][s][0], wj[0], 0));
   // word (s, combo) = bytes {(h0,hb0), (h0,hb1), (h1,hb0), (h1,hb1)}: columns 16 apart sit in
   // lanes 2 apart; the hb = 0 lane builds pairs 0-1, its partner pairs 2-3
   const int hb = (mm >> 1) & 1;
 #pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    const uint32_t send = hb ? R[s][0] : R[s][1];
-    const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 2);
-    const uint32_t mine = hb ? R[s][1] : R[s][0];
-    const uint32_t lo = hb ? recv : mine, hi = hb ? mine : recv;
+  for (int t = 0; t < NI; ++t)
 #pragma unroll
-    for (int pl = 0; pl < 2; ++pl) {
-      const int p = pl + 2 * hb;
-      const int w = 2 * (mm >> 2) + (p & 1), j = (2 * mm + (p >> 1)) & 3;
-      const uint32_t word = __byte_perm(lo, hi, pl ? 0x7362 : 0x5140);
-      *reinterpret_cast<uint32_t*>(xs + s8_word_off(nrx, kb, br, s, c, 4 * w + j)) = word;
+    for (int s = 0; s < 4; ++s) {
+      const uint32_t send = hb ? R[t][s][0] : R[t][s][1];
+      const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 2);
+      const uint32_t mine = hb ? R[t][s][1] : R[t][s][0];
+      const uint32_t lo = hb ? recv : mine, hi = hb ? mine : recv;
+#pragma unroll
+      for (int pl = 0; pl < 2; ++pl) {
+        const int p = pl + 2 * hb;
+        const int w = 2 * (mm >> 2) + (p & 1), j = (2 * mm + (p >> 1)) & 3;
+        const uint32_t word = __byte_perm(lo, hi, pl ? 0x7362 : 0x5140);
+        if (t < nvalid) *reinterpret_cast<uint32_t*>(xs + s8_word_off(nrx, kb[t], br[t], s, c, 4 * w + j)) = word;
+      }
     }
-  }
 #pragma unroll
-  for (int s = 0; s < 4; ++s) cs[s] = __reduce_add_sync(0xffffffffu, cs[s]);
-  if (lane == 0) {
-    int4 v = make_int4(-cs[0], -cs[1], -cs[2], -cs[3]);
-    *reinterpret_cast<int4*>(ncs + (kb * nrx + br) * 4) = v;
-    fsc[kb * nrx + br] = __int_as_float((127 + ex - 29) << 23);   // 2^(ex - 29)
-  }
+  for (int t = 0; t < NI; ++t)
+#pragma unroll
+    for (int s = 0; s < 4; ++s) cs[t][s] = __reduce_add_sync(0xffffffffu, cs[t][s]);
+  if (lane == 0)
+#pragma unroll
+    for (int t = 0; t < NI; ++t)
+      if (t < nvalid) {
+        int4 v = make_int4(-cs[t][0], -cs[t][1], -cs[t][2], -cs[t][3]);
+        *reinterpret_cast<int4*>(ncs + (kb[t] * nrx + br[t]) * 4) = v;
+        fsc[kb[t] * nrx + br[t]] = __int_as_float((127 + ex[t] - 29) << 23);   // 2^(ex - 29)
+      }
+}
+__device__ __forceinline__ void s8_stage_block(const float (&f)[8], uint8_t* xs, int32_t* ncs, float* fsc, int nrx,
+                                               int kb, int br) {
+  const float(&f1)[1][8] = *reinterpret_cast<const float(*)[1][8]>(&f);
+  const int k1[1] = {kb}, b1[1] = {br};
+  s8_stage_blocks<1>(f1, xs, ncs, fsc, nrx, k1, b1, 1);
 }
 
 __device__ __forceinline__ void imma(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -337,33 +362,33 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
       }
       issue_rest();
 #pragma unroll 1
-      for (int i = 0; i < 4; ++i) {   // one copy of the staging code; the loaded rows rotate down
-        const int item = i0 + i * NW;
-        if (item < n_items) {
-          const int kb = item >> (nrx - 1), br = item & (nrx - 1);   // nrx is 1 or 2
-          const int64_t kx = (int64_t)kb * kBlock + lane * 8;
-          float f[8];
-          s8_f8<T>(va[0], f);
-          if (i == 0 && i0 == warp) {   // dev trace: when the first activation load has landed
-            __syncwarp();
-            if (trace && lane == 0 && f[0] != 12345.0f) stamp(11);
-          }
+      for (int i = 0; i < 4; i += 2) {   // two blocks per pass (their latency chains interleave)
+        float f[2][8];
+        int kbs[2], brs[2];
+        int nv = 0;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int item = i0 + (i + t) * NW;
+          const int it = item < n_items ? item : i0;
+          kbs[t] = it >> (nrx - 1);
+          brs[t] = it & (nrx - 1);
+          nv += item < n_items;
+          const int64_t kx = (int64_t)kbs[t] * kBlock + lane * 8;
+          s8_f8<T>(va[t], f[t]);
           if (PRE == 2) {
             float up[8];
-            s8_f8<T>(vb[0], up);
+            s8_f8<T>(vb[t], up);
 #pragma unroll
             for (int e = 0; e < 8; ++e)
-              f[e] = kx + e < a.cols ? s8_rnd<T>(s8_rnd<T>(f[e] / (1.0f + __expf(-f[e]))) * up[e]) : 0.0f;
+              f[t][e] = kx + e < a.cols ? s8_rnd<T>(s8_rnd<T>(f[t][e] / (1.0f + __expf(-f[t][e]))) * up[e]) : 0.0f;
           }
-          s8_stage_block(f, xs, ncs, fsc, nrx, kb, br);
         }
-        va[0] = va[1];
-        va[1] = va[2];
-        va[2] = va[3];
+        if (nv > 0) s8_stage_blocks<2>(f, xs, ncs, fsc, nrx, kbs, brs, nv);
+        va[0] = va[2];
+        va[1] = va[3];
         if (PRE == 2) {
-          vb[0] = vb[1];
-          vb[1] = vb[2];
-          vb[2] = vb[3];
+          vb[0] = vb[2];
+          vb[1] = vb[3];
         }
       }
     }
