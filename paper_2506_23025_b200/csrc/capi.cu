@@ -95,7 +95,7 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
   if (use_umma)
     return gemm_umma(fmt, act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, uniform, workspace,
                      ws_bytes, pdl, st, (flags >> 24) & 0xF);
-  if (batch <= 2 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols))
+  if (batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols))
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, pdl, st, 0, nullptr, nullptr,
                    nullptr, 0.0f);
   const size_t esz = 2;
@@ -118,7 +118,7 @@ int tr_linear_pre(int fmt, const void* w, const void* x, void* y, int64_t batch,
   TR_REQUIRE(batch >= 1 && batch <= 8 && rows >= 1 && cols >= 1, "tr_linear_pre: 1 <= batch <= 8");
   TR_REQUIRE(ldx >= (pre_op == TR_PRE_SILU_MUL ? 2 * cols : cols) && ldy >= rows, "tr_linear_pre: leading dimensions");
   TR_REQUIRE(((uintptr_t)w & 15) == 0, "tr_linear_pre: weight buffer must be 16-byte aligned");
-  if (batch <= 2 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols))
+  if (batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols))
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, (flags >> 8) & 0xFFFF,
                    flags & TR_LINEAR_PDL, (cudaStream_t)stream, pre_op, delta, gamma, x_out, eps);
   return gemv_tq2(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, (flags >> 8) & 0xFFFF,

@@ -48,10 +48,10 @@ constexpr int kS8SU = 2;              // units per ring slot (one bulk copy)
 constexpr int kS8NSMax = 4;
 constexpr int kS8ItemBytes = 1024;    // staged x per (block, batch row): 4 slices x 4 chunks x 16 words
 
-template <int NW> struct S8Cfg {
+template <int NW, int NG = 1> struct S8Cfg {   // NG MMA groups of 2 batch rows
   static constexpr int kSlotBytes = kS8SU * kUnitBytes;
   static constexpr size_t kRedOff = 1024;                         // [mbarriers | slot tags]
-  static constexpr size_t kRedBytes = (size_t)2 * NW * 64 * 4;    // 2 parked tiles per warp x 64 floats
+  static constexpr size_t kRedBytes = (size_t)2 * NW * 64 * NG * 4;   // 2 parked tiles per warp x 64 NG floats
   static constexpr size_t kCsOff = kRedOff + kRedBytes;           // -Cs: nb x nrx x 4 int32
   __host__ __device__ static size_t f_off(int nb, int nrx) { return kCsOff + (size_t)nb * nrx * 16; }
   __host__ __device__ static size_t xs_off(int nb, int nrx) {
@@ -211,12 +211,14 @@ __device__ __forceinline__ void imma_c(int (&d)[4], const uint32_t (&a)[4], uint
 }
 __device__ __forceinline__ uint32_t u4c(const uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 
-template <typename T, int NW, int PRE>
+template <typename T, int NW, int PRE, int NG>
 __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Args a) {
-  using Cfg = S8Cfg<NW>;
+  using Cfg = S8Cfg<NW, NG>;
   constexpr int kSlotBytes = Cfg::kSlotBytes;
   extern __shared__ __align__(128) uint8_t smem[];
-  const int NS = a.ns, nrx = a.batch, nb = a.nb;
+  // batch rows nbr; staged layout rows nrx (1, 2, or 4 for NG = 2: batch 3-4), log2 lr
+  const int NS = a.ns, nbr = a.batch, nb = a.nb;
+  const int nrx = NG == 2 ? 4 : nbr, lr = NG == 2 ? 2 : nbr - 1;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                 // NW * NS <= 64
   int* slot_tile = reinterpret_cast<int*>(smem + 512);                 // 2 * NW
   float* red = reinterpret_cast<float*>(smem + Cfg::kRedOff);
@@ -292,12 +294,14 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   if (PRE == 1) {   // x = rmsnorm(x + delta) * gamma; CTA 0 stores x + delta (the residual)
     float* ss_buf = red;   // nb * nrx partial sums of squares, then nrx inverse RMS
     for (int item = warp; item < nb * nrx; item += NW) {
-      const int kb = item >> (nrx - 1), br = item & (nrx - 1);   // nrx is 1 or 2
+      const int kb = item >> lr, br = item & (nrx - 1);
       const int64_t kx = (int64_t)kb * kBlock + lane * 8;
       float f[8];
-      const uint4 xv = s8_load8(xg + br * a.ldx, kx, a.cols, a.x_vec);
+      const bool live = br < nbr;   // (layout rows past the batch stage zeros)
+      const uint4 xv = live ? s8_load8(xg + br * a.ldx, kx, a.cols, a.x_vec) : make_uint4(0, 0, 0, 0);
       uint4 dv = make_uint4(0, 0, 0, 0);
-      if (a.pre_delta) dv = s8_load8(reinterpret_cast<const T*>(a.pre_delta) + br * a.ldx, kx, a.cols, a.x_vec);
+      if (a.pre_delta && live)
+        dv = s8_load8(reinterpret_cast<const T*>(a.pre_delta) + br * a.ldx, kx, a.cols, a.x_vec);
       issue_rest();
       s8_f8<T>(xv, f);
       if (a.pre_delta) {
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
       }
       const uint4 hv = s8_pack8<T>(f);
       *reinterpret_cast<uint4*>(xs + (size_t)item * kS8ItemBytes + lane * 16) = hv;   // parked in its own item
-      if (blockIdx.x == 0 && a.pre_out && kx < a.cols) {
+      if (blockIdx.x == 0 && a.pre_out && kx < a.cols && live) {
         T* o = reinterpret_cast<T*>(a.pre_out) + br * a.ldx + kx;
         if (kx + 8 <= a.cols && a.x_vec) {
           *reinterpret_cast<uint4*>(o) = hv;
@@ -335,7 +339,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
     __syncthreads();
     const T* gam = reinterpret_cast<const T*>(a.pre_gamma);
     for (int item = warp; item < nb * nrx; item += NW) {
-      const int kb = item >> (nrx - 1), br = item & (nrx - 1);   // nrx is 1 or 2
+      const int kb = item >> lr, br = item & (nrx - 1);
       const int64_t kx = (int64_t)kb * kBlock + lane * 8;
       float f[8], gm[8];
       s8_f8<T>(*reinterpret_cast<const uint4*>(xs + (size_t)item * kS8ItemBytes + lane * 16), f);
@@ -354,10 +358,11 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
       for (int i = 0; i < 4; ++i) {
         const int item = i0 + i * NW;
         if (item < n_items) {
-          const int kb = item >> (nrx - 1), br = item & (nrx - 1);   // nrx is 1 or 2
+          const int kb = item >> lr, br = item & (nrx - 1);
           const int64_t kx = (int64_t)kb * kBlock + lane * 8;
-          va[i] = s8_load8(xg + br * a.ldx, kx, a.cols, a.x_vec);
-          if (PRE == 2) vb[i] = s8_load8(xg + br * a.ldx + a.cols, kx, a.cols, a.x_vec);
+          const bool live = br < nbr;   // (layout rows past the batch stage zeros)
+          va[i] = live ? s8_load8(xg + br * a.ldx, kx, a.cols, a.x_vec) : make_uint4(0, 0, 0, 0);
+          if (PRE == 2) vb[i] = live ? s8_load8(xg + br * a.ldx + a.cols, kx, a.cols, a.x_vec) : make_uint4(0, 0, 0, 0);
         }
       }
       issue_rest();
@@ -370,7 +375,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
         for (int t = 0; t < 2; ++t) {
           const int item = i0 + (i + t) * NW;
           const int it = item < n_items ? item : i0;
-          kbs[t] = it >> (nrx - 1);
+          kbs[t] = it >> lr;
           brs[t] = it & (nrx - 1);
           nv += item < n_items;
           const int64_t kx = (int64_t)kbs[t] * kBlock + lane * 8;
@@ -401,86 +406,140 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   stamp(2);
 
   // ---- main loop: units [wu0, wu1), tile by tile
+  // MMA group G2 covers batch rows 2 G2, 2 G2 + 1 (slice-columns 8 G2 .. 8 G2 + 7)
   T* y = reinterpret_cast<T*>(a.y);
-  const int nBc = g & (4 * nrx - 1);          // B column of this lane: slice-column g
-  const int bB = nBc >> 2, sB = nBc & 3;
-  const int swB = ((c >> 1) << 1) | (sB & 1);
-  // B fragment base in shared space: the group swizzle (q ^ swB) becomes an XOR on bits 4-5
-  const uint32_t xsB32 = smem_u32(xs + (size_t)bB * kS8ItemBytes + sB * 256 + c * 64) ^ (uint32_t)(swB << 4);
-  const int kb_shift = 9 + nrx;                // log2(nrx * kS8ItemBytes)
-  const int bD = min(c >> 1, nrx - 1);         // D columns of this lane: slices 2(c&1), +1 of row c>>1
-  const int32_t* ncsD = ncs + bD * 4 + 2 * (c & 1);
-  const float* fscD = fsc + bD;
+  uint32_t xsB32[NG];
+  const int32_t* ncsD[NG];
+  const float* fscD[NG];
+#pragma unroll
+  for (int G2 = 0; G2 < NG; ++G2) {
+    const int nBc = NG == 1 ? (g & (4 * nrx - 1)) : 8 * G2 + g;   // B column of this lane: slice-column
+    const int bB = nBc >> 2, sB = nBc & 3;
+    const int swB = ((c >> 1) << 1) | (sB & 1);
+    // B fragment base in shared space: the group swizzle (q ^ swB) becomes an XOR on bits 4-5
+    xsB32[G2] = smem_u32(xs + (size_t)bB * kS8ItemBytes + sB * 256 + c * 64) ^ (uint32_t)(swB << 4);
+    const int bD = NG == 1 ? min(c >> 1, nrx - 1) : 2 * G2 + (c >> 1);   // D: slices 2(c&1), +1 of this row
+    ncsD[G2] = ncs + bD * 4 + 2 * (c & 1);
+    fscD[G2] = fsc + bD;
+  }
+  const int kb_shift = 10 + lr;                // log2(nrx * kS8ItemBytes)
   const float lane_w = (c & 1) ? 65536.0f : 1.0f;
 
-  auto store_tile = [&](int tile, float v0, float v1) {
+  auto store_tile = [&](int tile, const float (&v)[NG][2]) {
     if (trace) return;
-    if ((c & 1) == 0 && (c >> 1) < nrx) {
-      const int r0 = tile * 16 + g, r1 = r0 + 8;
-      if (r0 < a.rows) y[(c >> 1) * a.ldy + r0] = Act<T>::from_float(v0);
-      if (r1 < a.rows) y[(c >> 1) * a.ldy + r1] = Act<T>::from_float(v1);
+#pragma unroll
+    for (int G2 = 0; G2 < NG; ++G2) {
+      const int row = 2 * G2 + (c >> 1);
+      if ((c & 1) == 0 && row < nbr) {
+        const int r0 = tile * 16 + g, r1 = r0 + 8;
+        if (r0 < a.rows) y[row * a.ldy + r0] = Act<T>::from_float(v[G2][0]);
+        if (r1 < a.rows) y[row * a.ldy + r1] = Act<T>::from_float(v[G2][1]);
+      }
     }
   };
   const int first_tile = wu0 < wu1 ? wu0 / nb : -1;
   int cur = first_tile;
-  float acc0 = 0.0f, acc1 = 0.0f;
+  float acc[NG][2];
+#pragma unroll
+  for (int G2 = 0; G2 < NG; ++G2) acc[G2][0] = acc[G2][1] = 0.0f;
   auto close_tile = [&](int tile) {   // combine the two slice pairs; store or park
-    float v0 = acc0 * lane_w, v1 = acc1 * lane_w;
-    v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
-    v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+    float v[NG][2];
+#pragma unroll
+    for (int G2 = 0; G2 < NG; ++G2)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        v[G2][e] = acc[G2][e] * lane_w;
+        v[G2][e] += __shfl_xor_sync(0xffffffffu, v[G2][e], 1);
+      }
     if (tile * nb >= wu0 && (tile + 1) * nb <= wu1) {
-      store_tile(tile, v0, v1);
+      store_tile(tile, v);
       return;
     }
     const int which = (tile == first_tile) ? 0 : 1;
-    float* dst = red + (2 * warp + which) * 64;
-    dst[lane] = v0;
-    dst[32 + lane] = v1;
+    float* dst = red + (2 * warp + which) * 64 * NG;
+#pragma unroll
+    for (int G2 = 0; G2 < NG; ++G2) {
+      dst[G2 * 64 + lane] = v[G2][0];
+      dst[G2 * 64 + 32 + lane] = v[G2][1];
+    }
     if (lane == 0) slot_tile[2 * warp + which] = tile;
   };
 
-  // The two units of a ring slot: their 16 IMMAs run as four independent accumulator
-  // chains (even / odd MMAs of each unit) so the tensor pipe sees 4-deep chains, not 8+8.
+  // The two units of a ring slot.  NG = 1: their 16 IMMAs run as four independent accumulator
+  // chains (even / odd MMAs of each unit); NG = 2: 32 IMMAs, two chains per unit (one per group).
   auto mma_pair = [&](const uint4 (&wl)[kS8SU], const uint4 (&wh)[kS8SU], const int (&kbq)[kS8SU],
-                      int (&D)[kS8SU][4]) {
-    uint4 xw[kS8SU][4];
-    int2 cs[kS8SU];
-#pragma unroll
-    for (int q = 0; q < kS8SU; ++q) {
-      const uint32_t xp = xsB32 + ((uint32_t)kbq[q] << kb_shift);
-#pragma unroll
-      for (int i4 = 0; i4 < 4; ++i4) xw[q][i4] = ld_shared_v4u(xp ^ (i4 << 4));
-      cs[q] = *reinterpret_cast<const int2*>(ncsD + (kbq[q] << (nrx + 1)));
-    }
-    int da[kS8SU][4], db[kS8SU][4];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int w = i >> 1, j0 = 2 * (i & 1);
-      const uint32_t m0 = 0x03030303u << (2 * j0), m1 = 0x03030303u << (2 * j0 + 2);
+                      int (&D)[kS8SU][NG][4]) {
+    if constexpr (NG == 1) {
+      uint4 xw[kS8SU][4];
+      int2 cs[kS8SU];
 #pragma unroll
       for (int q = 0; q < kS8SU; ++q) {
-        const uint32_t lw = u4c(wl[q], w), hw = u4c(wh[q], w);
-        const uint32_t A[4] = {lw & m0, hw & m0, lw & m1, hw & m1};
-        const uint32_t b0 = u4c(xw[q][w], j0), b1 = u4c(xw[q][w], j0 + 1);
-        if (i == 0)
-          imma_c(da[q], A, b0, b1, cs[q].x, cs[q].y, cs[q].x, cs[q].y);
-        else if (i == 1)
-          imma_c(db[q], A, b0, b1, 0, 0, 0, 0);
-        else
-          imma((i & 1) ? db[q] : da[q], A, b0, b1);
+        const uint32_t xp = xsB32[0] + ((uint32_t)kbq[q] << kb_shift);
+#pragma unroll
+        for (int i4 = 0; i4 < 4; ++i4) xw[q][i4] = ld_shared_v4u(xp ^ (i4 << 4));
+        cs[q] = *reinterpret_cast<const int2*>(ncsD[0] + (kbq[q] << (lr + 2)));
+      }
+      int da[kS8SU][4], db[kS8SU][4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int w = i >> 1, j0 = 2 * (i & 1);
+        const uint32_t m0 = 0x03030303u << (2 * j0), m1 = 0x03030303u << (2 * j0 + 2);
+#pragma unroll
+        for (int q = 0; q < kS8SU; ++q) {
+          const uint32_t lw = u4c(wl[q], w), hw = u4c(wh[q], w);
+          const uint32_t A[4] = {lw & m0, hw & m0, lw & m1, hw & m1};
+          const uint32_t b0 = u4c(xw[q][w], j0), b1 = u4c(xw[q][w], j0 + 1);
+          if (i == 0)
+            imma_c(da[q], A, b0, b1, cs[q].x, cs[q].y, cs[q].x, cs[q].y);
+          else if (i == 1)
+            imma_c(db[q], A, b0, b1, 0, 0, 0, 0);
+          else
+            imma((i & 1) ? db[q] : da[q], A, b0, b1);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kS8SU; ++q)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) D[q][0][e] = da[q][e] + db[q][e];
+    } else {
+#pragma unroll
+      for (int q = 0; q < kS8SU; ++q) {
+        uint4 xw[NG][4];
+        int2 cs[NG];
+#pragma unroll
+        for (int G2 = 0; G2 < NG; ++G2) {
+          const uint32_t xp = xsB32[G2] + ((uint32_t)kbq[q] << kb_shift);
+#pragma unroll
+          for (int i4 = 0; i4 < 4; ++i4) xw[G2][i4] = ld_shared_v4u(xp ^ (i4 << 4));
+          cs[G2] = *reinterpret_cast<const int2*>(ncsD[G2] + (kbq[q] << (lr + 2)));
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int w = i >> 1, j0 = 2 * (i & 1);
+          const uint32_t m0 = 0x03030303u << (2 * j0), m1 = 0x03030303u << (2 * j0 + 2);
+          const uint32_t lw = u4c(wl[q], w), hw = u4c(wh[q], w);
+          const uint32_t A[4] = {lw & m0, hw & m0, lw & m1, hw & m1};
+#pragma unroll
+          for (int G2 = 0; G2 < NG; ++G2) {
+            const uint32_t b0 = u4c(xw[G2][w], j0), b1 = u4c(xw[G2][w], j0 + 1);
+            if (i == 0)
+              imma_c(D[q][G2], A, b0, b1, cs[G2].x, cs[G2].y, cs[G2].x, cs[G2].y);
+            else
+              imma(D[q][G2], A, b0, b1);
+          }
+        }
       }
     }
-#pragma unroll
-    for (int q = 0; q < kS8SU; ++q)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) D[q][e] = da[q][e] + db[q][e];
   };
-  auto epilogue = [&](const int (&d)[4], uint32_t sv, int kbq) {   // block scale x grid, into the row sums
-    const float fb = fscD[kbq * nrx];
+  auto epilogue = [&](const int (&d)[NG][4], uint32_t sv, int kbq) {   // block scale x grid, into the row sums
     const float2 sc = __half22float2(*reinterpret_cast<const __half2*>(&sv));
-    const int v0 = d[0] + d[1] * 256, v1 = d[2] + d[3] * 256;
-    acc0 = fmaf((float)v0, sc.x * fb, acc0);
-    acc1 = fmaf((float)v1, sc.y * fb, acc1);
+#pragma unroll
+    for (int G2 = 0; G2 < NG; ++G2) {
+      const float fb = fscD[G2][kbq * nrx];
+      const int v0 = d[G2][0] + d[G2][1] * 256, v1 = d[G2][2] + d[G2][3] * 256;
+      acc[G2][0] = fmaf((float)v0, sc.x * fb, acc[G2][0]);
+      acc[G2][1] = fmaf((float)v1, sc.y * fb, acc[G2][1]);
+    }
   };
 
   int kb = wu0 < wu1 ? wu0 - first_tile * nb : 0;
@@ -490,9 +549,6 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   for (int u = wu0; u < wu1; ++k) {
     const int s = k & (NS - 1);
     const int n = min(kS8SU, wu1 - u);
-#ifdef S8_NOWAIT   // dev probe: math on the first ring fill only (wrong results)
-    if (k >= NS) goto skip_wait;
-#endif
     if (k > 0) {   // refill the slot read in the previous iteration (its loads have completed)
       __syncwarp();
       if (lane == 0) {
@@ -501,9 +557,6 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
       }
     }
     mbar_wait(&mybar[s], (k >> nslog) & 1);
-#ifdef S8_NOWAIT
-  skip_wait:
-#endif
     const uint8_t* slot = myring + s * kSlotBytes;
     uint4 wl[kS8SU], wh[kS8SU];
     uint32_t sv[kS8SU];
@@ -529,23 +582,20 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
         wh[q] = wh[0];
       }
     }
-#ifdef S8_NOMATH   // dev probe: stream the weights only (wrong results)
-    acc0 += __uint_as_float(wl[0].x ^ wh[1].y ^ sv[0]);
-#else
-    int D[kS8SU][4];
+    int D[kS8SU][NG][4];
     mma_pair(wl, wh, kbq, D);
 #pragma unroll
     for (int q = 0; q < kS8SU; ++q) {
       if (q < n) {
         if (wrap[q]) {   // next tile
           close_tile(cur);
-          acc0 = acc1 = 0.0f;
+#pragma unroll
+          for (int G2 = 0; G2 < NG; ++G2) acc[G2][0] = acc[G2][1] = 0.0f;
           ++cur;
         }
         epilogue(D[q], sv[q], kbq[q]);
       }
     }
-#endif
     u += n;
   }
   stamp(9);
@@ -559,13 +609,18 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
     if (tile < 0) continue;
     const unsigned match = __ballot_sync(0xffffffffu, my_tag == tile);
     if (match & ((1u << i) - 1u)) continue;   // a lower slot holds this tile: it reduces
-    float v0 = 0.0f, v1 = 0.0f;
+    float v[NG][2];
+#pragma unroll
+    for (int G2 = 0; G2 < NG; ++G2) v[G2][0] = v[G2][1] = 0.0f;
     for (unsigned mq = match; mq; mq &= mq - 1) {   // ascending slot order: deterministic
       const int q = __ffs(mq) - 1;
-      v0 += red[q * 64 + lane];
-      v1 += red[q * 64 + 32 + lane];
+#pragma unroll
+      for (int G2 = 0; G2 < NG; ++G2) {
+        v[G2][0] += red[q * 64 * NG + G2 * 64 + lane];
+        v[G2][1] += red[q * 64 * NG + G2 * 64 + 32 + lane];
+      }
     }
-    store_tile(tile, v0, v1);
+    store_tile(tile, v);
   }
   stamp(10);
   if (warp == 0) stamp(3);
@@ -587,32 +642,40 @@ constexpr int kS8SmallCtaUnits = S8_SMALL_UNITS;   // units per CTA at or below 
 
 static bool s8_small(int n_tiles, int nb, int grid) { return (int64_t)ceil_div(n_tiles, grid) * nb <= kS8SmallCtaUnits; }
 
-template <int NW>
+static int s8_layout_rows(int batch) { return batch <= 2 ? batch : 4; }   // staged rows (NG = 2 pads to 4)
+
+template <int NW, int NG>
 static size_t s8_smem_plan(int batch, int nb, int n_tiles, int grid, int* ns_out) {
   int ns = s8_ns<NW>(n_tiles, nb, grid);
-  size_t sm = S8Cfg<NW>::smem(nb, batch, ns);
+  const int nra = s8_layout_rows(batch);
+  size_t sm = S8Cfg<NW, NG>::smem(nb, nra, ns);
   while (sm > 227 * 1024 && ns > 1) {   // wide activations: a shallower weight ring
     ns >>= 1;
-    sm = S8Cfg<NW>::smem(nb, batch, ns);
+    sm = S8Cfg<NW, NG>::smem(nb, nra, ns);
   }
   if (ns_out) *ns_out = ns;
   return sm;
 }
 
-// true when the int8-slice GEMV takes this product (batch 1-2, activations fit with a ring of >= 2)
-bool gemv_s8_fits(int batch, int rows, int cols) {
-  if (batch < 1 || batch > 2) return false;
-  const int nb = (int)ceil_div(cols, kBlock), n_tiles = (int)ceil_div(rows, 16);
-  const int grid = sm_count() < n_tiles ? sm_count() : n_tiles;
+template <int NG>
+static bool s8_fits_ng(int batch, int nb, int n_tiles, int grid) {
   int ns = 0;
-  const size_t sm = s8_small(n_tiles, nb, grid) ? s8_smem_plan<8>(batch, nb, n_tiles, grid, &ns)
-                                                : s8_smem_plan<16>(batch, nb, n_tiles, grid, &ns);
+  const size_t sm = s8_small(n_tiles, nb, grid) ? s8_smem_plan<8, NG>(batch, nb, n_tiles, grid, &ns)
+                                                : s8_smem_plan<16, NG>(batch, nb, n_tiles, grid, &ns);
   return sm <= 227 * 1024 && (ns >= 2 || s8_ns<16>(n_tiles, nb, grid) < 2);
 }
 
-template <typename T, int NW, int PRE>
+// true when the int8-slice GEMV takes this product (batch 1-4, activations fit with a ring of >= 2)
+bool gemv_s8_fits(int batch, int rows, int cols) {
+  if (batch < 1 || batch > 4) return false;
+  const int nb = (int)ceil_div(cols, kBlock), n_tiles = (int)ceil_div(rows, 16);
+  const int grid = sm_count() < n_tiles ? sm_count() : n_tiles;
+  return batch <= 2 ? s8_fits_ng<1>(batch, nb, n_tiles, grid) : s8_fits_ng<2>(batch, nb, n_tiles, grid);
+}
+
+template <typename T, int NW, int PRE, int NG>
 static int launch_s8_k(S8Args& a, int grid, int pdl, cudaStream_t st) {
-  auto kern = k_gemv_s8<T, NW, PRE>;
+  auto kern = k_gemv_s8<T, NW, PRE, NG>;
   static int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -620,7 +683,7 @@ static int launch_s8_k(S8Args& a, int grid, int pdl, cudaStream_t st) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured_dev = dev;
   }
-  const size_t smem = s8_smem_plan<NW>(a.batch, a.nb, a.n_tiles, grid, &a.ns);
+  const size_t smem = s8_smem_plan<NW, NG>(a.batch, a.nb, a.n_tiles, grid, &a.ns);
   if (smem > 227 * 1024) {
     set_error("tr_linear(gemv-s8): %d blocks per row x batch %d need %zu B of shared memory", a.nb, a.batch, smem);
     return -1;
@@ -642,11 +705,15 @@ static int launch_s8_k(S8Args& a, int grid, int pdl, cudaStream_t st) {
   }
   return 0;
 }
+template <typename T, int NW, int NG>
+static int launch_s8_ng(S8Args& a, int grid, int pdl, cudaStream_t st) {   // one kernel per fused producer
+  if (a.pre == 1) return launch_s8_k<T, NW, 1, NG>(a, grid, pdl, st);
+  if (a.pre == 2) return launch_s8_k<T, NW, 2, NG>(a, grid, pdl, st);
+  return launch_s8_k<T, NW, 0, NG>(a, grid, pdl, st);
+}
 template <typename T, int NW>
-static int launch_s8(S8Args& a, int grid, int pdl, cudaStream_t st) {   // one kernel per fused producer
-  if (a.pre == 1) return launch_s8_k<T, NW, 1>(a, grid, pdl, st);
-  if (a.pre == 2) return launch_s8_k<T, NW, 2>(a, grid, pdl, st);
-  return launch_s8_k<T, NW, 0>(a, grid, pdl, st);
+static int launch_s8(S8Args& a, int grid, int pdl, cudaStream_t st) {
+  return a.batch <= 2 ? launch_s8_ng<T, NW, 1>(a, grid, pdl, st) : launch_s8_ng<T, NW, 2>(a, grid, pdl, st);
 }
 
 int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows, int cols,

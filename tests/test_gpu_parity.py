@@ -561,14 +561,14 @@ def _s8_inputs(rng, kind, batch, cols, dtype):
     elif kind == "huge":     # near the top of the format
         x = x * (6e4 if dtype == "float16" else 1e30)
     elif kind == "rows":     # batch rows of very different magnitude
-        x = x * np.array([1e-3, 1e3][:batch])[:, None]
+        x = x * np.array([1e-3, 1e3, 1.0, 1e-5][:batch])[:, None]
     return torch.from_numpy(x.astype(np.float32)).to(getattr(torch, dtype)).cuda()
 
 
 @pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
 @pytest.mark.parametrize("kind", ["uniform", "range", "zeros", "tiny", "huge", "rows"])
 @pytest.mark.parametrize("rows,cols", [(37, 1500), (300, 4096), (640, 11008)])
-@pytest.mark.parametrize("batch", [1, 2])
+@pytest.mark.parametrize("batch", [1, 2, 3, 4])
 @pytest.mark.parametrize("per_block", [False, True])
 def test_gemv_s8_vs_oracle(tp, dtype, kind, rows, cols, batch, per_block):
     rng = np.random.default_rng(rows + cols + batch + len(kind))
@@ -599,8 +599,10 @@ def test_gemv_s8_exact_integer_cases(tp):
     rows, cols = 256, 4096
     W = (rng.integers(0, 3, size=(rows, cols)) - 1).astype(np.float32)
     w = tp.pack_matrix(W, tp.DType.TQ2).to_device()
-    x = torch.from_numpy(rng.integers(-8, 9, size=(2, cols)).astype(np.float32)).half().cuda()
+    x = torch.from_numpy(rng.integers(-8, 9, size=(4, cols)).astype(np.float32)).half().cuda()
     y = tp.linear(x, w).float().cpu().numpy()
+    np.testing.assert_array_equal(tp.linear(x[:3], w).float().cpu().numpy(), y[:3])   # batch 3 and 4: same bits
+    np.testing.assert_array_equal(tp.linear(x[:2], w).float().cpu().numpy(), y[:2])
     ref = (x.float().cpu().numpy().astype(np.float64) @ W.T.astype(np.float64))
     np.testing.assert_array_equal(y, ref.astype(np.float16).astype(np.float32))
     for ctas in (1, 7, 148):   # exact sums: any partition gives the same bits
