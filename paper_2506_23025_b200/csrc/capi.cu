@@ -34,7 +34,7 @@ size_t gemv_workspace_bytes(int batch, int rows, int cols);
 bool gemv_s8_fits(int batch, int rows, int cols);
 int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows, int cols,
             int ctas, int pdl, cudaStream_t st, int pre, const void* pre_delta, const void* pre_gamma, void* pre_out,
-            float eps);
+            float eps, int cosched);
 int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
               int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg);
 size_t umma_workspace_bytes(int batch, int rows, int cols);
@@ -97,7 +97,7 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
                      ws_bytes, pdl, st, (flags >> 24) & 0xF);
   if (batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols))
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, pdl, st, 0, nullptr, nullptr,
-                   nullptr, 0.0f);
+                   nullptr, 0.0f, (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0);
   const size_t esz = 2;
   for (int64_t n0 = 0; n0 < batch; n0 += 32) {
     const int nb_ = (int)(batch - n0 < 32 ? batch - n0 : 32);
@@ -120,7 +120,8 @@ int tr_linear_pre(int fmt, const void* w, const void* x, void* y, int64_t batch,
   TR_REQUIRE(((uintptr_t)w & 15) == 0, "tr_linear_pre: weight buffer must be 16-byte aligned");
   if (batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols))
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, (flags >> 8) & 0xFFFF,
-                   flags & TR_LINEAR_PDL, (cudaStream_t)stream, pre_op, delta, gamma, x_out, eps);
+                   flags & TR_LINEAR_PDL, (cudaStream_t)stream, pre_op, delta, gamma, x_out, eps,
+                   (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0);
   return gemv_tq2(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, (flags >> 8) & 0xFFFF,
                   flags & TR_LINEAR_PDL, (cudaStream_t)stream, pre_op, delta, gamma, x_out, eps);
 }

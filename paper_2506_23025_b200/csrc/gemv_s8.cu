@@ -36,6 +36,7 @@ struct S8Args {
   int x_vec;
   int batch;   // 1 or 2
   int ns;      // ring slots per warp (power of two)
+  int cosched;   // co-scheduled with neighbouring GEMVs: half-SM CTAs (TR_LINEAR_COSCHEDULE)
   int dbg;     // development probe: 2 = per-CTA / per-warp %globaltimer stamps into y (no output)
   int pre;     // fused producer of x (K3's GemvArgs::pre): 1 add+RMSNorm, 2 SwiGLU
   const void* pre_delta;
@@ -640,16 +641,22 @@ static int s8_ns(int n_tiles, int nb, int grid) {
 #endif
 constexpr int kS8SmallCtaUnits = S8_SMALL_UNITS;   // units per CTA at or below which 8 warps x 2 CTAs/SM are used
 
-static bool s8_small(int n_tiles, int nb, int grid) { return (int64_t)ceil_div(n_tiles, grid) * nb <= kS8SmallCtaUnits; }
+// 8 warps x 2 CTAs per SM (the next PDL-chained layer co-resides and prefetches) win for short
+// per-CTA ranges, and up to 80 units while staging stays cheap (<= 16 blocks: <= 2 per warp);
+// measured on the BASELINE and decoder shapes (scripts/dev/gpu53.sh)
+static bool s8_small(int n_tiles, int nb, int grid) {
+  const int64_t units = (int64_t)ceil_div(n_tiles, grid) * nb;
+  return units <= kS8SmallCtaUnits || (units <= 80 && nb <= 16);
+}
 
 static int s8_layout_rows(int batch) { return batch <= 2 ? batch : 4; }   // staged rows (NG = 2 pads to 4)
 
 template <int NW, int NG>
-static size_t s8_smem_plan(int batch, int nb, int n_tiles, int grid, int* ns_out) {
+static size_t s8_smem_plan(int batch, int nb, int n_tiles, int grid, int* ns_out, size_t cap = 227 * 1024) {
   int ns = s8_ns<NW>(n_tiles, nb, grid);
   const int nra = s8_layout_rows(batch);
   size_t sm = S8Cfg<NW, NG>::smem(nb, nra, ns);
-  while (sm > 227 * 1024 && ns > 1) {   // wide activations: a shallower weight ring
+  while (sm > cap && ns > 1) {   // wide activations: a shallower weight ring
     ns >>= 1;
     sm = S8Cfg<NW, NG>::smem(nb, nra, ns);
   }
@@ -718,7 +725,7 @@ static int launch_s8(S8Args& a, int grid, int pdl, cudaStream_t st) {
 
 int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows, int cols,
             int ctas, int pdl, cudaStream_t st, int pre, const void* pre_delta, const void* pre_gamma, void* pre_out,
-            float eps) {
+            float eps, int cosched) {
   if (!gemv_s8_fits(batch, rows, cols)) {
     set_error("tr_linear(gemv-s8): batch %d x %d columns does not fit the int8-slice GEMV", batch, cols);
     return -1;
@@ -745,7 +752,8 @@ int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t
   int grid = ctas > 0 ? ctas : sm_count();
   if (grid > a.n_tiles) grid = a.n_tiles;
   const bool bf = act != kActF16;
-  if (s8_small(a.n_tiles, a.nb, grid))
+  a.cosched = cosched;   // 8-warp CTAs (two per SM when their shared memory allows)
+  if (a.cosched || s8_small(a.n_tiles, a.nb, grid))
     return bf ? launch_s8<__nv_bfloat16, 8>(a, grid, pdl, st) : launch_s8<__half, 8>(a, grid, pdl, st);
   return bf ? launch_s8<__nv_bfloat16, 16>(a, grid, pdl, st) : launch_s8<__half, 16>(a, grid, pdl, st);
 }

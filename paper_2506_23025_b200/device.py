@@ -127,7 +127,7 @@ _PATHS = {"auto": 0, "umma": _lib.LINEAR_FORCE_UMMA, "gemv": _lib.LINEAR_FORCE_G
 
 def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, pdl: bool = False,
            ctas: int = 0, ws: torch.Tensor | None = None, path: str = "auto", ksplit: int = 0,
-           _probe: int = 0) -> torch.Tensor:
+           cosched: bool = False, _probe: int = 0) -> torch.Tensor:
     """y[..., rows] = x[..., cols] @ W^T for fp16/bf16 x on the GPU (TriRun hot path).
 
     Accumulation is fp32: per 256-block partial sums are scaled by the block's
@@ -137,6 +137,8 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
     tensor-core GEMM, smaller ones the decode GEMV; ``path`` ("umma" / "gemv")
     forces one.  ``ctas`` forces the GEMV's CTA count and ``ksplit`` the GEMM's
     K split (0 = automatic); ``ws`` overrides the per-stream workspace.
+    ``cosched`` (TR_LINEAR_COSCHEDULE) marks a layer in a back-to-back GEMV chain: the
+    int8-slice GEMV then runs as half-SM CTAs so the next layer co-resides and prefetches.
     """
     if x.dtype not in _ACT:
         raise TypeError(f"activations must be float16 or bfloat16, got {x.dtype}")
@@ -153,6 +155,8 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
         out = torch.empty((*lead, w.rows), dtype=x.dtype, device=x.device)
     y2 = out.view(-1, w.rows)
     flags = (_lib.LINEAR_PDL if pdl else 0) | (_lib.LINEAR_UNIFORM_SCALE if w.uniform_scale else 0) | _PATHS[path]
+    if cosched:   # back-to-back GEMV chain: half-SM CTAs so consecutive layers co-reside
+        flags |= _lib.LINEAR_COSCHEDULE
     # one knob: the GEMV's CTA count or the tensor-core GEMM's K split, whichever path runs
     flags |= ((int(ksplit or ctas)) & 0xFFFF) << 8
     flags |= (int(_probe) & 0xF) << 24   # development probes (see csrc); 0 in production

@@ -81,7 +81,9 @@ class LinearStack:
             return
         cur = self.x
         for w, out in zip(self.weights, self.bufs):
-            linear(cur, w, out=out, pdl=self.pdl)
+            # back-to-back GEMVs: half-SM CTAs, so each layer's successor co-resides and
+            # prefetches its weights while it computes (TR_LINEAR_COSCHEDULE)
+            linear(cur, w, out=out, pdl=self.pdl, cosched=True)
             cur = out
 
     @property
