@@ -99,6 +99,8 @@ class TernaryDecoder:
         self.out_tokens = torch.zeros(S, dtype=torch.long, device=self.device)
         self.h0 = torch.zeros((1, d), device=self.device, dtype=dtype)   # embedding row of the next token
         self._positions = torch.arange(S, device=self.device)
+        # TR_LINEAR_COSCHEDULE per decode GEMV (qkv, o, gate_up, down): 8-warp CTAs (measured)
+        self.cosched = (False, False, False, False)
         self._prefill_graphs = {}
         self.graph = None
 
@@ -196,17 +198,18 @@ class TernaryDecoder:
         for i in range(cfg.n_layers):
             lw = self.lin[i]
             # residual stream ping-pongs: the GEMV reads hs[cur] and stores hs[cur] + delta to hs[1 - cur]
+            cs = self.cosched
             qkv = linear_pre(hs[cur], lw["qkv"], _lib.PRE_ADD_RMSNORM, delta, self.norm_attn[i], hs[1 - cur],
-                             cfg.eps, pdl=True)
+                             cfg.eps, pdl=True, cosched=cs[0])
             cur = 1 - cur
             att = torch.empty((1, d), device=self.device, dtype=self.dtype)
             _lib.call("tr_attn_decode", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(), self.sin.data_ptr(),
                       self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(), H, D, S, D ** -0.5, st)
-            o = linear(att, lw["o"], pdl=True)
+            o = linear(att, lw["o"], pdl=True, cosched=cs[1])
             gu = linear_pre(hs[cur], lw["gate_up"], _lib.PRE_ADD_RMSNORM, o, self.norm_mlp[i], hs[1 - cur],
-                            cfg.eps, pdl=True)
+                            cfg.eps, pdl=True, cosched=cs[2])
             cur = 1 - cur
-            delta = linear_pre(gu, lw["down"], _lib.PRE_SILU_MUL, pdl=True)
+            delta = linear_pre(gu, lw["down"], _lib.PRE_SILU_MUL, pdl=True, cosched=cs[3])
         xn = torch.empty((1, d), device=self.device, dtype=self.dtype)
         _lib.call("tr_add_rmsnorm", act, hs[cur].data_ptr(), delta.data_ptr(), self.norm_out.data_ptr(), xn.data_ptr(),
                   1, d, cfg.eps, st)

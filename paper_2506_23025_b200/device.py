@@ -170,7 +170,7 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
 
 def linear_pre(x: torch.Tensor, w: TernaryWeight, pre: int, delta: torch.Tensor | None = None,
                gamma: torch.Tensor | None = None, x_out: torch.Tensor | None = None, eps: float = 1e-5,
-               out: torch.Tensor | None = None, pdl: bool = False) -> torch.Tensor:
+               out: torch.Tensor | None = None, pdl: bool = False, cosched: bool = False) -> torch.Tensor:
     """``linear`` with the producer of its input fused into the GEMV's activation staging.
 
     pre = _lib.PRE_ADD_RMSNORM: y = rmsnorm(x + delta) * gamma @ W^T, and x + delta is
@@ -183,7 +183,8 @@ def linear_pre(x: torch.Tensor, w: TernaryWeight, pre: int, delta: torch.Tensor 
         out = torch.empty((batch, w.rows), dtype=x.dtype, device=x.device)
     ptr = lambda t: 0 if t is None else t.data_ptr()
     _lib.call("tr_linear_pre", int(w.fmt), w.data.data_ptr(), x2.data_ptr(), out.data_ptr(), batch, w.rows, w.cols,
-              _ACT[x.dtype], x2.stride(0), out.stride(0), _lib.LINEAR_PDL if pdl else 0, int(pre), ptr(delta),
+              _ACT[x.dtype], x2.stride(0), out.stride(0),
+              (_lib.LINEAR_PDL if pdl else 0) | (_lib.LINEAR_COSCHEDULE if cosched else 0), int(pre), ptr(delta),
               ptr(gamma), ptr(x_out), float(eps), _lib.stream_handle())
     return out
 

@@ -607,3 +607,17 @@ def test_gemv_s8_exact_integer_cases(tp):
     np.testing.assert_array_equal(y, ref.astype(np.float16).astype(np.float32))
     for ctas in (1, 7, 148):   # exact sums: any partition gives the same bits
         np.testing.assert_array_equal(tp.linear(x, w, ctas=ctas).float().cpu().numpy(), y)
+
+
+@pytest.mark.parametrize("rows,cols", [(4096, 4096), (4096, 11008), (640, 1500)])
+@pytest.mark.parametrize("batch", [1, 3])
+def test_linear_cosched_variant(tp, rows, cols, batch):
+    # TR_LINEAR_COSCHEDULE (8-warp CTAs for back-to-back GEMV chains): same product, other warp split
+    rng = np.random.default_rng(rows + cols + batch)
+    payload, scales = _rand_packed(rng, rows, cols, per_block=True)
+    w = tp.PackedMatrix(rows=rows, cols=cols, fmt=tp.DType.TQ2, payload=payload, scales=scales).to_device()
+    x = torch.from_numpy(rng.uniform(-1, 1, size=(batch, cols)).astype(np.float32)).half().cuda()
+    ref = _oracle_ref(payload, scales, cols, 2, x.float().cpu().numpy())
+    y = tp.linear(x, w, cosched=True)
+    assert rel_err(y.float().cpu().numpy(), ref) <= 2e-3
+    assert torch.equal(y, tp.linear(x, w, cosched=True))   # deterministic
