@@ -14,13 +14,19 @@ from __future__ import annotations
 import numpy as np
 import torch
 
+
+def _writable(a):
+    """C-contiguous and writable (torch.from_numpy warns on read-only views, e.g. np.frombuffer)."""
+    a = np.ascontiguousarray(a)
+    return a if a.flags.writeable else a.copy()
+
 from . import _lib
 
 NAME = "cuda"
 
 
 def _dev(a: np.ndarray) -> torch.Tensor:
-    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    return torch.from_numpy(_writable(a)).cuda()
 
 
 def _run(name: str, *args) -> None:

@@ -12,6 +12,12 @@ from __future__ import annotations
 import numpy as np
 import torch
 
+
+def _writable(a):
+    """C-contiguous and writable (torch.from_numpy warns on read-only views, e.g. np.frombuffer)."""
+    a = np.ascontiguousarray(a)
+    return a if a.flags.writeable else a.copy()
+
 from . import _lib
 from .blocks import BLOCK_ELEMENTS, DType
 
@@ -73,8 +79,8 @@ class TernaryWeight:
     @classmethod
     def from_packed(cls, pm) -> "TernaryWeight":
         """From a host PackedMatrix (the offline-packed checkpoint form)."""
-        payload = torch.from_numpy(np.ascontiguousarray(pm.payload)).cuda()
-        scales = torch.from_numpy(np.ascontiguousarray(pm.scales).view(np.uint16).view(np.float16)).cuda()
+        payload = torch.from_numpy(_writable(pm.payload)).cuda()
+        scales = torch.from_numpy(_writable(pm.scales).view(np.uint16).view(np.float16)).cuda()
         return cls.from_device_packed(payload, scales, pm.rows, pm.cols, pm.fmt)
 
     @classmethod

@@ -621,3 +621,22 @@ def test_linear_cosched_variant(tp, rows, cols, batch):
     y = tp.linear(x, w, cosched=True)
     assert rel_err(y.float().cpu().numpy(), ref) <= 2e-3
     assert torch.equal(y, tp.linear(x, w, cosched=True))   # deterministic
+
+
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
+@pytest.mark.parametrize("rows,cols", [(33, 1001), (300, 777), (128, 4100)])
+@pytest.mark.parametrize("batch", [1, 2, 3, 4, 8])
+def test_linear_ragged_and_strided_activations(tp, dtype, rows, cols, batch):
+    # odd column counts (unaligned rows: the scalar activation path) and a strided x view
+    tdt = getattr(torch, dtype)
+    rng = np.random.default_rng(rows * 3 + cols + batch)
+    payload, scales = _rand_packed(rng, rows, cols, per_block=True)
+    w = tp.PackedMatrix(rows=rows, cols=cols, fmt=tp.DType.TQ2, payload=payload, scales=scales).to_device()
+    big = torch.from_numpy(rng.uniform(-1, 1, size=(batch, cols + 24)).astype(np.float32)).to(tdt).cuda()
+    x = big[:, 5:5 + cols]   # ldx = cols + 24, misaligned start
+    ref = _oracle_ref(payload, scales, cols, 2, x.float().cpu().numpy())
+    tol = 2e-3 if dtype == "float16" else 6e-3
+    y = tp.linear(x, w)
+    assert rel_err(y.float().cpu().numpy(), ref) <= tol
+    y16 = tp.linear(x, w, path="gemv_f16") if batch <= 8 else y
+    assert rel_err(y16.float().cpu().numpy(), ref) <= tol
