@@ -14,13 +14,13 @@ from __future__ import annotations
 import numpy as np
 import torch
 
+from . import _lib
+
 
 def _writable(a):
     """C-contiguous and writable (torch.from_numpy warns on read-only views, e.g. np.frombuffer)."""
     a = np.ascontiguousarray(a)
     return a if a.flags.writeable else a.copy()
-
-from . import _lib
 
 NAME = "cuda"
 

@@ -12,20 +12,19 @@ from __future__ import annotations
 import numpy as np
 import torch
 
+from . import _lib
+from .blocks import BLOCK_ELEMENTS, DType
+
 
 def _writable(a):
     """C-contiguous and writable (torch.from_numpy warns on read-only views, e.g. np.frombuffer)."""
     a = np.ascontiguousarray(a)
     return a if a.flags.writeable else a.copy()
 
-from . import _lib
-from .blocks import BLOCK_ELEMENTS, DType
 
 _ACT = {torch.float16: _lib.ACT_F16, torch.bfloat16: _lib.ACT_BF16}
 
 _WORKSPACES: dict = {}
-
-
 _RETIRED_WORKSPACES: list = []
 
 
