@@ -22,6 +22,7 @@ def _writable(a):
     a = np.ascontiguousarray(a)
     return a if a.flags.writeable else a.copy()
 
+
 NAME = "cuda"
 
 
