@@ -314,7 +314,7 @@ __global__ void k_silu_mul(const T* __restrict__ gu, T* __restrict__ out, int F,
     unpack8<T>(*reinterpret_cast<const uint4*>(gu + t * 2 * F + f), g);
     unpack8<T>(*reinterpret_cast<const uint4*>(gu + t * 2 * F + F + f), u);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) o[e] = to_f(Act<T>::from_float(g[e] / (1.0f + __expf(-g[e])))) * u[e];
+    for (int e = 0; e < 8; ++e) o[e] = to_f(Act<T>::from_float(__fdividef(g[e], 1.0f + __expf(-g[e])))) * u[e];
     *reinterpret_cast<uint4*>(out + t * F + f) = pack8<T>(o);
   }
 }

@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
             s8_f8<T>(vb[t], up);
 #pragma unroll
             for (int e = 0; e < 8; ++e)
-              f[t][e] = kx + e < a.cols ? s8_rnd<T>(s8_rnd<T>(f[t][e] / (1.0f + __expf(-f[t][e]))) * up[e]) : 0.0f;
+              f[t][e] = kx + e < a.cols ? s8_rnd<T>(s8_rnd<T>(__fdividef(f[t][e], 1.0f + __expf(-f[t][e]))) * up[e]) : 0.0f;
           }
         }
         if (nv > 0) s8_stage_blocks<2>(f, xs, ncs, fsc, nrx, kbs, brs, nv);
