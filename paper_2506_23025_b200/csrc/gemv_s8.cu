@@ -293,7 +293,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   // ---- stage the activations as int8 slices (fused producer first when asked)
   const T* xg = reinterpret_cast<const T*>(a.x);
   if (PRE == 1) {   // x = rmsnorm(x + delta) * gamma; CTA 0 stores x + delta (the residual)
-    float* ss_buf = red;   // nb * nrx partial sums of squares, then nrx inverse RMS
+    float* ss_buf = red;   // nb * nrx partial sums of squares
+    const T* gam = reinterpret_cast<const T*>(a.pre_gamma);
+    uint4 gv0 = make_uint4(0, 0, 0, 0);   // gamma of this warp's first block, loaded with x and delta
     for (int item = warp; item < nb * nrx; item += NW) {
       const int kb = item >> lr, br = item & (nrx - 1);
       const int64_t kx = (int64_t)kb * kBlock + lane * 8;
@@ -303,6 +305,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
       uint4 dv = make_uint4(0, 0, 0, 0);
       if (a.pre_delta && live)
         dv = s8_load8(reinterpret_cast<const T*>(a.pre_delta) + br * a.ldx, kx, a.cols, a.x_vec);
+      if (item == warp) gv0 = s8_load8(gam, kx, a.cols, a.x_vec);
       issue_rest();
       s8_f8<T>(xv, f);
       if (a.pre_delta) {
@@ -330,22 +333,18 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
       if (lane == 0) ss_buf[item] = ss;
     }
     __syncthreads();
-    for (int br = warp; br < nrx; br += NW) {   // fixed-order sums: same value in every CTA
-      float ss = 0.0f;
-      for (int kb = lane; kb < nb; kb += 32) ss += ss_buf[kb * nrx + br];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      if (lane == 0) ss_buf[nb * nrx + br] = rsqrtf(ss / a.cols + a.eps);
-    }
-    __syncthreads();
-    const T* gam = reinterpret_cast<const T*>(a.pre_gamma);
     for (int item = warp; item < nb * nrx; item += NW) {
       const int kb = item >> lr, br = item & (nrx - 1);
       const int64_t kx = (int64_t)kb * kBlock + lane * 8;
       float f[8], gm[8];
       s8_f8<T>(*reinterpret_cast<const uint4*>(xs + (size_t)item * kS8ItemBytes + lane * 16), f);
-      s8_f8<T>(s8_load8(gam, kx, a.cols, a.x_vec), gm);
-      const float iv = ss_buf[nb * nrx + br];
+      s8_f8<T>(item == warp ? gv0 : s8_load8(gam, kx, a.cols, a.x_vec), gm);
+      // inverse RMS of row br: the same fixed-order sum in every warp and CTA
+      float ss = 0.0f;
+      for (int q = lane; q < nb; q += 32) ss += ss_buf[q * nrx + br];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const float iv = rsqrtf(ss / a.cols + a.eps);
 #pragma unroll
       for (int e = 0; e < 8; ++e) f[e] = s8_rnd<T>(s8_rnd<T>(f[e] * iv) * gm[e]);
       __syncwarp();   // every lane holds its h before the item's bytes are overwritten
