@@ -16,6 +16,6 @@ def weight():   # the bench's synthetic weights: random trits, per-channel fp16 
 ws = [weight() for _ in range(copies)]
 x = torch.randn(batch, cols, device="cuda").half()
 for i in range(3 * copies):
-    tp.linear(x, ws[i % copies], ctas=ctas)
+    tp.linear(x, ws[i % copies], ctas=ctas, cosched=os.environ.get("COSCHED") == "1")
 torch.cuda.synchronize()
 print("ok")

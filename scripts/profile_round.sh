@@ -8,6 +8,6 @@ tail -c 600 gpurun_out/bench.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_gemv|k_gemm" -c 300 --csv \
   --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --sweep "" --cpu-seconds 0.1 > /dev/null 2>&1; echo "launches rc=$?"
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_gemv -s 6 -c 1 \
-  -o gpurun_out/prof_gemv python scripts/ncu_target.py 11008 4096 1 > /dev/null 2>&1; echo "gemv prof rc=$?"
+  -o gpurun_out/prof_gemv env COSCHED=1 python scripts/ncu_target.py 11008 4096 1 > /dev/null 2>&1; echo "gemv prof rc=$?"
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_gemm_umma -s 6 -c 1 \
   -o gpurun_out/prof_umma python scripts/ncu_target.py 11008 4096 128 > /dev/null 2>&1; echo "umma prof rc=$?"
