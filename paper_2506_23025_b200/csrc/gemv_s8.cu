@@ -246,11 +246,13 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   stamp(0);
 
   // the CTA owns whole tiles [t0, t1); warp w a contiguous slice of their units
-  const int t0 = (int)((int64_t)blockIdx.x * a.n_tiles / gridDim.x);
-  const int t1 = (int)((int64_t)(blockIdx.x + 1) * a.n_tiles / gridDim.x);
-  const int LL = (t1 - t0) * nb;
-  const int wu0 = t0 * nb + (int)((int64_t)warp * LL / NW);
-  const int wu1 = t0 * nb + (int)((int64_t)(warp + 1) * LL / NW);
+  // (32-bit unsigned arithmetic: tiles x grid < 2^32 -- a 64-bit division here sat in front of
+  // the first weight copies)
+  const unsigned t0 = blockIdx.x * (unsigned)a.n_tiles / gridDim.x;
+  const unsigned t1 = (blockIdx.x + 1) * (unsigned)a.n_tiles / gridDim.x;
+  const int LL = (int)(t1 - t0) * nb;
+  const int wu0 = (int)t0 * nb + (int)((unsigned)(warp * LL) / NW);
+  const int wu1 = (int)t0 * nb + (int)((unsigned)((warp + 1) * LL) / NW);
 
   // ---- weight stream (lane 0): bulk copies of kS8SU units into the warp's ring
   int pu = wu0;
