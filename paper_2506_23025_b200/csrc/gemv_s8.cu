@@ -570,6 +570,18 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
         sv[q] = *reinterpret_cast<const uint32_t*>(slot + q * kUnitBytes + kTileBlockBytes + g * 4);
       }
     }
+    if (n == kS8SU && kb + kS8SU <= nb) {   // common case: a full slot inside one tile
+      int kbq[kS8SU];
+#pragma unroll
+      for (int q = 0; q < kS8SU; ++q) kbq[q] = kb + q;
+      int D[kS8SU][NG][4];
+      mma_pair(wl, wh, kbq, D);
+#pragma unroll
+      for (int q = 0; q < kS8SU; ++q) epilogue(D[q], sv[q], kbq[q]);
+      kb += kS8SU;
+      u += n;
+      continue;
+    }
     // blocks of the slot's units (a partial last slot recomputes unit 0 and drops it)
     int kbq[kS8SU];
     bool wrap[kS8SU];
