@@ -45,7 +45,10 @@ struct S8Args {
   float eps;
 };
 
-constexpr int kS8SU = 2;              // units per ring slot (one bulk copy)
+constexpr int kS8SU = 2;
+#ifndef S8_TWO_CHAINS
+#define S8_TWO_CHAINS 0   // 1: each unit's 8 IMMAs as two accumulator chains (measured 1-2% slower)
+#endif              // units per ring slot (one bulk copy)
 constexpr int kS8NSMax = 4;
 constexpr int kS8ItemBytes = 1024;    // staged x per (block, batch row): 4 slices x 4 chunks x 16 words
 
@@ -467,8 +470,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
     if (lane == 0) slot_tile[2 * warp + which] = tile;
   };
 
-  // The two units of a ring slot.  NG = 1: their 16 IMMAs run as four independent accumulator
-  // chains (even / odd MMAs of each unit); NG = 2: 32 IMMAs, two chains per unit (one per group).
+  // The two units of a ring slot, interleaved: NG = 1: two accumulator chains of 8 IMMAs;
+  // NG = 2: 32 IMMAs, two chains per unit (one per group).
   auto mma_pair = [&](const uint4 (&wl)[kS8SU], const uint4 (&wh)[kS8SU], const int (&kbq)[kS8SU],
                       int (&D)[kS8SU][NG][4]) {
     if constexpr (NG == 1) {
@@ -493,16 +496,16 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
           const uint32_t b0 = u4c(xw[q][w], j0), b1 = u4c(xw[q][w], j0 + 1);
           if (i == 0)
             imma_c(da[q], A, b0, b1, cs[q].x, cs[q].y, cs[q].x, cs[q].y);
-          else if (i == 1)
+          else if (S8_TWO_CHAINS && i == 1)
             imma_c(db[q], A, b0, b1, 0, 0, 0, 0);
           else
-            imma((i & 1) ? db[q] : da[q], A, b0, b1);
+            imma((S8_TWO_CHAINS && (i & 1)) ? db[q] : da[q], A, b0, b1);
         }
       }
 #pragma unroll
       for (int q = 0; q < kS8SU; ++q)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) D[q][0][e] = da[q][e] + db[q][e];
+        for (int e = 0; e < 4; ++e) D[q][0][e] = S8_TWO_CHAINS ? da[q][e] + db[q][e] : da[q][e];
     } else {
 #pragma unroll
       for (int q = 0; q < kS8SU; ++q) {

@@ -1,0 +1,7 @@
+#!/bin/bash
+for v in base onechain; do
+  if [ $v = base ]; then unset TRITRUN_LIB; else export TRITRUN_LIB=$PWD/scripts/dev/var/$v/libtritrun.so; fi
+  echo "== $v" >> gpurun_out/ab62.txt
+  timeout 300 python scripts/dev/gemv_sweep.py 1 auto 4096x4096,11008x4096,4096x11008,8192x8192,28672x8192 2>&1 | grep -v relerr >> gpurun_out/ab62.txt
+  timeout 300 python bench.py --steps 10 --warmup 3 --sweep "" --cpu-seconds 0.1 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench', d['value'], d['roofline']['avg_launch_us'])" >> gpurun_out/ab62.txt
+done
