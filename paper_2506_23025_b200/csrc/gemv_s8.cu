@@ -276,7 +276,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   }
   // weights do not depend on the previous kernel: prefetch before griddepcontrol.wait
   // (dev knob dbg&4: after it; dbg&8: one slot before, the rest after)
-  const int pre_slots = (a.dbg & 4) ? 0 : (a.dbg & 8) ? 1 : NS;
+  // Long per-warp ranges: only the first slot goes out before the wait -- the rest follows the
+  // activation loads, which would otherwise queue behind a deep ring fill (measured: -4..-10% on
+  // 9216x3072, 18432x3072, 11008x4096, 4096x11008; short ranges keep the whole ring in flight)
+  const int pre_slots = (a.dbg & 4) ? 0 : ((a.dbg & 8) || LL >= 5 * NW) ? 1 : NS;
   const bool ring_after_staging = (a.dbg & 12) == 12;   // dev probe: the whole ring after x is staged
   if (lane == 0)
     for (int s = 0; s < pre_slots; ++s) issue(s);
@@ -769,7 +772,7 @@ int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t
   if (grid > a.n_tiles) grid = a.n_tiles;
   const bool bf = act != kActF16;
   a.cosched = cosched;   // 8-warp CTAs (two per SM when their shared memory allows)
-  if (a.cosched || s8_small(a.n_tiles, a.nb, grid))
+  if (a.cosched || (s8_small(a.n_tiles, a.nb, grid) && !(a.dbg & 1)))   // (dev knob dbg&1: 16 warps)
     return bf ? launch_s8<__nv_bfloat16, 8>(a, grid, pdl, st) : launch_s8<__half, 8>(a, grid, pdl, st);
   return bf ? launch_s8<__nv_bfloat16, 16>(a, grid, pdl, st) : launch_s8<__half, 16>(a, grid, pdl, st);
 }
