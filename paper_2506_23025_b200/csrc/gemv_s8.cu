@@ -386,14 +386,13 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
           kbs[t] = it >> lr;
           brs[t] = it & (nrx - 1);
           nv += item < n_items;
-          const int64_t kx = (int64_t)kbs[t] * kBlock + lane * 8;
           s8_f8<T>(va[t], f[t]);
           if (PRE == 2) {
             float up[8];
             s8_f8<T>(vb[t], up);
 #pragma unroll
             for (int e = 0; e < 8; ++e)
-              f[t][e] = kx + e < a.cols ? s8_rnd<T>(s8_rnd<T>(__fdividef(f[t][e], 1.0f + __expf(-f[t][e]))) * up[e]) : 0.0f;
+              f[t][e] = s8_rnd<T>(s8_rnd<T>(__fdividef(f[t][e], 1.0f + __expf(-f[t][e]))) * up[e]);   // (0 past cols)
           }
         }
         if (nv > 0) s8_stage_blocks<2>(f, xs, ncs, fsc, nrx, kbs, brs, nv);

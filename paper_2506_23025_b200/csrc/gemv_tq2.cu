@@ -219,7 +219,7 @@ __device__ void stage_pre(const GemvArgs& a, const Ly_t& Ly, uint8_t* xs, int rs
       f8_from<T>(load_x8(xg + n * Ly.ldx, kx, cols, Ly.x_vec), g);
       f8_from<T>(load_x8(xg + n * Ly.ldx + cols, kx, cols, Ly.x_vec), u);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) f[e] = kx + e < cols ? rnd<T>(__fdividef(g[e], 1.0f + __expf(-g[e]))) * u[e] : 0.0f;
+      for (int e = 0; e < 8; ++e) f[e] = rnd<T>(__fdividef(g[e], 1.0f + __expf(-g[e]))) * u[e];   // (0 past cols)
       *reinterpret_cast<uint4*>(at(n, kb)) = f8_to<T>(f);
     } else {            // residual add, stored rounded; sum of squares per (block, row)
       f8_from<T>(load_x8(xg + n * Ly.ldx, kx, cols, Ly.x_vec), f);
