@@ -303,18 +303,36 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   if (PRE == 1) {   // x = rmsnorm(x + delta) * gamma; CTA 0 stores x + delta (the residual)
     float* ss_buf = red;   // nb * nrx partial sums of squares
     const T* gam = reinterpret_cast<const T*>(a.pre_gamma);
-    uint4 gv0 = make_uint4(0, 0, 0, 0);   // gamma of this warp's first block, loaded with x and delta
-    for (int item = warp; item < nb * nrx; item += NW) {
+    // x, delta and gamma of this warp's first two blocks are loaded together up front (one
+    // memory latency instead of one per block and pass); gamma stays in registers for pass 2
+    uint4 pxv[2], pdv[2], pgv[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int item = warp + i * NW;
+      pxv[i] = pdv[i] = pgv[i] = make_uint4(0, 0, 0, 0);
+      if (item < nb * nrx) {
+        const int kb = item >> lr, br = item & (nrx - 1);
+        const int64_t kx = (int64_t)kb * kBlock + lane * 8;
+        if (br < nbr) {
+          pxv[i] = s8_load8(xg + br * a.ldx, kx, a.cols, a.x_vec);
+          if (a.pre_delta) pdv[i] = s8_load8(reinterpret_cast<const T*>(a.pre_delta) + br * a.ldx, kx, a.cols, a.x_vec);
+        }
+        pgv[i] = s8_load8(gam, kx, a.cols, a.x_vec);
+      }
+    }
+    issue_rest();
+    for (int item = warp, ii = 0; item < nb * nrx; item += NW, ++ii) {
       const int kb = item >> lr, br = item & (nrx - 1);
       const int64_t kx = (int64_t)kb * kBlock + lane * 8;
       float f[8];
       const bool live = br < nbr;   // (layout rows past the batch stage zeros)
-      const uint4 xv = live ? s8_load8(xg + br * a.ldx, kx, a.cols, a.x_vec) : make_uint4(0, 0, 0, 0);
-      uint4 dv = make_uint4(0, 0, 0, 0);
-      if (a.pre_delta && live)
-        dv = s8_load8(reinterpret_cast<const T*>(a.pre_delta) + br * a.ldx, kx, a.cols, a.x_vec);
-      if (item == warp) gv0 = s8_load8(gam, kx, a.cols, a.x_vec);
-      issue_rest();
+      uint4 xv = ii == 0 ? pxv[0] : pxv[1], dv = ii == 0 ? pdv[0] : pdv[1];
+      if (ii >= 2) {
+        xv = live ? s8_load8(xg + br * a.ldx, kx, a.cols, a.x_vec) : make_uint4(0, 0, 0, 0);
+        dv = make_uint4(0, 0, 0, 0);
+        if (a.pre_delta && live)
+          dv = s8_load8(reinterpret_cast<const T*>(a.pre_delta) + br * a.ldx, kx, a.cols, a.x_vec);
+      }
       s8_f8<T>(xv, f);
       if (a.pre_delta) {
         float d[8];
@@ -341,12 +359,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
       if (lane == 0) ss_buf[item] = ss;
     }
     __syncthreads();
-    for (int item = warp; item < nb * nrx; item += NW) {
+    for (int item = warp, ii = 0; item < nb * nrx; item += NW, ++ii) {
       const int kb = item >> lr, br = item & (nrx - 1);
       const int64_t kx = (int64_t)kb * kBlock + lane * 8;
       float f[8], gm[8];
       s8_f8<T>(*reinterpret_cast<const uint4*>(xs + (size_t)item * kS8ItemBytes + lane * 16), f);
-      s8_f8<T>(item == warp ? gv0 : s8_load8(gam, kx, a.cols, a.x_vec), gm);
+      s8_f8<T>(ii == 0 ? pgv[0] : ii == 1 ? pgv[1] : s8_load8(gam, kx, a.cols, a.x_vec), gm);
       // inverse RMS of row br: the same fixed-order sum in every warp and CTA
       float ss = 0.0f;
       for (int q = lane; q < nb; q += 32) ss += ss_buf[q * nrx + br];
