@@ -14,9 +14,23 @@ namespace tr {
 __host__ __device__ inline int e_word(int col) { return 2 * (col >> 5) + ((col >> 1) & 1); }
 __host__ __device__ inline int e_bit(int col) { return 16 * (col & 1) + 8 * ((col >> 4) & 1) + 2 * ((col >> 2) & 3); }
 
+// Source of a (row, block): payload bytes at payload + (row nb + b) pstride, binary16 scale at
+// sbase + (row nb + b) sstride.  PackedMatrix arrays: pstride 64|52, separate scales (sstride 2);
+// TPK1 records (container.py:73-82): pstride 66|54 with the scale right after the payload.
+struct RepackSrc {
+  const uint8_t* payload;
+  int64_t pstride;
+  const uint8_t* sbase;
+  int64_t sstride;
+  __device__ __forceinline__ const uint8_t* pay(int64_t rb) const { return payload + rb * pstride; }
+  __device__ __forceinline__ __half scale(int64_t rb) const {
+    const uint8_t* p = sbase + rb * sstride;   // 2-byte aligned in both layouts
+    return __ushort_as_half(*reinterpret_cast<const uint16_t*>(p));
+  }
+};
+
 // One thread per output 32-bit word (256 words of payload per unit).
-__global__ void k_repack_tq2(const uint8_t* __restrict__ payload, const __half* __restrict__ scales,
-                             int64_t rows, int64_t nb, int64_t n_tiles, uint8_t* __restrict__ dst) {
+__global__ void k_repack_tq2(const RepackSrc src, int64_t rows, int64_t nb, int64_t n_tiles, uint8_t* __restrict__ dst) {
   const int64_t total = nb * n_tiles * 256;
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total; w += (int64_t)gridDim.x * blockDim.x) {
     const int64_t tb = w >> 8;                 // unit index = t * nb + b
@@ -28,8 +42,16 @@ __global__ void k_repack_tq2(const uint8_t* __restrict__ payload, const __half* 
     uint32_t word = 0;
     if (row < rows) {
       // reference chunk: 16 bytes, column col at byte col/4 bits 2*(col%4) (_kernels.pyx:23-35)
-      const uint4 v4 = *reinterpret_cast<const uint4*>(payload + (row * nb + b) * kTq2Payload + 16 * c);
-      const uint32_t v[4] = {v4.x, v4.y, v4.z, v4.w};
+      const uint8_t* cp = src.pay(row * nb + b) + 16 * c;
+      uint32_t v[4];
+      if ((src.pstride & 15) == 0) {
+        const uint4 v4 = *reinterpret_cast<const uint4*>(cp);
+        v[0] = v4.x, v[1] = v4.y, v[2] = v4.z, v[3] = v4.w;
+      } else {   // TPK1 records: 66-byte stride, 2-byte aligned
+        const uint16_t* h = reinterpret_cast<const uint16_t*>(cp);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = (uint32_t)h[2 * k] | ((uint32_t)h[2 * k + 1] << 16);
+      }
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -46,8 +68,8 @@ __global__ void k_repack_tq2(const uint8_t* __restrict__ payload, const __half* 
     if ((w & 255) < 8) {   // the 8 half2 scale pairs of this unit
       const int gg = (int)(w & 255);
       const int64_t r0 = 16 * t + gg, r1 = r0 + 8;
-      const __half s0 = r0 < rows ? scales[r0 * nb + b] : __ushort_as_half(0);
-      const __half s1 = r1 < rows ? scales[r1 * nb + b] : __ushort_as_half(0);
+      const __half s0 = r0 < rows ? src.scale(r0 * nb + b) : __ushort_as_half(0);
+      const __half s1 = r1 < rows ? src.scale(r1 * nb + b) : __ushort_as_half(0);
       reinterpret_cast<__half2*>(unit + kTileBlockBytes)[gg] = __halves2half2(s0, s1);
     }
   }
@@ -97,15 +119,15 @@ __device__ __forceinline__ void dec5(uint32_t s, uint8_t* d, int stride) {   // 
 }
 
 // one thread per (padded row, block): reference codes -> digits -> pair-group codes
-__global__ void k_repack_tq1(const uint8_t* __restrict__ payload, const __half* __restrict__ scales, int64_t rows,
-                             int64_t nb, int64_t rows_pad, uint8_t* __restrict__ dst) {
+__global__ void k_repack_tq1(const RepackSrc srcs, int64_t rows, int64_t nb, int64_t rows_pad,
+                             uint8_t* __restrict__ dst) {
   const int64_t total = rows_pad * nb;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = q / nb, b = q % nb, t = row / 16;
     const int rt = (int)(row % 16);
     uint8_t d[260];
     if (row < rows) {
-      const uint8_t* src = payload + (row * nb + b) * kTq1Payload;
+      const uint8_t* src = srcs.pay(row * nb + b);
       for (int c = 0; c < kTq1Payload; ++c) dec5(src[c], d + 5 * c, 1);
     } else {
       for (int i = 0; i < 260; ++i) d[i] = 1;
@@ -123,7 +145,7 @@ __global__ void k_repack_tq1(const uint8_t* __restrict__ payload, const __half* 
       out[2 * g] = enc5(ev, 1);
       out[2 * g + 1] = enc5(od, 1);
     }
-    const __half s = row < rows ? scales[row * nb + b] : __ushort_as_half(0);
+    const __half s = row < rows ? srcs.scale(row * nb + b) : __ushort_as_half(0);
     reinterpret_cast<__half*>(unit + kQ1TileBlockBytes)[2 * (rt & 7) + (rt >> 3)] = s;
   }
 }
@@ -168,25 +190,36 @@ int64_t tr_layout_bytes(int fmt, int64_t rows, int64_t cols) {
   return -1;
 }
 
+static int repack_from(int fmt, const RepackSrc& src, int64_t rows, int64_t cols, void* dst, cudaStream_t st,
+                       const char* what) {
+  TR_REQUIRE(fmt == kFmtTq2 || fmt == kFmtTq1, "%s: fmt must be TQ2 (2) or TQ1 (3), got %d", what, fmt);
+  TR_REQUIRE(rows >= 1 && cols >= 1, "%s: matrix must be non-empty", what);
+  TR_REQUIRE(((uintptr_t)dst & 15) == 0 && ((uintptr_t)src.sbase & 1) == 0, "%s: misaligned buffers", what);
+  const int64_t nb = ceil_div(cols, kBlock);
+  if (fmt == kFmtTq1) {
+    const int64_t rp = rows_padded(rows);
+    const int grid = (int)(ceil_div(rp * nb, 128) > 148 * 32 ? 148 * 32 : ceil_div(rp * nb, 128));
+    k_repack_tq1<<<grid, 128, 0, st>>>(src, rows, nb, rp, (uint8_t*)dst);
+    return check_launch(what);
+  }
+  TR_REQUIRE(((uintptr_t)src.payload & 1) == 0 && ((src.pstride & 15) != 0 || ((uintptr_t)src.payload & 15) == 0),
+             "%s: misaligned payload", what);
+  const int64_t n_tiles = rows_padded(rows) / 16, total = nb * n_tiles * 256;
+  const int grid = (int)(ceil_div(total, 256) > 148 * 64 ? 148 * 64 : ceil_div(total, 256));
+  k_repack_tq2<<<grid, 256, 0, st>>>(src, rows, nb, n_tiles, (uint8_t*)dst);
+  return check_launch(what);
+}
+
 int tr_repack(int fmt, const uint8_t* payload, const uint16_t* scales_f16, int64_t rows, int64_t cols, void* dst,
               void* stream) {
-  TR_REQUIRE(fmt == kFmtTq2 || fmt == kFmtTq1, "tr_repack: fmt must be TQ2 (2) or TQ1 (3), got %d", fmt);
-  TR_REQUIRE(rows >= 1 && cols >= 1, "tr_repack: matrix must be non-empty");
-  if (fmt == kFmtTq1) {
-    TR_REQUIRE(((uintptr_t)dst & 15) == 0, "tr_repack: misaligned buffers");
-    const int64_t nb = ceil_div(cols, kBlock), rp = rows_padded(rows);
-    const int grid = (int)(ceil_div(rp * nb, 128) > 148 * 32 ? 148 * 32 : ceil_div(rp * nb, 128));
-    k_repack_tq1<<<grid, 128, 0, (cudaStream_t)stream>>>(payload, (const __half*)scales_f16, rows, nb, rp,
-                                                         (uint8_t*)dst);
-    return check_launch("tr_repack(tq1)");
-  }
-  TR_REQUIRE(((uintptr_t)payload & 3) == 0 && ((uintptr_t)dst & 15) == 0, "tr_repack: misaligned buffers");
-  int64_t nb = ceil_div(cols, kBlock), n_tiles = rows_padded(rows) / 16;
-  int64_t total = nb * n_tiles * 256;
-  int grid = (int)(ceil_div(total, 256) > 148 * 64 ? 148 * 64 : ceil_div(total, 256));
-  k_repack_tq2<<<grid, 256, 0, (cudaStream_t)stream>>>(payload, (const __half*)scales_f16, rows, nb, n_tiles,
-                                                       (uint8_t*)dst);
-  return check_launch("tr_repack");
+  const RepackSrc src = {payload, fmt == kFmtTq1 ? kTq1Payload : kTq2Payload, (const uint8_t*)scales_f16, 2};
+  return repack_from(fmt, src, rows, cols, dst, (cudaStream_t)stream, "tr_repack");
+}
+
+int tr_repack_records(int fmt, const uint8_t* records, int64_t rows, int64_t cols, void* dst, void* stream) {
+  const int64_t pb = fmt == kFmtTq1 ? kTq1Payload : kTq2Payload;
+  const RepackSrc src = {records, pb + 2, records + pb, pb + 2};
+  return repack_from(fmt, src, rows, cols, dst, (cudaStream_t)stream, "tr_repack_records");
 }
 
 int tr_unrepack(int fmt, const void* src, int64_t rows, int64_t cols, uint8_t* payload, uint16_t* scales_f16,

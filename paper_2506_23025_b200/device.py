@@ -155,6 +155,11 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
     x2 = x.reshape(-1, w.cols)
     if x2.stride(-1) != 1:
         x2 = x2.contiguous()
+    if w.fmt == DType.TQ1 and (x2.stride(0) % 8 or x2.data_ptr() % 16):
+        # the TQ1 path reads activations by TMA: rows 16-byte aligned (pad the row pitch)
+        xp = torch.zeros((x2.shape[0], -(-w.cols // 8) * 8), dtype=x2.dtype, device=x2.device)
+        xp[:, : w.cols] = x2
+        x2 = xp[:, : w.cols]
     batch = x2.shape[0]
     if out is None:
         out = torch.empty((*lead, w.rows), dtype=x.dtype, device=x.device)

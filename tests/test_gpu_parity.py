@@ -640,3 +640,28 @@ def test_linear_ragged_and_strided_activations(tp, dtype, rows, cols, batch):
     assert rel_err(y.float().cpu().numpy(), ref) <= tol
     y16 = tp.linear(x, w, path="gemv_f16") if batch <= 8 else y
     assert rel_err(y16.float().cpu().numpy(), ref) <= tol
+
+
+# ---------------------------------------------------------------- TPK1 container -> device
+
+def test_tpk1_load_to_device_matches_reference(tp):
+    import os
+    from paper_2506_23025_b200.container import load_to_device
+
+    gdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    g = np.load(os.path.join(gdir, "model_tpk1.npz"))
+    m = load_to_device(os.path.join(gdir, "model.tpk1"))
+    for key, name, fmt, (rows, cols) in [("qkv", "layers.0.attn.qkv", 2, (48, 300)),
+                                         ("down", "layers.0.mlp.down", 3, (40, 700)),
+                                         ("up", "layers.0.mlp.up", 2, (130, 512))]:
+        w = m[name]
+        assert (w.rows, w.cols, int(w.fmt)) == (rows, cols, fmt)
+        p, s = w.unpack()   # the device tiles invert back to the reference's own arrays, bit for bit
+        np.testing.assert_array_equal(p.cpu().numpy(), g[f"{key}_payload"])
+        np.testing.assert_array_equal(s.cpu().numpy().view(np.uint16), g[f"{key}_scales"])
+        x = torch.from_numpy(np.random.default_rng(rows).uniform(-1, 1, size=(3, cols)).astype(np.float32)).half().cuda()
+        ref = _oracle_ref(g[f"{key}_payload"], g[f"{key}_scales"].view(np.float16), cols, fmt, x.float().cpu().numpy())
+        assert rel_err(tp.linear(x, w).float().cpu().numpy(), ref) <= 2e-3
+    assert m["layers.0.attn.qkv"].uniform_scale and not m["layers.0.mlp.down"].uniform_scale
+    assert torch.equal(m["embed"].cpu(), torch.from_numpy(g["embed"]))
+    assert torch.equal(m["norm"].cpu(), torch.from_numpy(g["norm"]))
