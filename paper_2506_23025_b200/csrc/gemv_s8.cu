@@ -1,4 +1,4 @@
-// K3-S8: decode GEMV for batch 1-2 on the int8 tensor-core MMA, TQ2 weights.
+// K3-S8: decode GEMV for batch 1-4 on the int8 tensor-core MMA, TQ2 weights.
 //
 // Semantics are K3's (reference linear.py:137-166, _kernels.pyx:136-168, paper App. F):
 //   y[n, r] = sum_b s[r, b] * (sum_{k in block b} trit[r, k] * x[n, k]),
@@ -17,7 +17,7 @@
 //    every class -- one int32 accumulator, exact;
 //  * the 4 slices (x 2 batch rows) are the N = 8 columns of mma.sync.m16n8k32.u8.s8.s32, which
 //    has the HMMA.16816's issue cost at twice the K: 8 IMMA + 32 LOP3 per unit instead of
-//    16 HMMA + 64 LOP3 + 20 FFMA;
+//    16 HMMA + 64 LOP3 + 20 FFMA (batch 3-4: a second MMA group on the same A fragments);
 //  * the trit offset is folded into the accumulator: the first MMA of a block starts from
 //    -Cs, Cs[slice] = sum_k 4^j(k) b_slice(k), so D = sum_k 4^j (d - 1) b(k) exactly;
 //  * per block: two slices combine in int32, one I2F + FFMA per row applies the block scale
@@ -37,7 +37,9 @@ struct S8Args {
   int batch;   // 1 or 2
   int ns;      // ring slots per warp (power of two)
   int cosched;   // co-scheduled with neighbouring GEMVs: half-SM CTAs (TR_LINEAR_COSCHEDULE)
-  int dbg;     // development probe: 2 = per-CTA / per-warp %globaltimer stamps into y (no output)
+  // development probes (tr_linear knob bits 12-15; 0 in production): 1 = 16 warps, 2 = per-CTA /
+  // per-warp %globaltimer stamps into y (no output), 4 / 8 / 12 = ring issue order variants
+  int dbg;
   int pre;     // fused producer of x (K3's GemvArgs::pre): 1 add+RMSNorm, 2 SwiGLU
   const void* pre_delta;
   const void* pre_gamma;
