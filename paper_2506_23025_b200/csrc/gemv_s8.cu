@@ -48,6 +48,9 @@ struct S8Args {
 };
 
 constexpr int kS8SU = 2;
+#ifndef S8_PRE1_UNITS
+#define S8_PRE1_UNITS 5   // per-warp units from which only one ring slot goes out before the wait
+#endif
 #ifndef S8_TWO_CHAINS
 #define S8_TWO_CHAINS 0   // 1: each unit's 8 IMMAs as two accumulator chains (measured 1-2% slower)
 #endif              // units per ring slot (one bulk copy)
@@ -281,7 +284,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   // Long per-warp ranges: only the first slot goes out before the wait -- the rest follows the
   // activation loads, which would otherwise queue behind a deep ring fill (measured: -4..-10% on
   // 9216x3072, 18432x3072, 11008x4096, 4096x11008; short ranges keep the whole ring in flight)
-  const int pre_slots = (a.dbg & 4) ? 0 : ((a.dbg & 8) || LL >= 5 * NW) ? 1 : NS;
+  const int pre_slots = (a.dbg & 4) ? 0 : ((a.dbg & 8) || LL >= S8_PRE1_UNITS * NW) ? 1 : NS;
   const bool ring_after_staging = (a.dbg & 12) == 12;   // dev probe: the whole ring after x is staged
   if (lane == 0)
     for (int s = 0; s < pre_slots; ++s) issue(s);
