@@ -25,6 +25,7 @@ LINEAR_FORCE_UMMA = 4
 LINEAR_FORCE_GEMV = 8
 LINEAR_GEMV_F16 = 16
 LINEAR_COSCHEDULE = 32
+LINEAR_EPI_SWIGLU = 64
 PRE_ADD_RMSNORM = 1
 PRE_SILU_MUL = 2
 

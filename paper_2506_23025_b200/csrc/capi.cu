@@ -34,7 +34,7 @@ size_t gemv_workspace_bytes(int batch, int rows, int cols);
 bool gemv_s8_fits(int batch, int rows, int cols);
 int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows, int cols,
             int ctas, int pdl, cudaStream_t st, int pre, const void* pre_delta, const void* pre_gamma, void* pre_out,
-            float eps, int cosched);
+            float eps, int cosched, int epi);
 int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
               int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg);
 size_t umma_workspace_bytes(int batch, int rows, int cols);
@@ -71,7 +71,8 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
   TR_REQUIRE(rows >= 1 && cols >= 1 && batch >= 0, "tr_linear: bad shape batch=%lld rows=%lld cols=%lld",
              (long long)batch, (long long)rows, (long long)cols);
   TR_REQUIRE(rows < (1LL << 30) && cols < (1LL << 30), "tr_linear: shape too large");
-  TR_REQUIRE(ldx >= cols && ldy >= rows, "tr_linear: leading dimensions too small");
+  TR_REQUIRE(ldx >= cols && ldy >= ((flags & TR_LINEAR_EPI_SWIGLU) ? rows / 2 : rows),
+             "tr_linear: leading dimensions too small");
   TR_REQUIRE(((uintptr_t)w & 15) == 0, "tr_linear: weight buffer must be 16-byte aligned");
   if (batch == 0) return 0;
   const int pdl = flags & TR_LINEAR_PDL;
@@ -95,9 +96,12 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
   if (use_umma)
     return gemm_umma(fmt, act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, uniform, workspace,
                      ws_bytes, pdl, st, (flags >> 24) & 0xF);
+  if (flags & TR_LINEAR_EPI_SWIGLU)
+    TR_REQUIRE(batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols),
+               "tr_linear: the SwiGLU epilogue runs on the int8-slice GEMV only (batch <= 4)");
   if (batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols))
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, pdl, st, 0, nullptr, nullptr,
-                   nullptr, 0.0f, (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0);
+                   nullptr, 0.0f, (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, (flags & TR_LINEAR_EPI_SWIGLU) ? 1 : 0);
   const size_t esz = 2;
   for (int64_t n0 = 0; n0 < batch; n0 += 32) {
     const int nb_ = (int)(batch - n0 < 32 ? batch - n0 : 32);
@@ -116,12 +120,17 @@ int tr_linear_pre(int fmt, const void* w, const void* x, void* y, int64_t batch,
   TR_REQUIRE(pre_op == TR_PRE_ADD_RMSNORM || pre_op == TR_PRE_SILU_MUL, "tr_linear_pre: bad pre_op %d", pre_op);
   TR_REQUIRE(pre_op != TR_PRE_ADD_RMSNORM || gamma != nullptr, "tr_linear_pre: RMSNorm needs gamma");
   TR_REQUIRE(batch >= 1 && batch <= 8 && rows >= 1 && cols >= 1, "tr_linear_pre: 1 <= batch <= 8");
-  TR_REQUIRE(ldx >= (pre_op == TR_PRE_SILU_MUL ? 2 * cols : cols) && ldy >= rows, "tr_linear_pre: leading dimensions");
+  TR_REQUIRE(ldx >= (pre_op == TR_PRE_SILU_MUL ? 2 * cols : cols) &&
+                 ldy >= ((flags & TR_LINEAR_EPI_SWIGLU) ? rows / 2 : rows),
+             "tr_linear_pre: leading dimensions");
   TR_REQUIRE(((uintptr_t)w & 15) == 0, "tr_linear_pre: weight buffer must be 16-byte aligned");
+  if (flags & TR_LINEAR_EPI_SWIGLU)
+    TR_REQUIRE(batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols),
+               "tr_linear_pre: the SwiGLU epilogue runs on the int8-slice GEMV only (batch <= 4)");
   if (batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols))
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, (flags >> 8) & 0xFFFF,
                    flags & TR_LINEAR_PDL, (cudaStream_t)stream, pre_op, delta, gamma, x_out, eps,
-                   (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0);
+                   (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, (flags & TR_LINEAR_EPI_SWIGLU) ? 1 : 0);
   return gemv_tq2(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, (flags >> 8) & 0xFFFF,
                   flags & TR_LINEAR_PDL, (cudaStream_t)stream, pre_op, delta, gamma, x_out, eps);
 }

@@ -36,6 +36,8 @@ struct S8Args {
   int x_vec;
   int batch;   // 1 or 2
   int ns;      // ring slots per warp (power of two)
+  int epi;       // 1: SwiGLU epilogue -- W rows are 16-row tiles alternating gate / up; the CTA
+                 //    keeps its tile results in shared memory and stores silu(gate) * up (rows / 2)
   int cosched;   // co-scheduled with neighbouring GEMVs: half-SM CTAs (TR_LINEAR_COSCHEDULE)
   // development probes (tr_linear knob bits 12-15; 0 in production): 1 = 16 warps, 2 = per-CTA /
   // per-warp %globaltimer stamps into y (no output), 4 / 8 / 12 = ring issue order variants
@@ -256,8 +258,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   // the CTA owns whole tiles [t0, t1); warp w a contiguous slice of their units
   // (32-bit unsigned arithmetic: tiles x grid < 2^32 -- a 64-bit division here sat in front of
   // the first weight copies)
-  const unsigned t0 = blockIdx.x * (unsigned)a.n_tiles / gridDim.x;
-  const unsigned t1 = (blockIdx.x + 1) * (unsigned)a.n_tiles / gridDim.x;
+  // (SwiGLU epilogue: whole gate / up tile pairs per CTA)
+  const unsigned tq = a.epi ? 2u : 1u, tn = (unsigned)a.n_tiles / tq;
+  const unsigned t0 = tq * (blockIdx.x * tn / gridDim.x);
+  const unsigned t1 = tq * ((blockIdx.x + 1) * tn / gridDim.x);
   const int LL = (int)(t1 - t0) * nb;
   const int wu0 = (int)t0 * nb + (int)((unsigned)(warp * LL) / NW);
   const int wu1 = (int)t0 * nb + (int)((unsigned)((warp + 1) * LL) / NW);
@@ -455,8 +459,21 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   const int kb_shift = 10 + lr;                // log2(nrx * kS8ItemBytes)
   const float lane_w = (c & 1) ? 65536.0f : 1.0f;
 
+  float* tv = reinterpret_cast<float*>(smem + Cfg::smem(nb, nrx, NS));   // (epi) [tile - t0][16 rows][4]
   auto store_tile = [&](int tile, const float (&v)[NG][2]) {
     if (trace) return;
+    if (a.epi) {   // keep: the pair's other tile may come from another warp
+#pragma unroll
+      for (int G2 = 0; G2 < NG; ++G2) {
+        const int row = 2 * G2 + (c >> 1);
+        if ((c & 1) == 0 && row < nbr) {
+          float* tt = tv + (size_t)(tile - (int)t0) * 64;
+          tt[g * 4 + row] = v[G2][0];
+          tt[(g + 8) * 4 + row] = v[G2][1];
+        }
+      }
+      return;
+    }
 #pragma unroll
     for (int G2 = 0; G2 < NG; ++G2) {
       const int row = 2 * G2 + (c >> 1);
@@ -664,6 +681,18 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
     }
     store_tile(tile, v);
   }
+  if (a.epi) {   // silu(gate) * up with the roundings of the unfused gate|up store + tr_silu_mul
+    __syncthreads();
+    const int npairs = (int)(t1 - t0) / 2, rows_out = a.rows / 2;
+    for (int idx = threadIdx.x; idx < npairs * 16 * nbr; idx += NW * 32) {
+      const int p = idx / (16 * nbr), r = (idx / nbr) % 16, br = idx % nbr;
+      const float gt = s8_rnd<T>(tv[(size_t)(2 * p) * 64 + r * 4 + br]);
+      const float up = s8_rnd<T>(tv[(size_t)(2 * p + 1) * 64 + r * 4 + br]);
+      const int orow = ((int)t0 / 2 + p) * 16 + r;
+      if (orow < rows_out && !trace)
+        y[br * a.ldy + orow] = Act<T>::from_float(s8_rnd<T>(__fdividef(gt, 1.0f + __expf(-gt))) * up);
+    }
+  }
   stamp(10);
   if (warp == 0) stamp(3);
 }
@@ -721,6 +750,10 @@ bool gemv_s8_fits(int batch, int rows, int cols) {
   return batch <= 2 ? s8_fits_ng<1>(batch, nb, n_tiles, grid) : s8_fits_ng<2>(batch, nb, n_tiles, grid);
 }
 
+static size_t s8_tv_bytes(const S8Args& a, int grid) {   // SwiGLU epilogue: tile results of one CTA
+  return a.epi ? (size_t)2 * ceil_div(a.n_tiles / 2, grid) * 64 * sizeof(float) : 0;
+}
+
 template <typename T, int NW, int PRE, int NG>
 static int launch_s8_k(S8Args& a, int grid, int pdl, cudaStream_t st) {
   auto kern = k_gemv_s8<T, NW, PRE, NG>;
@@ -731,7 +764,8 @@ static int launch_s8_k(S8Args& a, int grid, int pdl, cudaStream_t st) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured_dev = dev;
   }
-  const size_t smem = s8_smem_plan<NW, NG>(a.batch, a.nb, a.n_tiles, grid, &a.ns);
+  const size_t smem = s8_smem_plan<NW, NG>(a.batch, a.nb, a.n_tiles, grid, &a.ns, 227 * 1024 - s8_tv_bytes(a, grid)) +
+                      s8_tv_bytes(a, grid);
   if (smem > 227 * 1024) {
     set_error("tr_linear(gemv-s8): %d blocks per row x batch %d need %zu B of shared memory", a.nb, a.batch, smem);
     return -1;
@@ -766,7 +800,7 @@ static int launch_s8(S8Args& a, int grid, int pdl, cudaStream_t st) {
 
 int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows, int cols,
             int ctas, int pdl, cudaStream_t st, int pre, const void* pre_delta, const void* pre_gamma, void* pre_out,
-            float eps, int cosched) {
+            float eps, int cosched, int epi) {
   if (!gemv_s8_fits(batch, rows, cols)) {
     set_error("tr_linear(gemv-s8): batch %d x %d columns does not fit the int8-slice GEMV", batch, cols);
     return -1;
@@ -790,8 +824,14 @@ int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t
   a.eps = eps;
   a.dbg = (ctas >> 12) & 0xF;
   ctas &= 0xFFF;
+  a.epi = epi;
+  if (epi && (rows % 32) != 0) {
+    set_error("tr_linear(swiglu epilogue): rows (%d) must be whole 16-row gate/up tile pairs", rows);
+    return -1;
+  }
   int grid = ctas > 0 ? ctas : sm_count();
-  if (grid > a.n_tiles) grid = a.n_tiles;
+  const int units_of_work = epi ? a.n_tiles / 2 : a.n_tiles;   // (tile pairs for the SwiGLU epilogue)
+  if (grid > units_of_work) grid = units_of_work;
   const bool bf = act != kActF16;
   a.cosched = cosched;   // 8-warp CTAs (two per SM when their shared memory allows)
   if (a.cosched || (s8_small(a.n_tiles, a.nb, grid) && !(a.dbg & 1)))   // (dev knob dbg&1: 16 warps)

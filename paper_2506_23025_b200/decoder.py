@@ -28,7 +28,8 @@ import torch
 import torch.nn.functional as F
 
 from . import _lib
-from .device import _ACT, TernaryWeight, linear, linear_pre
+from .blocks import DType
+from .device import _ACT, TernaryWeight, interleave_gate_up, linear, linear_pre
 
 
 @dataclass(frozen=True)
@@ -55,6 +56,13 @@ class DecoderConfig:
         d, f = self.d_model, self.d_ff
         per = lambda r, c: r * (-(-c // 256)) * 66
         return self.n_layers * (per(3 * d, d) + per(d, d) + per(2 * f, d) + per(d, f))
+
+
+def _interleaved(w: TernaryWeight, d_ff: int) -> TernaryWeight:
+    """The same packed gate|up weight with rows as alternating 16-row gate / up tiles."""
+    payload, scales = w.unpack()
+    idx = interleave_gate_up(torch.arange(2 * d_ff, device=payload.device).unsqueeze(1), d_ff).squeeze(1)
+    return TernaryWeight.from_device_packed(payload[idx].contiguous(), scales[idx].contiguous(), w.rows, w.cols, w.fmt)
 
 
 def _ternary(rows, cols, gen, device):
@@ -84,6 +92,12 @@ class TernaryDecoder:
             self.lin = [{k: w.dequantize(dtype) for k, w in lw.items()} for lw in weights["layers"]]
         else:
             self.lin = weights["layers"]
+        # decode: gate|up rows as alternating 16-row gate / up tiles, so the GEMV's epilogue
+        # emits silu(gate) * up and the down projection reads a plain activation (same trits
+        # and scales, rows permuted on the device)
+        self.gate_up_il = None
+        if not dense and fused and f % 16 == 0 and all(lw["gate_up"].fmt is DType.TQ2 for lw in weights["layers"]):
+            self.gate_up_il = [_interleaved(lw["gate_up"], f) for lw in weights["layers"]]
         self.norm_attn = [torch.ones(d, device=self.device, dtype=dtype) for _ in range(L)]
         self.norm_mlp = [torch.ones(d, device=self.device, dtype=dtype) for _ in range(L)]
         self.norm_out = torch.ones(d, device=self.device, dtype=dtype)
@@ -206,10 +220,16 @@ class TernaryDecoder:
             _lib.call("tr_attn_decode", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(), self.sin.data_ptr(),
                       self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(), H, D, S, D ** -0.5, st)
             o = linear(att, lw["o"], pdl=True, cosched=cs[1])
-            gu = linear_pre(hs[cur], lw["gate_up"], _lib.PRE_ADD_RMSNORM, o, self.norm_mlp[i], hs[1 - cur],
-                            cfg.eps, pdl=True, cosched=cs[2])
-            cur = 1 - cur
-            delta = linear_pre(gu, lw["down"], _lib.PRE_SILU_MUL, pdl=True, cosched=cs[3])
+            if self.gate_up_il is not None:   # SwiGLU in the gate|up GEMV's epilogue
+                act_ = linear_pre(hs[cur], self.gate_up_il[i], _lib.PRE_ADD_RMSNORM, o, self.norm_mlp[i],
+                                  hs[1 - cur], cfg.eps, pdl=True, cosched=cs[2], epi_swiglu=True)
+                cur = 1 - cur
+                delta = linear(act_, lw["down"], pdl=True, cosched=cs[3])
+            else:
+                gu = linear_pre(hs[cur], lw["gate_up"], _lib.PRE_ADD_RMSNORM, o, self.norm_mlp[i], hs[1 - cur],
+                                cfg.eps, pdl=True, cosched=cs[2])
+                cur = 1 - cur
+                delta = linear_pre(gu, lw["down"], _lib.PRE_SILU_MUL, pdl=True, cosched=cs[3])
         xn = torch.empty((1, d), device=self.device, dtype=self.dtype)
         _lib.call("tr_add_rmsnorm", act, hs[cur].data_ptr(), delta.data_ptr(), self.norm_out.data_ptr(), xn.data_ptr(),
                   1, d, cfg.eps, st)

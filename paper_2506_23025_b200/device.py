@@ -132,7 +132,7 @@ _PATHS = {"auto": 0, "umma": _lib.LINEAR_FORCE_UMMA, "gemv": _lib.LINEAR_FORCE_G
 
 def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, pdl: bool = False,
            ctas: int = 0, ws: torch.Tensor | None = None, path: str = "auto", ksplit: int = 0,
-           cosched: bool = False, _probe: int = 0) -> torch.Tensor:
+           cosched: bool = False, epi_swiglu: bool = False, _probe: int = 0) -> torch.Tensor:
     """y[..., rows] = x[..., cols] @ W^T for fp16/bf16 x on the GPU (TriRun hot path).
 
     Accumulation is fp32: per 256-block partial sums are scaled by the block's
@@ -144,6 +144,8 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
     K split (0 = automatic); ``ws`` overrides the per-stream workspace.
     ``cosched`` (TR_LINEAR_COSCHEDULE) marks a layer in a back-to-back GEMV chain: the
     int8-slice GEMV then runs as half-SM CTAs so the next layer co-resides and prefetches.
+    ``epi_swiglu`` (TR_LINEAR_EPI_SWIGLU): W is a gate|up weight with 16-row tiles alternating
+    gate / up (``interleave_gate_up``); the result is silu(gate) * up, rows // 2 wide.
     """
     if x.dtype not in _ACT:
         raise TypeError(f"activations must be float16 or bfloat16, got {x.dtype}")
@@ -161,10 +163,13 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
         xp[:, : w.cols] = x2
         x2 = xp[:, : w.cols]
     batch = x2.shape[0]
+    rows_out = w.rows // 2 if epi_swiglu else w.rows
     if out is None:
-        out = torch.empty((*lead, w.rows), dtype=x.dtype, device=x.device)
-    y2 = out.view(-1, w.rows)
+        out = torch.empty((*lead, rows_out), dtype=x.dtype, device=x.device)
+    y2 = out.view(-1, rows_out)
     flags = (_lib.LINEAR_PDL if pdl else 0) | (_lib.LINEAR_UNIFORM_SCALE if w.uniform_scale else 0) | _PATHS[path]
+    if epi_swiglu:
+        flags |= _lib.LINEAR_EPI_SWIGLU
     if cosched:   # back-to-back GEMV chain: half-SM CTAs so consecutive layers co-reside
         flags |= _lib.LINEAR_COSCHEDULE
     # one knob: the GEMV's CTA count or the tensor-core GEMM's K split, whichever path runs
@@ -180,7 +185,8 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
 
 def linear_pre(x: torch.Tensor, w: TernaryWeight, pre: int, delta: torch.Tensor | None = None,
                gamma: torch.Tensor | None = None, x_out: torch.Tensor | None = None, eps: float = 1e-5,
-               out: torch.Tensor | None = None, pdl: bool = False, cosched: bool = False) -> torch.Tensor:
+               out: torch.Tensor | None = None, pdl: bool = False, cosched: bool = False,
+               epi_swiglu: bool = False) -> torch.Tensor:
     """``linear`` with the producer of its input fused into the GEMV's activation staging.
 
     pre = _lib.PRE_ADD_RMSNORM: y = rmsnorm(x + delta) * gamma @ W^T, and x + delta is
@@ -190,11 +196,12 @@ def linear_pre(x: torch.Tensor, w: TernaryWeight, pre: int, delta: torch.Tensor 
     x2 = x.reshape(-1, x.shape[-1])
     batch = x2.shape[0]
     if out is None:
-        out = torch.empty((batch, w.rows), dtype=x.dtype, device=x.device)
+        out = torch.empty((batch, w.rows // 2 if epi_swiglu else w.rows), dtype=x.dtype, device=x.device)
     ptr = lambda t: 0 if t is None else t.data_ptr()
     _lib.call("tr_linear_pre", int(w.fmt), w.data.data_ptr(), x2.data_ptr(), out.data_ptr(), batch, w.rows, w.cols,
               _ACT[x.dtype], x2.stride(0), out.stride(0),
-              (_lib.LINEAR_PDL if pdl else 0) | (_lib.LINEAR_COSCHEDULE if cosched else 0), int(pre), ptr(delta),
+              (_lib.LINEAR_PDL if pdl else 0) | (_lib.LINEAR_COSCHEDULE if cosched else 0)
+              | (_lib.LINEAR_EPI_SWIGLU if epi_swiglu else 0), int(pre), ptr(delta),
               ptr(gamma), ptr(x_out), float(eps), _lib.stream_handle())
     return out
 
@@ -217,3 +224,12 @@ class TernaryLinear(torch.nn.Module):
 
     def extra_repr(self) -> str:
         return f"in_features={self.in_features}, out_features={self.out_features}, fmt={self.weight_t.fmt.name}"
+
+
+def interleave_gate_up(W: torch.Tensor, d_ff: int) -> torch.Tensor:
+    """Rows of a [gate (d_ff) ; up (d_ff)] matrix as 16-row tiles alternating gate / up (the
+    layout TR_LINEAR_EPI_SWIGLU expects): tile 2p = gate rows 16p.., tile 2p+1 = up rows 16p..."""
+    if d_ff % 16:
+        raise ValueError(f"d_ff ({d_ff}) must be a multiple of 16")
+    g, u = W[:d_ff].reshape(d_ff // 16, 16, -1), W[d_ff:2 * d_ff].reshape(d_ff // 16, 16, -1)
+    return torch.stack((g, u), dim=1).reshape(2 * d_ff, -1)

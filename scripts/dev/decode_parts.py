@@ -46,6 +46,10 @@ parts = {
     "gate_up (rmsnorm fused)": lambda: [linear_pre(h[0], m.lin[i]["gate_up"], _lib.PRE_ADD_RMSNORM, h[1], m.norm_mlp[i], out_d, cfg.eps, out=out_gu, pdl=True) for i in range(L)],
     "down (swiglu fused)": lambda: [linear_pre(gu, m.lin[i]["down"], _lib.PRE_SILU_MUL, out=out_d, pdl=True) for i in range(L)],
 }
+if m.gate_up_il is not None:
+    out_a = torch.empty(1, f, device=dev).half()
+    parts["gate_up (rmsnorm + swiglu epilogue)"] = lambda: [linear_pre(h[0], m.gate_up_il[i], _lib.PRE_ADD_RMSNORM, h[1], m.norm_mlp[i], out_d, cfg.eps, out=out_a, pdl=True, epi_swiglu=True) for i in range(L)]
+    parts["down (plain)"] = lambda: [linear(gu[:, :f], m.lin[i]["down"], out=out_d, pdl=True) for i in range(L)]
 res = {k: round(timeit(v) / L, 2) for k, v in parts.items()}
 m.reset(); m.prefill(torch.randint(0, cfg.vocab, (64,), device=dev)); m.capture()
 torch.cuda.synchronize()
@@ -54,5 +58,13 @@ e0.record()
 for _ in range(20): m.graph.replay()
 e1.record(); e1.synchronize()
 res["full step (ms)"] = round(e0.elapsed_time(e1) / 20, 4)
-res["sum of 30 layers (ms)"] = round(sum(v for k, v in res.items() if "ms" not in k) * L / 1e3, 4)
+if m.gate_up_il is not None:   # A/B: the same model with the SwiGLU staged in the down GEMV
+    m.gate_up_il = None
+    m.reset(); m.prefill(torch.randint(0, cfg.vocab, (64,), device=dev)); m.capture()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(20): m.graph.replay()
+    e1.record(); e1.synchronize()
+    res["full step, no epilogue (ms)"] = round(e0.elapsed_time(e1) / 20, 4)
+res["sum of 30 layers (ms)"] = round(sum(v for k, v in res.items() if "ms" not in k and "epilogue" not in k and "plain" not in k) * L / 1e3, 4)
 print(json.dumps(res))

@@ -547,6 +547,45 @@ def test_linear_pre_fused_producers(tp, dtype, batch):
     assert torch.equal(y2, ref2)   # identical staged activations -> identical product
 
 
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
+@pytest.mark.parametrize("batch", [1, 2, 3, 4])
+@pytest.mark.parametrize("d,f", [(3072, 9216), (1496, 48), (4096, 11008)])
+def test_linear_epi_swiglu(tp, dtype, batch, d, f):
+    # TR_LINEAR_EPI_SWIGLU on an interleaved gate|up weight == plain linear, then tr_silu_mul
+    from paper_2506_23025_b200 import _lib
+    from paper_2506_23025_b200.device import _ACT, interleave_gate_up, linear_pre
+
+    tdt = getattr(torch, dtype)
+    g = torch.Generator(device="cuda").manual_seed(batch + f)
+    W = torch.randn(2 * f, d, generator=g, device="cuda")
+    w_il = tp.TernaryWeight.from_float(interleave_gate_up(W, f))
+    w = tp.TernaryWeight.from_float(W)
+    x = torch.randn(batch, d, generator=g, device="cuda").to(tdt)
+    st = _lib.stream_handle()
+    gu = tp.linear(x, w)
+    ref = torch.empty((batch, f), dtype=tdt, device="cuda")
+    _lib.call("tr_silu_mul", _ACT[tdt], gu.data_ptr(), ref.data_ptr(), batch, f, st)
+    ref = ref.float()
+    tol = 2e-2 if dtype == "bfloat16" else 4e-3   # two roundings of silu(g) * u, relative to the row max
+    y = tp.linear(x, w_il, epi_swiglu=True).float()
+    assert y.shape == (batch, f)
+    assert ((y - ref).abs().amax(1) / ref.abs().amax(1)).max().item() <= tol
+    # fused with the add + rmsnorm producer (the decoder's MLP entry)
+    delta = torch.randn(batch, d, generator=g, device="cuda").to(tdt)
+    gamma = (torch.rand(d, generator=g, device="cuda") + 0.5).to(tdt)
+    h_ref, xn = x.clone(), torch.empty_like(x)
+    _lib.call("tr_add_rmsnorm", _ACT[tdt], h_ref.data_ptr(), delta.data_ptr(), gamma.data_ptr(), xn.data_ptr(),
+              batch, d, 1e-5, st)
+    gu2 = tp.linear(xn, w)
+    ref2 = torch.empty((batch, f), dtype=tdt, device="cuda")
+    _lib.call("tr_silu_mul", _ACT[tdt], gu2.data_ptr(), ref2.data_ptr(), batch, f, st)
+    ref2 = ref2.float()
+    h_out = torch.empty_like(x)
+    y2 = linear_pre(x, w_il, _lib.PRE_ADD_RMSNORM, delta, gamma, h_out, epi_swiglu=True).float()
+    assert torch.equal(h_out, h_ref)
+    assert ((y2 - ref2).abs().amax(1) / ref2.abs().amax(1)).max().item() <= tol
+
+
 # ---------------------------------------------------------------- int8-slice GEMV (batch 1-2)
 
 def _s8_inputs(rng, kind, batch, cols, dtype):
