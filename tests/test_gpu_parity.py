@@ -586,6 +586,19 @@ def test_linear_epi_swiglu(tp, dtype, batch, d, f):
     assert ((y2 - ref2).abs().amax(1) / ref2.abs().amax(1)).max().item() <= tol
 
 
+def test_linear_epi_swiglu_rejects_unsupported(tp):
+    # the epilogue needs whole gate/up tile pairs and the int8-slice GEMV (batch <= 4): loud errors
+    from paper_2506_23025_b200 import _lib
+
+    g = torch.Generator(device="cuda").manual_seed(0)
+    w_odd = tp.TernaryWeight.from_float(torch.randn(48, 512, generator=g, device="cuda"))   # 3 tiles
+    with pytest.raises(_lib.TriRunError):
+        tp.linear(torch.randn(1, 512, generator=g, device="cuda").half(), w_odd, epi_swiglu=True)
+    w = tp.TernaryWeight.from_float(torch.randn(64, 512, generator=g, device="cuda"))
+    with pytest.raises(_lib.TriRunError):
+        tp.linear(torch.randn(5, 512, generator=g, device="cuda").half(), w, epi_swiglu=True)
+
+
 # ---------------------------------------------------------------- int8-slice GEMV (batch 1-2)
 
 def _s8_inputs(rng, kind, batch, cols, dtype):
