@@ -139,8 +139,6 @@ __global__ void __launch_bounds__(128) k_attn_decode(const T* __restrict__ qkv, 
                                                      const T* __restrict__ cs, const T* __restrict__ sn,
                                                      T* __restrict__ kc, T* __restrict__ vc, T* __restrict__ out,
                                                      int H, int S, float scale) {
-  griddep_wait();
-  griddep_launch_dependents();
   static_assert(D == 128, "one key per thread, 4 dims per lane");
   __shared__ __align__(16) T vs[128][D];   // values of keys 0..pos
   __shared__ __align__(16) T kp[D];        // this token's rotated key
@@ -149,18 +147,32 @@ __global__ void __launch_bounds__(128) k_attn_decode(const T* __restrict__ qkv, 
   __shared__ float part[4][D];
   __shared__ float red[32];
   const int hh = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int p = (int)pos[0], n = p + 1;
   const T* kb = kc + (int64_t)hh * S * D;
   const T* vb = vc + (int64_t)hh * S * D;
-  // cached values -> shared memory (asynchronous), cached key tid -> registers
-  for (int c = tid; c < p * (D / 8); c += 128) cp_async16(&vs[c / (D / 8)][(c % (D / 8)) * 8], vb + (int64_t)c * 8);
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  // cached values [lo, hi) -> shared memory (asynchronous), cached key tid -> registers.  Each
+  // thread owns fixed chunks (c = tid mod 128), so a thread can top up its own range.
   uint4 kv[D / 8];
-  if (tid < p) {
-    const uint4* kr = reinterpret_cast<const uint4*>(kb + (int64_t)tid * D);
+  auto load_cache = [&](int lo, int hi) {
+    for (int c = lo * (D / 8) + tid; c < hi * (D / 8); c += 128)
+      cp_async16(&vs[c / (D / 8)][(c % (D / 8)) * 8], vb + (int64_t)c * 8);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    if (tid >= lo && tid < hi) {
+      const uint4* kr = reinterpret_cast<const uint4*>(kb + (int64_t)tid * D);
 #pragma unroll
-    for (int j = 0; j < D / 8; ++j) kv[j] = kr[j];
-  }
+      for (int j = 0; j < D / 8; ++j) kv[j] = kr[j];
+    }
+  };
+  // The cache rows before this token were written a whole decode step ago, so they load before
+  // griddepcontrol.wait, under the QKV GEMV's tail.  pos itself may still be in flight (layer 0:
+  // the previous step's greedy kernel can overlap through the PDL chain), so it is read again
+  // after the wait and the missing rows are topped up; pos never decreases while a chain is in
+  // flight (reset() is stream-ordered), so the speculative range is a prefix of the real one.
+  const int p_spec = (int)*reinterpret_cast<const volatile int64_t*>(pos);
+  load_cache(0, p_spec);
+  griddep_wait();
+  griddep_launch_dependents();
+  const int p = (int)pos[0], n = p + 1;
+  if (p > p_spec) load_cache(p_spec, p);
   // rotary embedding of this token's q and k; k and v into the caches (and shared memory)
   if (tid < D / 2) {
     const float c = to_f(cs[(int64_t)p * (D / 2) + tid]), s = to_f(sn[(int64_t)p * (D / 2) + tid]);

@@ -6,7 +6,7 @@ from paper_2506_23025_b200.decoder import DecoderConfig, TernaryDecoder
 cfg = DecoderConfig()
 m = TernaryDecoder(cfg)
 prompt = torch.randint(0, cfg.vocab, (64,), device="cuda")
-for combo in [(0,0,0,0),(1,1,1,1),(1,1,0,0),(0,0,1,0),(0,0,0,1),(1,1,1,0),(1,1,0,1)]:
+for combo in [(0,0,0,0),(1,1,1,1),(1,1,0,0),(0,0,1,1),(1,0,0,0),(0,1,0,0),(0,0,1,0),(0,0,0,1)]:
     m.cosched = tuple(bool(c) for c in combo)
     m.graph = None
     m.reset(); m.prefill(prompt); m.capture()
