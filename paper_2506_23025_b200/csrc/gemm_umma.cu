@@ -179,9 +179,15 @@ struct UmmaCfg {
   static constexpr int TBB = FMT == kFmtTq1 ? kQ1TileBlockBytes : kTileBlockBytes;
   // TMA requests cost ~100 SM cycles each whatever their size, so the weights move in
   // stages of KS blocks (8 requests of KS x 1056 B) and the activations in one 3-D box per block
+#ifndef UMMA_N128_RB
+#define UMMA_N128_RB 3
+#endif
+  // N = 128: three 64 KB activation stages and two weight stages (exactly 227 KB).  The
+  // activation ring's turnaround (commit -> refill -> landed) bounds the block rate, so its
+  // depth matters more than the weight ring's
   static constexpr int KS = N <= 32 ? 4 : 2;                 // 256-blocks per weight stage
-  static constexpr int RW = N <= 32 ? 4 : 3;                 // weight stages
-  static constexpr int RB = N <= 32 ? 4 : N <= 64 ? 3 : 2;   // activation stages (one block each)
+  static constexpr int RW = N <= 32 ? 4 : (N == 128 && UMMA_N128_RB == 3) ? 2 : 3;   // weight stages
+  static constexpr int RB = N <= 32 ? 4 : N <= 64 ? 3 : UMMA_N128_RB;   // activation stages (one block each)
   static constexpr int kStageWBytes = 8 * KS * UB;          // 128 rows x KS blocks
   static constexpr int kStageBBytes = N * 512;               // N rows x 256 K (4 swizzled 64-K atoms)
   static constexpr int kMaxA = 3;                            // TMEM A buffers (128 columns = one block each)
