@@ -187,13 +187,16 @@ struct UmmaCfg {
   // depth matters more than the weight ring's
   static constexpr int KS = N <= 32 ? 4 : 2;                 // 256-blocks per weight stage
   static constexpr int RW = N <= 32 ? 4 : (N == 128 && UMMA_N128_RB == 3) ? 2 : 3;   // weight stages
-  static constexpr int RB = N <= 32 ? 4 : N <= 64 ? 3 : UMMA_N128_RB;   // activation stages (one block each)
+  // (N = 32, 64: the spare shared memory goes to activation stages as well: +0.5-1.2% at b = 32-64;
+  // N = 16 measured no gain from 8)
+  static constexpr int RB = N <= 16 ? 4 : N <= 64 ? 5 : UMMA_N128_RB;   // activation stages (one block each)
   static constexpr int kStageWBytes = 8 * KS * UB;          // 128 rows x KS blocks
   static constexpr int kStageBBytes = N * 512;               // N rows x 256 K (4 swizzled 64-K atoms)
   static constexpr int kMaxA = 3;                            // TMEM A buffers (128 columns = one block each)
   static constexpr size_t kBOff = 1024;                      // 1024-aligned for the 128B swizzle
   static constexpr size_t kWOff = kBOff + (size_t)RB * kStageBBytes;
   static constexpr size_t kSmem = kWOff + (size_t)RW * kStageWBytes + 1024;   // + alignment slack
+  static_assert(kSmem <= 227 * 1024, "K5 stages exceed the shared memory of one CTA");
 };
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
