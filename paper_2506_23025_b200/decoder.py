@@ -73,6 +73,8 @@ def _ternary(rows, cols, gen, device):
 
 
 class TernaryDecoder:
+    STEPS_PER_GRAPH = 8   # decode steps per CUDA-graph replay (decode(n) uses single steps for the remainder)
+
     def __init__(self, cfg: DecoderConfig = DecoderConfig(), device="cuda", seed: int = 0, dense: bool = False,
                  weights=None, dtype=torch.float16, fused: bool = True):
         self.cfg, self.device, self.dense, self.dtype = cfg, torch.device(device), dense, dtype
@@ -117,6 +119,7 @@ class TernaryDecoder:
         self.cosched = (False, False, False, False)
         self._prefill_graphs = {}
         self.graph = None
+        self.graph_multi = None    # STEPS_PER_GRAPH decode steps in one graph (no replay boundaries)
 
     # -- building blocks ----------------------------------------------------------------
     def _lin(self, x, w):
@@ -291,6 +294,12 @@ class TernaryDecoder:
             self.graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(self.graph, stream=s):
                 self._decode_body()
+            # the same step chained STEPS_PER_GRAPH times: the PDL chain runs on across steps
+            # instead of draining at each replay boundary
+            self.graph_multi = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph_multi, stream=s):
+                for _ in range(self.STEPS_PER_GRAPH):
+                    self._decode_body()
         torch.cuda.synchronize(self.device)
         self.tok.copy_(saved[0])
         self.pos.copy_(saved[1])
@@ -302,7 +311,9 @@ class TernaryDecoder:
         """n greedy decode steps as n graph replays (no host synchronisation)."""
         if self.graph is None:
             self.capture()
-        for _ in range(n):
+        for _ in range(n // self.STEPS_PER_GRAPH):
+            self.graph_multi.replay()
+        for _ in range(n % self.STEPS_PER_GRAPH):
             self.graph.replay()
 
     def reset(self) -> None:
