@@ -401,12 +401,12 @@ def test_decoder_graph_decode_matches_eager_greedy(tp):
     prompt = torch.randint(0, cfg.vocab, (10,), device="cuda", generator=torch.Generator(device="cuda").manual_seed(3))
     m.reset()
     m.prefill(prompt)
-    m.decode(6)
-    graph_tokens = m.out_tokens[10:16].clone()
+    m.decode(11)   # one 8-step graph replay + three single-step replays
+    graph_tokens = m.out_tokens[10:21].clone()
     m.reset()
     m.prefill(prompt)
     eager = []
-    for _ in range(6):
+    for _ in range(11):
         logits = m.forward(m.tok, m.pos)
         nxt = logits.argmax().view(1)
         eager.append(int(nxt))
