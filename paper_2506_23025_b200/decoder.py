@@ -151,11 +151,13 @@ class TernaryDecoder:
         g, u = gu[:, : cfg.d_ff], gu[:, cfg.d_ff:]
         return h + self._lin(F.silu(g) * u, lw["down"])
 
-    def forward(self, tokens, pos, h_in=None):
+    def forward(self, tokens, pos, h_in=None, from_start: bool = False):
         """tokens [T] at positions pos [T] -> logits of the last position [vocab] (fills the cache).
-        h_in: the tokens' embedding rows when already gathered (the fused decode step)."""
+        h_in: the tokens' embedding rows when already gathered (the fused decode step).
+        from_start: the caller guarantees pos = 0..T-1 (a prompt), so prompt attention is plain
+        causal attention over the first T cache rows (the flash kernel, no mask tensor)."""
         if self.fused:
-            return self._forward_fused(tokens, pos, h_in)
+            return self._forward_fused(tokens, pos, h_in, from_start)
         T = tokens.shape[0]
         h = self.weights["embed"][tokens]
         for i in range(self.cfg.n_layers):
@@ -163,7 +165,7 @@ class TernaryDecoder:
         h = self._rms(h[-1:], self.norm_out)
         return F.linear(h, self.weights["lm_head"])[0]
 
-    def _forward_fused(self, tokens, pos, h_in=None):
+    def _forward_fused(self, tokens, pos, h_in=None, from_start=False):
         """Same computation with the glue as single kernels.  Decode (T = 1) of the ternary
         model folds residual-add + RMSNorm into the QKV / gate|up GEMVs and SwiGLU into the
         down GEMV (tr_linear_pre): 5 launches per layer."""
@@ -190,10 +192,14 @@ class TernaryDecoder:
             else:        # prompt: rope + cache append, then causal attention (not the decode hot path)
                 _lib.call("tr_rope_kv", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(), self.sin.data_ptr(),
                           q.data_ptr(), self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), T, H, D, S, st)
-                keys = torch.arange(S, device=self.device)
-                mask = keys[None, :] <= pos[:, None]
-                att = F.scaled_dot_product_attention(q.transpose(0, 1)[None], self.k_cache[i][None],
-                                                     self.v_cache[i][None], attn_mask=mask[None, None])
+                if from_start:
+                    att = F.scaled_dot_product_attention(q.transpose(0, 1)[None], self.k_cache[i][None, :, :T],
+                                                         self.v_cache[i][None, :, :T], is_causal=True)
+                else:
+                    keys = torch.arange(S, device=self.device)
+                    mask = keys[None, :] <= pos[:, None]
+                    att = F.scaled_dot_product_attention(q.transpose(0, 1)[None], self.k_cache[i][None],
+                                                         self.v_cache[i][None], attn_mask=mask[None, None])
                 att = att[0].transpose(0, 1).reshape(T, d)
             o = self._lin(att, lw["o"])
             _lib.call("tr_add_rmsnorm", act, h.data_ptr(), o.data_ptr(), self.norm_mlp[i].data_ptr(), xn.data_ptr(),
@@ -266,7 +272,7 @@ class TernaryDecoder:
 
     def _prefill_body(self, prompt: torch.Tensor) -> None:
         T = prompt.shape[0]
-        logits = self.forward(prompt, self._positions[:T])
+        logits = self.forward(prompt, self._positions[:T], from_start=True)
         self.tok.copy_(logits.argmax().view(1))
         self.pos.fill_(T)
         self.h0.copy_(self.weights["embed"][self.tok])

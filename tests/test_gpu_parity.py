@@ -365,6 +365,8 @@ def test_decoder_fused_glue_matches_torch_glue(tp, dtype):
     a, b = fused.forward(prompt, pos).float(), ref.forward(prompt, pos).float()   # prefill (T = 9)
     tol = 2e-2 if dtype == "bfloat16" else 5e-3
     assert ((a - b).abs().max() / b.abs().max()).item() <= tol
+    c = fused.forward(prompt, pos, from_start=True).float()   # causal flash path == masked path
+    assert ((c - b).abs().max() / b.abs().max()).item() <= tol
     t1, p1 = prompt[:1] * 0 + 7, torch.tensor([9], device="cuda")
     a, b = fused.forward(t1, p1).float(), ref.forward(t1, p1).float()             # one decode step (T = 1)
     assert ((a - b).abs().max() / b.abs().max()).item() <= tol
