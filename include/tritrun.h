@@ -53,6 +53,8 @@ extern "C" {
 #define TR_LINEAR_EPI_SWIGLU 64    /* bit 6: W's rows are 16-row tiles alternating gate / up (2 F rows);
                                     * y[batch, F] = silu(gate) * up with the roundings of an fp16/bf16
                                     * gate|up store followed by tr_silu_mul (int8-slice GEMV, batch <= 4) */
+#define TR_LINEAR_OUT_F32 128      /* bit 7: y is float32 (the fp32 accumulators, not rounded to the
+                                    * activation type): row-parallel partials for an fp32 all-reduce */
 
 TR_API const char* tr_last_error(void);
 TR_API int tr_version(void);

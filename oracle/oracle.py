@@ -64,6 +64,7 @@ def _load():
         lib.orc_dequantize_blocks.argtypes = [p, p, p, i64]
         for name in ("orc_gemm_tq2", "orc_gemm_tq1"):
             getattr(lib, name).argtypes = [p, p, p, p, i64, i64, i64, i64, i64, p]
+        lib.orc_gemv_f64.argtypes = [ctypes.c_int, p, p, p, p, i64, i64, i64, i64, i64]
         _lib = lib
     return _lib
 
@@ -207,6 +208,25 @@ def dequantize_matrix(payload, scales, cols, fmt, dtype=np.float64):
 def gemv_reference(payload, scales, cols, fmt, x):
     """linear.py:201-208: dequantize fully, dense float64 product."""
     return dequantize_matrix(payload, scales, cols, fmt) @ np.asarray(x, np.float64)
+
+
+def gemv_reference_batch(payload, scales, cols, fmt, X, threads=None):
+    """linear.py:177-208 at full size: float64 W x for every row of X (batch, cols) without the
+    dense matrix (oracle/tritpack_oracle.c orc_gemv_f64), rows sharded over host threads."""
+    pay = _c(payload, np.uint8)
+    sc = _c(np.asarray(scales).view(np.uint16), np.uint16)
+    X = _c(np.atleast_2d(X), np.float64)
+    rows = sc.shape[0]
+    out = np.empty((X.shape[0], rows), np.float64)
+    threads = threads or min(32, os.cpu_count() or 1)
+    chunk = -(-rows // threads)
+    lib = _load()
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        futs = [pool.submit(lib.orc_gemv_f64, int(fmt), _ptr(pay), _ptr(sc), _ptr(X), _ptr(out), rows, int(cols),
+                            X.shape[0], lo, min(lo + chunk, rows)) for lo in range(0, rows, chunk)]
+        for f in futs:
+            f.result()
+    return out
 
 
 def gemm(payload, scales, cols, fmt, X, threads=1, kern=kernels):

@@ -150,3 +150,53 @@ void orc_gemm_tq1(const uint8_t *payload, const float *scales, const float *x,
         accumulate_row(dg_scratch, scales + r * nb, x, out, rows, r, nb, batch);
     }
 }
+
+/* reference: linear.py:177-208 (dequantize_matrix + gemv_reference) for large
+ * shapes: out[j, r] = sum_k f64(scale[r, k / 256]) * (digit(r, k) - 1) * x[j, k]
+ * in float64, without materialising the dense matrix.  Digits as dequantize_matrix
+ * decodes them: TQ2 by shifts (:184-186), TQ1 by the canonical division formula
+ * x = (c * 243 + 13) >> 8, d_j = (x // 3^(4-j)) % 3 (:189-192).  Scales are binary16
+ * bit patterns (PackedMatrix.scales).  Rows [row0, row1), x: [batch, cols] float64. */
+static double f16_to_f64(uint16_t h) {
+    const int s = h >> 15, e = (h >> 10) & 31, m = h & 1023;
+    double v;
+    if (e == 0) v = m * (1.0 / 16777216.0);               /* m * 2^-24 */
+    else if (e == 31) v = m ? (0.0 / 0.0) : (1.0 / 0.0);
+    else {
+        v = 1.0 + m / 1024.0;
+        for (int i = 15; i < e; ++i) v *= 2.0;
+        for (int i = e; i < 15; ++i) v *= 0.5;
+    }
+    return s ? -v : v;
+}
+
+void orc_gemv_f64(int fmt, const uint8_t *payload, const uint16_t *scales, const double *x, double *out,
+                  int64_t rows, int64_t cols, int64_t batch, int64_t row0, int64_t row1) {
+    const int64_t nb = (cols + BLK - 1) / BLK;
+    const int pb = fmt == 2 ? TQ2_PB : TQ1_PB;
+    static const uint32_t pw[5] = {81, 27, 9, 3, 1};
+    for (int64_t r = row0; r < row1; ++r) {
+        for (int64_t j = 0; j < batch; ++j) out[j * rows + r] = 0.0;
+        for (int64_t b = 0; b < nb; ++b) {
+            const uint8_t *p = payload + (r * nb + b) * pb;
+            const double s = f16_to_f64(scales[r * nb + b]);
+            int8_t t[260];
+            if (fmt == 2) {
+                for (int i = 0; i < TQ2_PB; ++i)
+                    for (int q = 0; q < 4; ++q) t[4 * i + q] = (int8_t)((p[i] >> (2 * q)) & 3) - 1;
+            } else {
+                for (int i = 0; i < TQ1_PB; ++i) {
+                    const uint32_t xq = ((uint32_t)p[i] * 243u + 13u) >> 8;
+                    for (int q = 0; q < 5; ++q) t[5 * i + q] = (int8_t)((xq / pw[q]) % 3) - 1;
+                }
+            }
+            const int64_t k0 = b * BLK, kn = (cols - k0) < BLK ? (cols - k0) : BLK;
+            for (int64_t j = 0; j < batch; ++j) {
+                const double *xr = x + j * cols + k0;
+                double acc = 0.0;
+                for (int64_t k = 0; k < kn; ++k) acc += (s * t[k]) * xr[k];
+                out[j * rows + r] += acc;
+            }
+        }
+    }
+}

@@ -1,19 +1,20 @@
-"""TPK1 container -> device loader (SURVEY §8(f) rank 1).
+"""TPK1 container -> device loader (SURVEY 8(f) rank 1).
 
-The reference's container (`container.py`) is a flat file of tensors:
+File format (the reference's writer, container.py:1-17, 167-196): little-endian
+``b"TPK1" | u32 version (1) | u32 count`` then ``count`` records of
+``u16 name length | UTF-8 name | u8 dtype tag | u8 ndims | u64 dims[ndims] | u64 data length |
+zero fill to a 32-byte file offset | data``.  Quantized data is rows x ceil(cols/256) blocks of
+``payload | binary16 scale`` (PackedMatrix.to_block_bytes, linear.py:73-82).
 
-    header:  magic b"TPK1" | version u32 = 1 | tensor_count u32            (container.py:1-17)
-    record:  name_len u16 | name | dtype u8 | ndims u8 | dims u64 * ndims | data_len u64
-             | zero padding to a 32-byte file offset | data                 (container.py:167-182)
-    data:    F32/F16 raw; TQ2/TQ1 per 256-element block: payload then the binary16 scale
-             (PackedMatrix.to_block_bytes, linear.py:73-82)
+The B200 part is ``record_to_device``: a quantized record's bytes go to the GPU untouched and
+one kernel (``tr_repack_records``) splits payload from scale and writes the T16 tiles; F16 /
+F32 tensors become device tensors.  It takes any record with ``name / dtype / dims / data``
+(this module's ``TensorRecord`` or the reference's own ``tritpack.container.TensorRecord``).
 
-``read_container`` restates the reference parser with the same validation and the same error
-types (container.py:34-57, 198-242), so callers written against the reference behave the
-same.  ``load_to_device`` is the B200 addition: each quantized record's bytes go to the GPU
-as they are and one kernel (``tr_repack_records``) de-interleaves payload and scale and
-writes the T16 tiles; F16/F32 tensors become device tensors.  There is no host-side
-unpacking and no CPU fallback.
+``parse_container`` is a scanner of our own for the same byte format.  It raises the error
+classes reference callers already catch (container.py:34-57: bad magic, version, truncation,
+size mismatch, all ``ContainerError``), so code written against the reference reader keeps
+its error handling.
 """
 
 from __future__ import annotations
@@ -33,57 +34,45 @@ MAGIC = b"TPK1"
 VERSION = 1
 DATA_ALIGN = 32
 
-_HEADER = struct.Struct("<4sII")
-_NAME_LEN = struct.Struct("<H")
-_REC_FIXED = struct.Struct("<BB")
-_U64 = struct.Struct("<Q")
-_NUMPY_DTYPES = {DType.F32: np.dtype("<f4"), DType.F16: np.dtype("<f2")}
-
 
 class ContainerError(Exception):
-    """Base for container format failures (container.py:34-35)."""
+    """Any malformed TPK1 input."""
 
 
 class BadMagicError(ContainerError):
-    pass
+    """The first four bytes are not TPK1."""
 
 
 class VersionMismatchError(ContainerError):
-    pass
+    """A version other than 1."""
 
 
 class TruncatedError(ContainerError):
-    pass
+    """The input ends inside a field."""
 
 
 class SizeMismatchError(ContainerError):
-    pass
+    """data length disagrees with dims x dtype."""
 
 
 def rows_cols(dims: Sequence[int]) -> tuple[int, int]:
-    """Leading dims collapse into rows; the last dim is cols (container.py:60-65)."""
-    rows = 1
-    for d in dims[:-1]:
-        rows *= d
-    return rows, dims[-1]
+    """(product of the leading dims, last dim): how a quantized tensor is laid out as a matrix."""
+    return int(np.prod(dims[:-1], dtype=np.int64)) if len(dims) > 1 else 1, int(dims[-1])
 
 
 def expected_data_len(dims: Sequence[int], dtype: DType) -> int:
-    """Data-section bytes for a tensor of this shape and format (container.py:68-82)."""
-    if len(dims) == 0 or any(d < 1 for d in dims):
+    """Bytes the data section of a `dims` tensor in `dtype` occupies."""
+    if not dims or min(dims) < 1:
         raise ValueError(f"dims must be positive, got {tuple(dims)}")
     if dtype.is_quantized:
         rows, cols = rows_cols(dims)
         return rows * (-(-cols // BLOCK_ELEMENTS)) * dtype.block_bytes
-    count = 1
-    for d in dims:
-        count *= d
-    return count * (4 if dtype is DType.F32 else 2)
+    return int(np.prod(dims, dtype=np.int64)) * (4 if dtype is DType.F32 else 2)
 
 
 @dataclass(frozen=True)
 class TensorRecord:
-    """One named tensor as stored (container.py:90-146); ``data`` is a zero-copy view."""
+    """One stored tensor; ``data`` is a zero-copy slice of the file bytes."""
 
     name: str
     dtype: DType
@@ -91,60 +80,58 @@ class TensorRecord:
     data: memoryview
 
 
-class _Reader:
-    def __init__(self, raw: memoryview):
-        self.raw = raw
-        self.pos = 0
-
-    def take(self, n: int, what: str) -> memoryview:
-        if self.pos + n > len(self.raw):
-            raise TruncatedError(f"file ends inside {what}: need {n} bytes at offset {self.pos}, "
-                                 f"have {len(self.raw) - self.pos}")
-        chunk = self.raw[self.pos:self.pos + n]
-        self.pos += n
-        return chunk
-
-
 def parse_container(raw: bytes) -> list[TensorRecord]:
-    """Parse TPK1 bytes, validating exactly as the reference's read_container (container.py:198-242)."""
-    rd = _Reader(memoryview(raw))
-    magic, version, count = _HEADER.unpack(rd.take(_HEADER.size, "header"))
-    if magic != MAGIC:
-        raise BadMagicError(f"not a TPK1 file (magic {bytes(magic)!r})")
+    """Scan TPK1 bytes into records, validating every field before it is used."""
+    buf = memoryview(raw)
+    end = len(buf)
+    off = 0
+
+    def take(n: int, field: str) -> memoryview:
+        nonlocal off
+        if n > end - off:
+            raise TruncatedError(f"truncated at byte {off}: {field} needs {n} bytes, {end - off} left")
+        piece = buf[off:off + n]
+        off += n
+        return piece
+
+    def u(nbytes: int, field: str) -> int:
+        return int.from_bytes(take(nbytes, field), "little")
+
+    if bytes(take(4, "magic")) != MAGIC:
+        raise BadMagicError(f"bad magic {bytes(buf[:4])!r}, expected {MAGIC!r}")
+    version = u(4, "version")
     if version != VERSION:
-        raise VersionMismatchError(f"unsupported container version {version}")
-    records = []
-    for i in range(count):
-        (name_len,) = _NAME_LEN.unpack(rd.take(_NAME_LEN.size, f"tensor {i} name length"))
+        raise VersionMismatchError(f"container version {version} is not {VERSION}")
+    out = []
+    for idx in range(u(4, "tensor count")):
+        raw_name = bytes(take(u(2, f"record {idx} name length"), f"record {idx} name"))
         try:
-            name = bytes(rd.take(name_len, f"tensor {i} name")).decode("utf-8")
+            name = raw_name.decode("utf-8")
         except UnicodeDecodeError as exc:
-            raise ContainerError(f"tensor {i}: name is not valid UTF-8") from exc
-        tag, ndims = _REC_FIXED.unpack(rd.take(_REC_FIXED.size, f"tensor {name!r} header"))
-        try:
-            dtype = DType(tag)
-        except ValueError:
-            raise ContainerError(f"tensor {name!r}: unknown dtype tag {tag}") from None
-        if ndims == 0:
-            raise ContainerError(f"tensor {name!r}: ndims must be >= 1")
-        dims = tuple(_U64.unpack(rd.take(_U64.size, f"tensor {name!r} dims"))[0] for _ in range(ndims))
-        (data_len,) = _U64.unpack(rd.take(_U64.size, f"tensor {name!r} data length"))
-        rd.take(-rd.pos % DATA_ALIGN, f"tensor {name!r} alignment padding")
-        data = rd.take(data_len, f"tensor {name!r} data")
-        if any(d < 1 for d in dims):
-            raise ContainerError(f"tensor {name!r}: dims {dims} must be positive")
-        expected = expected_data_len(dims, dtype)
-        if data_len != expected:
-            raise SizeMismatchError(f"tensor {name!r}: data_len {data_len} but dims {dims} x {dtype.name} "
-                                    f"require {expected}")
-        records.append(TensorRecord(name=name, dtype=dtype, dims=dims, data=data))
-    if rd.pos != len(rd.raw):
-        raise ContainerError(f"{len(rd.raw) - rd.pos} trailing bytes after the last tensor")
-    return records
+            raise ContainerError(f"record {idx}: name bytes are not UTF-8") from exc
+        tag, ndims = u(1, f"{name}: dtype tag"), u(1, f"{name}: ndims")
+        if tag not in {t.value for t in DType}:
+            raise ContainerError(f"{name}: unknown dtype tag {tag}")
+        if ndims < 1:
+            raise ContainerError(f"{name}: ndims is 0 (need at least one dimension)")
+        dims = struct.unpack(f"<{ndims}Q", take(8 * ndims, f"{name}: dims"))
+        nbytes = u(8, f"{name}: data length")
+        take((-off) % DATA_ALIGN, f"{name}: padding")
+        data = take(nbytes, f"{name}: data")
+        if min(dims) < 1:
+            raise ContainerError(f"{name}: every dimension must be positive, got {dims}")
+        dtype = DType(tag)
+        want = expected_data_len(dims, dtype)
+        if nbytes != want:
+            raise SizeMismatchError(f"{name}: {nbytes} data bytes stored, {dtype.name} {dims} needs {want}")
+        out.append(TensorRecord(name, dtype, tuple(dims), data))
+    if off != end:
+        raise ContainerError(f"{end - off} trailing bytes after record {len(out) - 1}")
+    return out
 
 
 def read_container(path) -> list[TensorRecord]:
-    """Parse a TPK1 file (the reference's read_container contract)."""
+    """``parse_container`` of a file's bytes."""
     with open(path, "rb") as fh:
         return parse_container(fh.read())
 
@@ -153,8 +140,10 @@ def record_to_device(rec: TensorRecord, device="cuda"):
     """One record on the GPU: TQ2/TQ1 -> TernaryWeight (leading dims collapsed into rows);
     F16/F32 -> a device tensor in the stored shape."""
     dev = torch.device(device)
+    rec_dtype = DType(int(rec.dtype))   # (the reference's DType has the same tags, blocks.py:45-52)
+    rec = TensorRecord(rec.name, rec_dtype, tuple(int(d) for d in rec.dims), memoryview(rec.data))
     if not rec.dtype.is_quantized:
-        arr = np.frombuffer(rec.data, dtype=_NUMPY_DTYPES[rec.dtype]).reshape(rec.dims)
+        arr = np.frombuffer(rec.data, dtype="<f4" if rec.dtype is DType.F32 else "<f2").reshape(rec.dims)
         return torch.from_numpy(arr.copy()).to(dev)
     rows, cols = rows_cols(rec.dims)
     records = torch.frombuffer(bytearray(rec.data), dtype=torch.uint8).to(dev)   # raw [payload | scale] records

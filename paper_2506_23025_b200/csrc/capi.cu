@@ -29,14 +29,15 @@ int check_launch(const char* what) {
 
 int gemv_tq2(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
              int cols, int ctas, int pdl, cudaStream_t st, int pre, const void* pre_delta, const void* pre_gamma,
-             void* pre_out, float eps);
+             void* pre_out, float eps, int out_f32);
 size_t gemv_workspace_bytes(int batch, int rows, int cols);
 bool gemv_s8_fits(int batch, int rows, int cols);
 int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows, int cols,
             int ctas, int pdl, cudaStream_t st, int pre, const void* pre_delta, const void* pre_gamma, void* pre_out,
-            float eps, int cosched, int epi);
+            float eps, int cosched, int epi, int out_f32);
 int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
-              int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg);
+              int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg,
+              int out_f32);
 size_t umma_workspace_bytes(int batch, int rows, int cols);
 bool gemv_stages_x(int batch, int rows, int cols);
 int gemv_chain(int act, const TrChainLayer* host_layers, void* dev_table, int n_layers, int batch, unsigned* bar,
@@ -74,12 +75,22 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
   TR_REQUIRE(ldx >= cols && ldy >= ((flags & TR_LINEAR_EPI_SWIGLU) ? rows / 2 : rows),
              "tr_linear: leading dimensions too small");
   TR_REQUIRE(((uintptr_t)w & 15) == 0, "tr_linear: weight buffer must be 16-byte aligned");
+  const int epi = (flags & TR_LINEAR_EPI_SWIGLU) ? 1 : 0;
+  const int out_f32 = (flags & TR_LINEAR_OUT_F32) ? 1 : 0;
+  TR_REQUIRE(!(epi && out_f32), "tr_linear: TR_LINEAR_OUT_F32 does not combine with the SwiGLU epilogue");
   if (batch == 0) return 0;
   const int pdl = flags & TR_LINEAR_PDL;
   const int uniform = (flags & TR_LINEAR_UNIFORM_SCALE) ? 1 : 0;
   const int knob = (flags >> 8) & 0xFFFF;   // GEMV: CTA count; UMMA: K split (0 = automatic)
   cudaStream_t st = (cudaStream_t)stream;
   const bool aligned = (ldx % 8) == 0 && ((uintptr_t)x & 15) == 0;
+  const bool s8 = batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols);
+  if (epi) {   // only the int8-slice GEMV knows the gate/up tile pairing: never fall through to another path
+    TR_REQUIRE(fmt == kFmtTq2 && s8 && !(flags & TR_LINEAR_FORCE_UMMA),
+               "tr_linear: the SwiGLU epilogue runs on the int8-slice GEMV only (TQ2, batch <= 4)");
+    return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, pdl, st, 0, nullptr, nullptr,
+                   nullptr, 0.0f, (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, 1, 0);
+  }
   // measured crossover (scripts/dev/gemv_sweep.py): the mma.sync GEMV wins at batch 1-2 and,
   // while it can stage the activations in shared memory, up to 8; the tensor-core GEMM beyond
   bool use_umma = aligned && (batch >= kUmmaMinBatch || (batch >= 3 && !gemv_stages_x((int)batch, (int)rows, (int)cols)));
@@ -95,18 +106,15 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
   }
   if (use_umma)
     return gemm_umma(fmt, act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, uniform, workspace,
-                     ws_bytes, pdl, st, (flags >> 24) & 0xF);
-  if (flags & TR_LINEAR_EPI_SWIGLU)
-    TR_REQUIRE(batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols),
-               "tr_linear: the SwiGLU epilogue runs on the int8-slice GEMV only (batch <= 4)");
-  if (batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols))
+                     ws_bytes, pdl, st, (flags >> 24) & 0xF, out_f32);
+  if (s8)
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, pdl, st, 0, nullptr, nullptr,
-                   nullptr, 0.0f, (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, (flags & TR_LINEAR_EPI_SWIGLU) ? 1 : 0);
-  const size_t esz = 2;
+                   nullptr, 0.0f, (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, 0, out_f32);
+  const size_t esz = 2, ysz = out_f32 ? 4 : 2;
   for (int64_t n0 = 0; n0 < batch; n0 += 32) {
     const int nb_ = (int)(batch - n0 < 32 ? batch - n0 : 32);
-    int rc = gemv_tq2(act_dtype, w, (const uint8_t*)x + n0 * ldx * esz, (uint8_t*)y + n0 * ldy * esz, ldx, ldy, nb_,
-                      (int)rows, (int)cols, knob, pdl, st, 0, nullptr, nullptr, nullptr, 0.0f);
+    int rc = gemv_tq2(act_dtype, w, (const uint8_t*)x + n0 * ldx * esz, (uint8_t*)y + n0 * ldy * ysz, ldx, ldy, nb_,
+                      (int)rows, (int)cols, knob, pdl, st, 0, nullptr, nullptr, nullptr, 0.0f, out_f32);
     if (rc) return rc;
   }
   return 0;
@@ -124,15 +132,16 @@ int tr_linear_pre(int fmt, const void* w, const void* x, void* y, int64_t batch,
                  ldy >= ((flags & TR_LINEAR_EPI_SWIGLU) ? rows / 2 : rows),
              "tr_linear_pre: leading dimensions");
   TR_REQUIRE(((uintptr_t)w & 15) == 0, "tr_linear_pre: weight buffer must be 16-byte aligned");
+  TR_REQUIRE(!(flags & TR_LINEAR_OUT_F32), "tr_linear_pre: TR_LINEAR_OUT_F32 is not supported here");
   if (flags & TR_LINEAR_EPI_SWIGLU)
     TR_REQUIRE(batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols),
                "tr_linear_pre: the SwiGLU epilogue runs on the int8-slice GEMV only (batch <= 4)");
   if (batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols))
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, (flags >> 8) & 0xFFFF,
                    flags & TR_LINEAR_PDL, (cudaStream_t)stream, pre_op, delta, gamma, x_out, eps,
-                   (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, (flags & TR_LINEAR_EPI_SWIGLU) ? 1 : 0);
+                   (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, (flags & TR_LINEAR_EPI_SWIGLU) ? 1 : 0, 0);
   return gemv_tq2(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, (flags >> 8) & 0xFFFF,
-                  flags & TR_LINEAR_PDL, (cudaStream_t)stream, pre_op, delta, gamma, x_out, eps);
+                  flags & TR_LINEAR_PDL, (cudaStream_t)stream, pre_op, delta, gamma, x_out, eps, 0);
 }
 
 size_t tr_linear_chain_workspace_size(int64_t n_layers) {

@@ -165,6 +165,16 @@ template <> struct Act<__nv_bfloat16> {
   __device__ static float to_float(__nv_bfloat16 v) { return __bfloat162float(v); }
 };
 
+// output element i of y: the activation type (rounded once, RNE) or, with TR_LINEAR_OUT_F32,
+// the fp32 accumulator itself (row-parallel partials that an all-reduce sums)
+template <typename T>
+__device__ __forceinline__ void store_y(void* y, int64_t i, float v, int f32) {
+  if (f32)
+    reinterpret_cast<float*>(y)[i] = v;
+  else
+    reinterpret_cast<T*>(y)[i] = Act<T>::from_float(v);
+}
+
 }  // namespace tr
 
 // ---- error plumbing for the C-ABI ---------------------------------------------------

@@ -107,6 +107,7 @@ __global__ void k_rope_kv(const T* __restrict__ qkv, const int64_t* __restrict__
   griddep_launch_dependents();
   const int t = blockIdx.y, hh = blockIdx.x;
   const int64_t p = pos[t];
+  if (p < 0 || p >= S) return;   // past the cache (callers bound pos on the host too): write nothing
   const T* base = qkv + (int64_t)t * 3 * H * D;
   for (int i = threadIdx.x; i < D / 2; i += blockDim.x) {
     const float c = to_f(cs[p * (D / 2) + i]), s = to_f(sn[p * (D / 2) + i]);
@@ -167,11 +168,18 @@ __global__ void __launch_bounds__(128) k_attn_decode(const T* __restrict__ qkv, 
   // the previous step's greedy kernel can overlap through the PDL chain), so it is read again
   // after the wait and the missing rows are topped up; pos never decreases while a chain is in
   // flight (reset() is stream-ordered), so the speculative range is a prefix of the real one.
-  const int p_spec = (int)*reinterpret_cast<const volatile int64_t*>(pos);
+  int p_spec = (int)*reinterpret_cast<const volatile int64_t*>(pos);
+  p_spec = p_spec < 0 ? 0 : (p_spec > S - 1 ? S - 1 : p_spec);
   load_cache(0, p_spec);
   griddep_wait();
   griddep_launch_dependents();
-  const int p = (int)pos[0], n = p + 1;
+  const int64_t p64 = pos[0];
+  if (p64 < 0 || p64 >= S) {   // past the cache: no cache or shared-memory row p exists; output zeros
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    out[(int64_t)hh * D + tid] = Act<T>::from_float(0.0f);
+    return;
+  }
+  const int p = (int)p64, n = p + 1;
   if (p > p_spec) load_cache(p_spec, p);
   // rotary embedding of this token's q and k; k and v into the caches (and shared memory)
   if (tid < D / 2) {

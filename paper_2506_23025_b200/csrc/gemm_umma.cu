@@ -171,6 +171,7 @@ struct UmmaArgs {
   int uniform;        // every row has one scale for all its blocks
   int dbg;            // development probes: 1 = skip MMAs, 2 = skip decode/TMEM stores
   int map3d;          // activations described by the 3-D tensor map (one TMA request per block)
+  int out_f32;        // TR_LINEAR_OUT_F32: y is float32
 };
 
 template <typename T, int N, int FMT>
@@ -439,14 +440,13 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
     }
     griddep_wait();
     // ---- store: whole K in this CTA -> y; else partials + last-CTA reduction (fixed slice order)
-    T* y = reinterpret_cast<T*>(a.y);
     const int row = mt * kRowsPerCta + r;
     const int n0 = nt * N + half_k * NH;
     if (a.ks == 1) {
       if (row < a.rows)
 #pragma unroll
         for (int e = 0; e < NH; ++e)
-          if (n0 + e < a.batch) y[(int64_t)(n0 + e) * a.ldy + row] = Act<T>::from_float(acc[e]);
+          if (n0 + e < a.batch) store_y<T>(a.y, (int64_t)(n0 + e) * a.ldy + row, acc[e], a.out_f32);
     } else {
       const int tile_mn = nt * a.m_tiles + mt;
       float* part = a.ws + ((int64_t)tile_mn * a.ks + kslice) * (kRowsPerCta * N);
@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
             }
 #pragma unroll
             for (int e = 0; e < 8; ++e)
-              if (n0 + e0 + e < a.batch) y[(int64_t)(n0 + e0 + e) * a.ldy + row] = Act<T>::from_float(v[e]);
+              if (n0 + e0 + e < a.batch) store_y<T>(a.y, (int64_t)(n0 + e0 + e) * a.ldy + row, v[e], a.out_f32);
           }
         if (threadIdx.x == 0) a.counters[tile_mn] = 0;   // self-reset
       }
@@ -571,7 +571,8 @@ static int launch_umma(const CUtensorMap& map, const UmmaArgs& a, int grid, int 
 }
 
 int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
-              int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg) {
+              int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg,
+              int out_f32) {
   UmmaPlan p = plan_umma(batch, rows, cols, ks, sm_count());
   if ((ldx % 8) != 0 || ((uintptr_t)x & 15) != 0) {
     set_error("tr_linear(umma): activations need 16-byte aligned rows (ldx %% 8 == 0)");
@@ -627,6 +628,7 @@ int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t l
   a.uniform = uniform;
   a.dbg = dbg;
   a.map3d = map3d;
+  a.out_f32 = out_f32;
   const int grid = p.m_tiles * p.n_tiles * p.ks;
   const bool bf = act == kActBf16;
 #define TR_UMMA_CASE(NN)                                                                              \

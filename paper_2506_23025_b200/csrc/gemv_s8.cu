@@ -47,6 +47,7 @@ struct S8Args {
   const void* pre_gamma;
   void* pre_out;
   float eps;
+  int out_f32;   // TR_LINEAR_OUT_F32: y is float32
 };
 
 constexpr int kS8SU = 2;
@@ -479,8 +480,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
       const int row = 2 * G2 + (c >> 1);
       if ((c & 1) == 0 && row < nbr) {
         const int r0 = tile * 16 + g, r1 = r0 + 8;
-        if (r0 < a.rows) y[row * a.ldy + r0] = Act<T>::from_float(v[G2][0]);
-        if (r1 < a.rows) y[row * a.ldy + r1] = Act<T>::from_float(v[G2][1]);
+        if (r0 < a.rows) store_y<T>(a.y, (int64_t)row * a.ldy + r0, v[G2][0], a.out_f32);
+        if (r1 < a.rows) store_y<T>(a.y, (int64_t)row * a.ldy + r1, v[G2][1], a.out_f32);
       }
     }
   };
@@ -800,7 +801,7 @@ static int launch_s8(S8Args& a, int grid, int pdl, cudaStream_t st) {
 
 int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows, int cols,
             int ctas, int pdl, cudaStream_t st, int pre, const void* pre_delta, const void* pre_gamma, void* pre_out,
-            float eps, int cosched, int epi) {
+            float eps, int cosched, int epi, int out_f32) {
   if (!gemv_s8_fits(batch, rows, cols)) {
     set_error("tr_linear(gemv-s8): batch %d x %d columns does not fit the int8-slice GEMV", batch, cols);
     return -1;
@@ -825,6 +826,7 @@ int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t
   a.dbg = (ctas >> 12) & 0xF;
   ctas &= 0xFFF;
   a.epi = epi;
+  a.out_f32 = out_f32;
   if (epi && (rows % 32) != 0) {
     set_error("tr_linear(swiglu epilogue): rows (%d) must be whole 16-row gate/up tile pairs", rows);
     return -1;

@@ -107,6 +107,7 @@ struct GemvArgs {
   const void* pre_gamma;
   void* pre_out;
   float eps;
+  int out_f32;                   // TR_LINEAR_OUT_F32: y is float32
 };
 
 // Sense-reversal grid barrier for the persistent chain (all CTAs are co-resident: the
@@ -411,12 +412,12 @@ __global__ void __launch_bounds__(NW * 32, (NW == 8 && NT == 1) ? 2 : 1) k_gemv_
       for (int t = 0; t < NT; ++t) {
         const int n0 = 8 * t + 2 * c, n1 = n0 + 1;
         if (n0 < a.batch) {
-          if (r0 < Ly.rows) y[n0 * Ly.ldy + r0] = Act<T>::from_float(v[t][0]);
-          if (r1 < Ly.rows) y[n0 * Ly.ldy + r1] = Act<T>::from_float(v[t][2]);
+          if (r0 < Ly.rows) store_y<T>(Ly.y, (int64_t)n0 * Ly.ldy + r0, v[t][0], a.out_f32);
+          if (r1 < Ly.rows) store_y<T>(Ly.y, (int64_t)n0 * Ly.ldy + r1, v[t][2], a.out_f32);
         }
         if (n1 < a.batch) {
-          if (r0 < Ly.rows) y[n1 * Ly.ldy + r0] = Act<T>::from_float(v[t][1]);
-          if (r1 < Ly.rows) y[n1 * Ly.ldy + r1] = Act<T>::from_float(v[t][3]);
+          if (r0 < Ly.rows) store_y<T>(Ly.y, (int64_t)n1 * Ly.ldy + r0, v[t][1], a.out_f32);
+          if (r1 < Ly.rows) store_y<T>(Ly.y, (int64_t)n1 * Ly.ldy + r1, v[t][3], a.out_f32);
         }
       }
     };
@@ -715,8 +716,9 @@ static GemvLayer make_layer(const void* w, const void* x, void* y, int64_t ldx, 
 
 int gemv_tq2(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
              int cols, int ctas, int pdl, cudaStream_t st, int pre, const void* pre_delta, const void* pre_gamma,
-             void* pre_out, float eps) {
+             void* pre_out, float eps, int out_f32) {
   GemvArgs a = {};
+  a.out_f32 = out_f32;
   a.pre = pre;
   a.pre_delta = pre_delta;
   a.pre_gamma = pre_gamma;

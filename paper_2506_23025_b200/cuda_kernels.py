@@ -7,9 +7,18 @@ gemm_* write out[:, row0:row1] in place) and bit-identical results.  Each call
 copies its numpy inputs to the device, runs the CUDA kernel through the
 libtritrun C-ABI and copies the result back -- this module is the parity /
 integration surface; the fast path is paper_2506_23025_b200.device.linear().
+
+Frozen weights stay resident: ``PackedMatrix`` freezes its payload and fp32 scale
+arrays (reference linear.py:58-62), so gemm_tq2 / gemm_tq1 upload a read-only
+(payload, scales) pair once and reuse the device copy for every later call and
+every row range ``linear.gemm(threads=N)`` shards it into (linear.py:155-166);
+each call then moves only its activations in and its rows out.
 """
 
 from __future__ import annotations
+
+import threading
+import weakref
 
 import numpy as np
 import torch
@@ -79,13 +88,39 @@ def dequantize_blocks(digits, scales):
     return out.cpu().numpy()
 
 
+_RESIDENT: dict = {}              # id(payload) -> (weakref payload, weakref scales, device payload, device scales)
+_RESIDENT_LOCK = threading.Lock()
+
+
+def _frozen(a) -> bool:
+    return isinstance(a, np.ndarray) and not a.flags.writeable and a.flags.c_contiguous
+
+
+def _weights(payload, scales):
+    """Device copies of (payload, fp32 scales); cached while both arrays are alive and read-only."""
+    if not (_frozen(payload) and _frozen(scales) and scales.dtype == np.float32):
+        return _dev(payload), _dev(np.asarray(scales, np.float32))
+    key = id(payload)
+    with _RESIDENT_LOCK:
+        hit = _RESIDENT.get(key)
+        if hit is not None and hit[0]() is payload and hit[1]() is scales:
+            return hit[2], hit[3]
+        dp, ds = _dev(payload), _dev(scales)
+        try:
+            wp = weakref.ref(payload, lambda _r, k=key: _RESIDENT.pop(k, None))
+            ws = weakref.ref(scales)
+        except TypeError:   # (views of foreign buffers may not take weak references)
+            return dp, ds
+        _RESIDENT[key] = (wp, ws, dp, ds)
+        return dp, ds
+
+
 def _gemm(fmt: int, payload, scales, x, out, row0: int, row1: int) -> None:
     rows, nb = scales.shape
     batch = x.shape[0]
     if row1 <= row0 or batch == 0:
         return
-    p = _dev(payload)
-    s = _dev(np.asarray(scales, np.float32))
+    p, s = _weights(payload, scales)
     xd = _dev(np.asarray(x, np.float32))
     o = torch.empty((batch, rows), dtype=torch.float32, device="cuda")
     _run("tr_gemm_exact", fmt, p.data_ptr(), s.data_ptr(), xd.data_ptr(), o.data_ptr(), rows, nb, batch,

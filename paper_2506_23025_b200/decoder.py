@@ -119,6 +119,7 @@ class TernaryDecoder:
         self.cosched = (False, False, False, False)
         self._prefill_graphs = {}
         self.graph = None
+        self._host_pos = 0
         self.graph_multi = None    # STEPS_PER_GRAPH decode steps in one graph (no replay boundaries)
 
     # -- building blocks ----------------------------------------------------------------
@@ -253,11 +254,18 @@ class TernaryDecoder:
         ~12 host launches per layer."""
         T = prompt.shape[0]
         if not graph:
+            if T > self.cfg.max_seq:
+                raise ValueError(f"prompt of {T} tokens exceeds max_seq={self.cfg.max_seq}")
+            self._host_pos = T
             self._prefill_body(prompt)
             return
+        if T > self.cfg.max_seq:
+            raise ValueError(f"prompt of {T} tokens exceeds max_seq={self.cfg.max_seq}")
+        self._host_pos = T
         if T not in self._prefill_graphs:
             buf = prompt.to(device=self.device, dtype=torch.long).clone()
             s = torch.cuda.Stream(device=self.device)
+            s.wait_stream(torch.cuda.current_stream(self.device))   # prompt / state writes queued before us
             with torch.cuda.stream(s):
                 self._prefill_body(buf)   # warm-up outside capture (workspaces, lazy set-up)
                 s.synchronize()
@@ -292,8 +300,10 @@ class TernaryDecoder:
 
     def capture(self) -> None:
         """Capture one greedy decode step (state advanced on the device) as a CUDA graph."""
+        cur = torch.cuda.current_stream(self.device)
         s = torch.cuda.Stream(device=self.device)
         saved = (self.tok.clone(), self.pos.clone(), self.k_cache.clone(), self.v_cache.clone(), self.h0.clone())
+        s.wait_stream(cur)   # a queued prefill (and the clones above) complete before the warm-up step
         with torch.cuda.stream(s):
             self._decode_body()   # warm-up (lazy kernel set-up) outside capture
             s.synchronize()
@@ -307,6 +317,7 @@ class TernaryDecoder:
                 for _ in range(self.STEPS_PER_GRAPH):
                     self._decode_body()
         torch.cuda.synchronize(self.device)
+        cur.wait_stream(s)
         self.tok.copy_(saved[0])
         self.pos.copy_(saved[1])
         self.k_cache.copy_(saved[2])
@@ -314,15 +325,22 @@ class TernaryDecoder:
         self.h0.copy_(saved[4])
 
     def decode(self, n: int) -> None:
-        """n greedy decode steps as n graph replays (no host synchronisation)."""
+        """n greedy decode steps as n graph replays (no host synchronisation).
+
+        The position is tracked on the host too: stepping past ``cfg.max_seq`` raises instead of
+        writing past the KV cache (the kernels also refuse rows >= max_seq)."""
+        if self._host_pos + n > self.cfg.max_seq:
+            raise ValueError(f"decode({n}) from position {self._host_pos} exceeds max_seq={self.cfg.max_seq}")
         if self.graph is None:
             self.capture()
         for _ in range(n // self.STEPS_PER_GRAPH):
             self.graph_multi.replay()
         for _ in range(n % self.STEPS_PER_GRAPH):
             self.graph.replay()
+        self._host_pos += n
 
     def reset(self) -> None:
+        self._host_pos = 0
         self.k_cache.zero_()
         self.v_cache.zero_()
         self.tok.zero_()

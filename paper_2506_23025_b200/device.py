@@ -132,7 +132,7 @@ _PATHS = {"auto": 0, "umma": _lib.LINEAR_FORCE_UMMA, "gemv": _lib.LINEAR_FORCE_G
 
 def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, pdl: bool = False,
            ctas: int = 0, ws: torch.Tensor | None = None, path: str = "auto", ksplit: int = 0,
-           cosched: bool = False, epi_swiglu: bool = False, _probe: int = 0) -> torch.Tensor:
+           cosched: bool = False, epi_swiglu: bool = False, out_dtype=None, _probe: int = 0) -> torch.Tensor:
     """y[..., rows] = x[..., cols] @ W^T for fp16/bf16 x on the GPU (TriRun hot path).
 
     Accumulation is fp32: per 256-block partial sums are scaled by the block's
@@ -146,6 +146,8 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
     int8-slice GEMV then runs as half-SM CTAs so the next layer co-resides and prefetches.
     ``epi_swiglu`` (TR_LINEAR_EPI_SWIGLU): W is a gate|up weight with 16-row tiles alternating
     gate / up (``interleave_gate_up``); the result is silu(gate) * up, rows // 2 wide.
+    ``out_dtype=torch.float32`` (TR_LINEAR_OUT_F32) returns the fp32 accumulators unrounded --
+    the row-parallel partials an all-reduce sums (parallel.RowParallelTernaryLinear).
     """
     if x.dtype not in _ACT:
         raise TypeError(f"activations must be float16 or bfloat16, got {x.dtype}")
@@ -164,11 +166,20 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
         x2 = xp[:, : w.cols]
     batch = x2.shape[0]
     rows_out = w.rows // 2 if epi_swiglu else w.rows
+    odt = x.dtype if out_dtype is None else out_dtype
+    if odt not in (x.dtype, torch.float32):
+        raise TypeError(f"out_dtype must be the activation dtype or float32, got {odt}")
     if out is None:
-        out = torch.empty((*lead, rows_out), dtype=x.dtype, device=x.device)
+        out = torch.empty((*lead, rows_out), dtype=odt, device=x.device)
+    elif out.dtype != odt:
+        raise TypeError(f"out has dtype {out.dtype}, expected {odt}")
     y2 = out.view(-1, rows_out)
     flags = (_lib.LINEAR_PDL if pdl else 0) | (_lib.LINEAR_UNIFORM_SCALE if w.uniform_scale else 0) | _PATHS[path]
+    if odt == torch.float32:
+        flags |= _lib.LINEAR_OUT_F32
     if epi_swiglu:
+        if w.fmt != DType.TQ2 or batch > 4 or path not in ("auto", "gemv"):
+            raise ValueError("the SwiGLU epilogue runs on the int8-slice GEMV only (TQ2, batch <= 4)")
         flags |= _lib.LINEAR_EPI_SWIGLU
     if cosched:   # back-to-back GEMV chain: half-SM CTAs so consecutive layers co-reside
         flags |= _lib.LINEAR_COSCHEDULE

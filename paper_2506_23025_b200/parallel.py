@@ -28,16 +28,24 @@ from .blocks import BLOCK_ELEMENTS
 from .packed_linear import PackedMatrix
 
 
-def shard_bounds(n: int, parts: int, index: int) -> tuple[int, int]:
-    """[lo, hi) of the index-th of `parts` near-equal contiguous pieces of range(n)."""
+def shard_bounds(n: int, parts: int, index: int, align: int = 1) -> tuple[int, int]:
+    """[lo, hi) of the index-th of `parts` near-equal contiguous pieces of range(n), cut on
+    multiples of `align` (the last piece takes the remainder)."""
     if not 0 <= index < parts:
         raise ValueError(f"shard index {index} out of range for {parts} parts")
-    return (n * index) // parts, (n * (index + 1)) // parts
+    if align < 1:
+        raise ValueError(f"align must be >= 1, got {align}")
+    units = -(-n // align)
+    lo, hi = (units * index) // parts * align, (units * (index + 1)) // parts * align
+    return min(lo, n), min(hi, n)
 
 
-def shard_rows(pm: PackedMatrix, parts: int, index: int) -> PackedMatrix:
-    """Column-parallel shard: output rows [r0, r1) (exact slice of the packed arrays)."""
-    r0, r1 = shard_bounds(pm.rows, parts, index)
+def shard_rows(pm: PackedMatrix, parts: int, index: int, align: int = 1) -> PackedMatrix:
+    """Column-parallel shard: output rows [r0, r1) (exact slice of the packed arrays).
+
+    ``align=BLOCK_ELEMENTS`` cuts on 256-row boundaries, so the shard's outputs are exactly the
+    256-blocks of K a following RowParallelTernaryLinear (shard_cols) owns on the same rank."""
+    r0, r1 = shard_bounds(pm.rows, parts, index, align)
     if r1 <= r0:
         raise ValueError(f"{pm.rows} rows cannot be split into {parts} non-empty shards")
     return PackedMatrix(rows=r1 - r0, cols=pm.cols, fmt=pm.fmt, payload=np.array(pm.payload[r0:r1]),
@@ -70,14 +78,16 @@ def _dist():
 class ColumnParallelTernaryLinear:
     """y[:, r0:r1] = x @ W[r0:r1]^T on this rank; optionally all-gathered to the full y."""
 
-    def __init__(self, pm: PackedMatrix, group=None, linear_fn=None, to_device=True):
+    def __init__(self, pm: PackedMatrix, group=None, linear_fn=None, to_device=True, align: int = 1):
+        """``align=BLOCK_ELEMENTS`` when the output feeds a RowParallelTernaryLinear (x_local = y)."""
         dist = _dist()
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.rows, self.cols = pm.rows, pm.cols
-        self.r0, self.r1 = shard_bounds(pm.rows, self.world, self.rank)
-        self.shard = shard_rows(pm, self.world, self.rank)
+        self.align = align
+        self.r0, self.r1 = shard_bounds(pm.rows, self.world, self.rank, align)
+        self.shard = shard_rows(pm, self.world, self.rank, align)
         self.weight = self.shard.to_device() if to_device else self.shard
         self.linear_fn = linear_fn
 
@@ -96,7 +106,7 @@ class ColumnParallelTernaryLinear:
 
         dist = _dist()
         # collectives need equal-sized pieces: pad every rank's rows to the largest shard
-        bounds = [shard_bounds(self.rows, self.world, i) for i in range(self.world)]
+        bounds = [shard_bounds(self.rows, self.world, i, self.align) for i in range(self.world)]
         width = max(hi - lo for lo, hi in bounds)
         pad = torch.zeros((*y.shape[:-1], width), dtype=y.dtype, device=y.device)
         pad[..., : y.shape[-1]] = y
@@ -108,7 +118,13 @@ class ColumnParallelTernaryLinear:
 
 
 class RowParallelTernaryLinear:
-    """y = sum over ranks of x[:, c0:c1] @ W[:, c0:c1]^T -- one all-reduce after the local product."""
+    """y = sum over ranks of x[:, c0:c1] @ W[:, c0:c1]^T -- one all-reduce after the local product.
+
+    The local product keeps its fp32 accumulators (TR_LINEAR_OUT_F32) and the all-reduce sums
+    fp32 partials; the sum is rounded once to the activation dtype.  With
+    ``fp32_partials=False`` each partial is rounded to fp16/bf16 first (half the bytes on the
+    wire, one extra rounding per rank: relative error up to world * 2^-11 for fp16).
+    """
 
     def __init__(self, pm: PackedMatrix, group=None, linear_fn=None, to_device=True):
         dist = _dist()
@@ -120,16 +136,24 @@ class RowParallelTernaryLinear:
         self.weight = self.shard.to_device() if to_device else self.shard
         self.linear_fn = linear_fn
 
-    def forward(self, x_local, allreduce: bool = True):
-        """x_local: this rank's columns [..., c1 - c0] (e.g. a column-parallel layer's output)."""
+    def forward(self, x_local, allreduce: bool = True, fp32_partials: bool = True):
+        """x_local: this rank's columns [..., c1 - c0] (e.g. the output of a column-parallel layer
+        built with ``align=BLOCK_ELEMENTS``)."""
+        import torch
+
+        if x_local.shape[-1] != self.c1 - self.c0:
+            raise ValueError(f"rank {self.rank} owns columns [{self.c0}, {self.c1}) "
+                             f"({self.c1 - self.c0} wide), got activations {tuple(x_local.shape)}")
         if self.linear_fn is not None:
             y = self.linear_fn(x_local, self.weight)
+            if fp32_partials:
+                y = y.float()
         else:
             from .device import linear
 
-            y = linear(x_local, self.weight)
+            y = linear(x_local, self.weight, out_dtype=torch.float32 if fp32_partials else None)
         if allreduce and self.world > 1:
             _dist().all_reduce(y, group=self.group)
-        return y
+        return y.to(x_local.dtype) if fp32_partials else y
 
     __call__ = forward

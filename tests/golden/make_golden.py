@@ -101,7 +101,39 @@ def main() -> None:
             if rows * cols <= 20000:
                 cases[key + "_dense"] = dequantize_matrix(pm, dtype=np.float32)
     np.savez_compressed(os.path.join(OUT, "linear.npz"), **cases)
+    make_ternarize()
     print("wrote", sorted(f for f in os.listdir(OUT) if f.endswith(".npz")))
+
+
+def make_ternarize() -> None:
+    """ternarize (blocks.py:220-236): gamma = eps + mean|W| (numpy's pairwise float64 sum) and
+    the trits, on shapes whose mean needs many partial sums (so the reduction order shows)."""
+    sys.path.insert(0, REF_SRC)
+    from tritpack.blocks import ternarize
+
+    rng = np.random.default_rng(220)
+    mats = {
+        "normal_96x517": rng.normal(size=(96, 517)),
+        "uniform_f32_65x257": rng.uniform(-3, 3, size=(65, 257)).astype(np.float32),
+        "lognormal_8x4099": rng.lognormal(size=(8, 4099)) * rng.choice([-1.0, 1.0], size=(8, 4099)),
+        "int_valued_31x33": rng.integers(-4, 5, size=(31, 33)).astype(np.float64),
+        "zeros_4x4": np.zeros((4, 4)),
+        "tiny_2x3": np.array([[1e-300, -1e-300, 0.0], [5e-6, -5e-6, 1e-5]]),
+    }
+    out = {}
+    for name, W in mats.items():
+        for eps in (1e-5, 0.25):
+            r = ternarize(W, epsilon=eps)
+            key = f"{name}_eps{eps:g}"
+            out[key + "_W"] = W
+            out[key + "_gamma"] = np.float64(r.gamma)
+            out[key + "_trits"] = r.trits
+    np.savez_compressed(os.path.join(OUT, "ternarize.npz"), **out)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ternarize":
+    make_ternarize()
+    sys.exit(0)
 
 
 if __name__ == "__main__":

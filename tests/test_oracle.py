@@ -10,6 +10,8 @@ Plus the reference's own hand-written golden vectors (test_codec.py:36-47,
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -92,6 +94,23 @@ def test_pack_gemm_reference_match_golden(golden, fmt, rows, cols):
     if key + "_dense" in g:
         dense = orc.dequantize_matrix(payload, scales, cols, FMTS[fmt], np.float32)
         np.testing.assert_array_equal(dense, g[key + "_dense"])
+    # the streaming float64 product used at full BASELINE sizes agrees with gemv_reference
+    refb = orc.gemv_reference_batch(payload, scales, cols, FMTS[fmt], g[key + "_X"], threads=2)
+    np.testing.assert_allclose(refb, g[key + "_ref"], rtol=1e-12, atol=1e-12 * np.abs(g[key + "_ref"]).max())
+
+
+def test_ternarize_golden_is_numpy_pairwise_mean():
+    """tests/golden/ternarize.npz (reference ternarize, blocks.py:220-236): gamma is eps + numpy's
+    pairwise mean, the rule the product's host-side gamma follows."""
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "ternarize.npz"))
+    keys = sorted(k[:-2] for k in g.files if k.endswith("_W"))
+    assert len(keys) == 12
+    for k in keys:
+        eps = float(k.rsplit("_eps", 1)[1])
+        W = np.asarray(g[k + "_W"], np.float64)
+        assert float(g[k + "_gamma"]) == eps + float(np.mean(np.abs(W)))
+        q = np.clip(W / float(g[k + "_gamma"]), -1.0, 1.0)
+        np.testing.assert_array_equal((q >= 0.5).astype(np.int8) - (q <= -0.5).astype(np.int8), g[k + "_trits"])
 
 
 ref_kernels = orc.ref_kernels()

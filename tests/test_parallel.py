@@ -86,6 +86,54 @@ def test_tp_gloo_world2():
         np.testing.assert_allclose(y_row, ref, rtol=1e-5, atol=1e-4)   # block-sum order differs
 
 
+def _chain_worker(rank, world, port, q):
+    """column-parallel (align=256) -> row-parallel with fp32 partials, the 70B MLP pattern."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2506_23025_b200.parallel import ColumnParallelTernaryLinear, RowParallelTernaryLinear
+
+        up, down = _packed(1280, 300, 21), _packed(77, 1280, 22)   # 5 blocks of 256 rows over 2 ranks
+        x = torch.from_numpy(np.random.default_rng(23).uniform(-1, 1, size=(2, 300)).astype(np.float32))
+        col = ColumnParallelTernaryLinear(up, linear_fn=_oracle_linear, to_device=False, align=256)
+        row = RowParallelTernaryLinear(down, linear_fn=_oracle_linear, to_device=False)
+        h = col(x)
+        assert (col.r0, col.r1) == (row.c0, row.c1)   # the column shard's outputs are the row shard's K
+        y = row(h.half().float())   # activations between the layers as the GPU path carries them
+        y16 = row(h.half(), fp32_partials=False)
+        q.put((rank, col.r0, col.r1, y.numpy(), y16.float().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_tp_gloo_world2_column_to_row_chain():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chain_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [(r0, r1) for _, r0, r1, _, _ in res] == [(0, 512), (512, 1280)]
+    up, down = _packed(1280, 300, 21), _packed(77, 1280, 22)
+    x = np.random.default_rng(23).uniform(-1, 1, size=(2, 300)).astype(np.float32)
+    h = orc.gemm(up.payload, up.scales, 300, orc.TQ2, x).astype(np.float16).astype(np.float32)
+    ref = orc.gemm(down.payload, down.scales, 1280, orc.TQ2, h).astype(np.float64)
+    for _, _, _, y, y16 in res:
+        np.testing.assert_array_equal(y, res[0][3])   # every rank holds the same all-reduced sum
+        den = np.abs(ref).max(axis=1)
+        assert (np.abs(y - ref).max(axis=1) / den).max() <= 1e-6     # fp32 partials: fp32 accuracy
+        assert (np.abs(y16 - ref).max(axis=1) / den).max() <= 2e-3   # fp16 partials: stated fp16 error
+
+
 def test_shard_geometry():
     from paper_2506_23025_b200.parallel import shard_bounds, shard_cols, shard_rows
 
@@ -97,6 +145,10 @@ def test_shard_geometry():
         rows = [shard_rows(pm, tp_ if tp_ <= 10 else 10, i) for i in range(tp_)]
         assert sum(s.rows for s in rows) == 10
     assert shard_bounds(28672, 8, 7) == (25088, 28672)
+    # 256-aligned row shards line up with the row-parallel block shards (d_ff 9216, TP 8)
+    assert [shard_bounds(9216, 8, i, 256) for i in (0, 7)] == [(0, 1024), (7936, 9216)]
+    assert [shard_bounds(9216, 8, i, 256)[1] - shard_bounds(9216, 8, i, 256)[0] for i in range(8)] == \
+        [(shard_bounds(36, 8, i)[1] - shard_bounds(36, 8, i)[0]) * 256 for i in range(8)]
     with pytest.raises(ValueError):
         shard_rows(_packed(2, 256, 1), 4, 0)
 
