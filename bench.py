@@ -50,8 +50,9 @@ def parse():
     p.add_argument("--replicas", type=int, default=32)
     p.add_argument("--sweep", default="1,2,4,8,16,32,64,128")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
-    p.add_argument("--extras", default="decode,tq1,tp70b",
-                   help="extra sections on rank 0 at N=1: decode (configs[2]), tq1 (configs[3]), tp70b (configs[4])")
+    p.add_argument("--extras", default="decode,tq1,tp70b,boundary",
+                   help="extra sections on rank 0 at N=1: decode (configs[2]), tq1 (configs[3]), tp70b (configs[4]), "
+                        "boundary (the unmodified reference's linear.gemm on backend 'cuda', configs[0])")
     return p.parse_args()
 
 
@@ -223,12 +224,21 @@ def timed_graph(replay, steps, warmup, dist):
     return ms
 
 
+def uniform_x(batch, cols, seed, dtype=None):
+    """The timed activations: seeded U(-1, 1) (perf.py:91), rounded to fp16."""
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return (torch.rand((batch, cols), generator=g, device="cuda") * 2 - 1).to(dtype or torch.float16)
+
+
 def dense_stack(weights, batch):
-    """PyTorch fp16 (cuBLAS) baseline on the dequantized weights of the same stack, CUDA-graphed."""
+    """PyTorch fp16 (cuBLAS) baseline on the dequantized weights of the same stack, CUDA-graphed,
+    on the same seeded U(-1, 1) activations as the ternary stack."""
     import torch
 
     dws = [w.dequantize(torch.float16) for w in weights]
-    x = torch.zeros((batch, dws[0].shape[1]), dtype=torch.float16, device="cuda")
+    x = uniform_x(batch, dws[0].shape[1], 4242 + batch)
     s = torch.cuda.Stream()
     g = torch.cuda.CUDAGraph()
 
@@ -264,6 +274,50 @@ def _time_layers(ws, x, path="auto", reps=10):
     return timed_graph(g.replay, reps, 3, None) / reps / len(ws)
 
 
+def run_boundary():
+    """configs[0] through the reference's own API: the UNMODIFIED tritpack (baseline/_ref) with this
+    repo's kernel module registered as backend "cuda", linear.gemm(pm, X) from host
+    numpy and back, synchronous, per call -- next to the reference's compiled CPU backend."""
+    import numpy as np
+
+    ref_root = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_root, "tritpack")):
+        return {"unavailable": "reference not installed in baseline/_ref"}
+    sys.path.insert(0, ref_root)
+    from tritpack import backend
+    from tritpack import linear as rl
+    from tritpack.blocks import DType as RD
+
+    from paper_2506_23025_b200 import cuda_kernels
+
+    backend._BY_NAME["cuda"] = cuda_kernels
+    rng = np.random.default_rng(0)
+    T = (rng.integers(0, 3, size=(4096, 4096)) - 1).astype(np.float32)
+    gam = np.float16(0.02 * (1 + rng.uniform(0, 1, size=(4096, 1)))).astype(np.float32)
+    pm = rl.pack_matrix(gam * T, RD.TQ2, backend="compiled")
+    X = np.float16(rng.uniform(-1, 1, size=(1, 4096))).astype(np.float32)
+    nbytes = pm.weight_bytes + X.nbytes + 4096 * 4
+    res = {"shape": "4096x4096", "batch": 1, "format": "TQ2", "api": "tritpack.linear.gemm(pm, X, threads, backend)",
+           "bytes_per_call": nbytes}
+    ncpu = os.cpu_count() or 1
+    for name, be, threads, reps in (("cuda_1thread", "cuda", 1, 50), ("cuda_threads", "cuda", ncpu, 50),
+                                    ("compiled_cpu_threads", "compiled", ncpu, 8)):
+        for _ in range(2):
+            y = rl.gemm(pm, X, threads=threads, backend=be)
+        times = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            y = rl.gemm(pm, X, threads=threads, backend=be)
+            times.append(time.perf_counter() - t0)
+        med = statistics.median(times)
+        res[name] = {"threads": threads, "us_per_call": round(med * 1e6, 1), "gbs": round(nbytes / med / 1e9, 3)}
+        res.setdefault("outputs", []).append(y)
+    a, b, c = res.pop("outputs")
+    res["bit_identical_cuda_vs_compiled"] = bool(np.array_equal(a.view(np.uint32), c.view(np.uint32)) and
+                                                 np.array_equal(b.view(np.uint32), c.view(np.uint32)))
+    return res
+
+
 def run_extras(args, stack_ws):
     """configs[2] decode tokens/s, configs[3] TQ1 8192^2, configs[4] 70B layer shapes (1 GPU + TP shards)."""
     import torch
@@ -273,6 +327,8 @@ def run_extras(args, stack_ws):
     want = set(args.extras.split(","))
     del stack_ws
     torch.cuda.empty_cache()
+    if "boundary" in want:
+        out["reference_boundary_4096sq"] = run_boundary()
     if "tq1" in want:   # 1.6-bit weights decoded on the fly (tcgen05 path), next to TQ2 on the same trits
         res = []
         for fmt, bpb in ((tp.DType.TQ1, 54), (tp.DType.TQ2, 66)):
@@ -355,6 +411,7 @@ def run_ours(args, rank, world, dist):
     hbm, tf_burst, tf_sust, peak_kind = peaks()
     ws = make_stack_weights(args.replicas, seed=1234 + rank)
     stack = LinearStack(ws, batch=1)
+    stack.x.copy_(uniform_x(1, stack.x.shape[1], 4242 + 1))   # the graph reads x in place
     nbytes = stack.algorithmic_bytes()
     dev_index = torch.cuda.current_device()
 
@@ -381,6 +438,7 @@ def run_ours(args, rank, world, dist):
     if args.sweep:
         for b in [int(v) for v in args.sweep.split(",") if v]:
             st = LinearStack(ws, batch=b)
+            st.x.copy_(uniform_x(b, st.x.shape[1], 4242 + b))
             t = timed_graph(st.replay, 20, 3, None) / 20
             g, dws = dense_stack(ws, b)
             td = timed_graph(g.replay, 10, 2, None) / 10

@@ -604,6 +604,15 @@ def test_linear_epi_swiglu_rejects_unsupported(tp):
     w = tp.TernaryWeight.from_float(torch.randn(64, 512, generator=g, device="cuda"))
     with pytest.raises(_lib.TriRunError):
         tp.linear(torch.randn(5, 512, generator=g, device="cuda").half(), w, epi_swiglu=True)
+    # batch >= 9 / a forced tensor-core path used to run K5 and write all rows into
+    # the rows/2-wide output; now every non-GEMV path is refused before any launch
+    for b, path in ((16, "auto"), (2, "umma")):
+        out = torch.full((b, 32), 7.0, dtype=torch.float16, device="cuda")
+        with pytest.raises(_lib.TriRunError):
+            tp.linear(torch.randn(b, 512, generator=g, device="cuda").half(), w, out=out, epi_swiglu=True, path=path)
+        assert bool((out == 7.0).all())
+    with pytest.raises(_lib.TriRunError):   # fp32 output does not combine with the epilogue
+        tp.linear(torch.randn(1, 512, generator=g, device="cuda").half(), w, epi_swiglu=True, out_dtype=torch.float32)
 
 
 # ---------------------------------------------------------------- int8-slice GEMV (batch 1-2)
