@@ -132,26 +132,37 @@ TR_API int tr_linear_pre(int fmt, const void* w, const void* x, void* y, int64_t
                          int act_dtype, int64_t ldx, int64_t ldy, int flags, int pre_op, const void* delta,
                          const void* gamma, void* x_out, float eps, void* stream);
 
-/* One product of a chain (tr_linear_chain): y[batch, rows] = x[batch, cols] @ W^T, TQ2 device layout. */
+/* One product of a chain (tr_linear_chain): y[batch, rows] = x_eff[batch, cols] @ W^T, TQ2 device
+ * layout, where x_eff is x or, with pre_op, its fused producer exactly as in tr_linear_pre
+ * (TR_PRE_ADD_RMSNORM: rmsnorm(x + delta) * gamma, x + delta stored to x_out; TR_PRE_SILU_MUL:
+ * silu(x[:, :cols]) * x[:, cols:]).  flags: TR_LINEAR_EPI_SWIGLU (rows are gate/up tile pairs,
+ * y is rows/2 wide) or TR_LINEAR_OUT_F32. */
 typedef struct {
   const void* w;
   const void* x;
   void* y;
   int64_t ldx, ldy, rows, cols;
+  int32_t pre_op;        /* 0, TR_PRE_ADD_RMSNORM or TR_PRE_SILU_MUL */
+  int32_t flags;         /* TR_LINEAR_EPI_SWIGLU | TR_LINEAR_OUT_F32 */
+  const void* delta;     /* TR_PRE_ADD_RMSNORM: added to x (may be NULL) */
+  const void* gamma;     /* TR_PRE_ADD_RMSNORM: norm weight [cols] */
+  void* x_out;           /* TR_PRE_ADD_RMSNORM: receives x + delta (may be NULL) */
+  float eps;
 } TrChainLayer;
 
-/* Bytes of caller-owned device workspace tr_linear_chain needs for n_layers (zero it once:
- * the first 256 bytes hold the grid barrier, which the kernel leaves reset). */
+/* Bytes of caller-owned device workspace tr_linear_chain needs for n_layers (zero it once: the
+ * first 4 KiB hold the per-product arrival counters, which every launch leaves zeroed). */
 TR_API size_t tr_linear_chain_workspace_size(int64_t n_layers);
-/* Upload the chain's layer table into the workspace (synchronous; call once, outside any
- * stream capture, and again whenever a pointer or shape changes). */
+/* Validate the chain and upload its product table into the workspace (synchronous; call once,
+ * outside any stream capture, and again whenever a pointer or shape changes). */
 TR_API int tr_linear_chain_prepare(const TrChainLayer* layers, int64_t n_layers, int64_t batch, void* workspace,
                                    size_t ws_bytes);
-/* A dependent chain of TQ2 products (layer l's x is typically layer l-1's y) for batch 1..8
- * in ONE persistent cooperative launch: a grid barrier between layers, and every warp's TMA
- * weight ring prefetching the next layer's weights across the barrier (weights do not depend
- * on x).  `layers` is the same HOST array given to tr_linear_chain_prepare (used for the
- * launch plan only); graph-capturable. */
+/* A dependent chain of products (layer l reads what layers < l wrote) for batch 1..4 in ONE
+ * persistent launch (K6): one CTA per SM, each warp's TMA weight ring streaming the next
+ * products' weights while the grid waits for a product's inputs; products ordered by arrival
+ * counters in the workspace, not kernel boundaries.  Same arithmetic as tr_linear /
+ * tr_linear_pre on the int8-slice GEMV.  `layers` is the HOST array given to
+ * tr_linear_chain_prepare; graph-capturable.  (up to 256 products) */
 TR_API int tr_linear_chain(int act_dtype, const TrChainLayer* layers, int64_t n_layers, int64_t batch, int flags,
                            void* workspace, size_t ws_bytes, void* stream);
 

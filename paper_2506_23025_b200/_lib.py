@@ -38,10 +38,12 @@ _i64 = ctypes.c_int64
 _int = ctypes.c_int
 
 class TrChainLayer(ctypes.Structure):
-    """include/tritrun.h TrChainLayer: one product of a tr_linear_chain."""
+    """include/tritrun.h TrChainLayer: one product of a tr_linear_chain (with its fused producer)."""
 
     _fields_ = [("w", ctypes.c_void_p), ("x", ctypes.c_void_p), ("y", ctypes.c_void_p), ("ldx", ctypes.c_int64),
-                ("ldy", ctypes.c_int64), ("rows", ctypes.c_int64), ("cols", ctypes.c_int64)]
+                ("ldy", ctypes.c_int64), ("rows", ctypes.c_int64), ("cols", ctypes.c_int64),
+                ("pre_op", ctypes.c_int32), ("flags", ctypes.c_int32), ("delta", ctypes.c_void_p),
+                ("gamma", ctypes.c_void_p), ("x_out", ctypes.c_void_p), ("eps", ctypes.c_float)]
 
 
 _SIGS = {

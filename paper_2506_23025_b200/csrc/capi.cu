@@ -40,9 +40,9 @@ int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t l
               int out_f32);
 size_t umma_workspace_bytes(int batch, int rows, int cols);
 bool gemv_stages_x(int batch, int rows, int cols);
-int gemv_chain(int act, const TrChainLayer* host_layers, void* dev_table, int n_layers, int batch, unsigned* bar,
-               int pdl, cudaStream_t st, bool upload);
-size_t gemv_chain_table_bytes(int n_layers);
+int gemv_chain_s8(int act, const TrChainLayer* host, int n, int batch, void* ws, size_t ws_bytes, int flags,
+                  cudaStream_t st, bool upload);
+size_t chain_workspace_bytes(int n_ops);
 
 // batch at which the tensor-core (tcgen05) GEMM takes over from the mma.sync GEMV
 constexpr int64_t kUmmaMinBatch = 9;
@@ -145,38 +145,22 @@ int tr_linear_pre(int fmt, const void* w, const void* x, void* y, int64_t batch,
 }
 
 size_t tr_linear_chain_workspace_size(int64_t n_layers) {
-  if (n_layers < 1) return 0;
-  return 256 + gemv_chain_table_bytes((int)n_layers);
-}
-
-static int check_chain(const TrChainLayer* layers, int64_t n_layers, void* workspace, size_t ws_bytes) {
-  TR_REQUIRE(n_layers >= 1 && n_layers < (1 << 20), "tr_linear_chain: bad layer count");
-  TR_REQUIRE(workspace != nullptr && ws_bytes >= tr_linear_chain_workspace_size(n_layers),
-             "tr_linear_chain: workspace too small; size it with tr_linear_chain_workspace_size");
-  for (int64_t l = 0; l < n_layers; ++l) {
-    const TrChainLayer& L = layers[l];
-    TR_REQUIRE(L.rows >= 1 && L.cols >= 1 && L.rows < (1LL << 30) && L.cols < (1LL << 30),
-               "tr_linear_chain: layer %lld: bad shape", (long long)l);
-    TR_REQUIRE(L.ldx >= L.cols && L.ldy >= L.rows, "tr_linear_chain: layer %lld: leading dimensions", (long long)l);
-    TR_REQUIRE(((uintptr_t)L.w & 15) == 0, "tr_linear_chain: layer %lld: weights must be 16-byte aligned",
-               (long long)l);
-  }
-  return 0;
+  if (n_layers < 1 || n_layers > 256) return 0;
+  return chain_workspace_bytes((int)n_layers);
 }
 
 int tr_linear_chain_prepare(const TrChainLayer* layers, int64_t n_layers, int64_t batch, void* workspace,
                             size_t ws_bytes) {
-  if (check_chain(layers, n_layers, workspace, ws_bytes)) return -1;
-  return gemv_chain(kActF16, layers, (uint8_t*)workspace + 256, (int)n_layers, (int)batch, (unsigned*)workspace, 0,
-                    nullptr, true);
+  TR_REQUIRE(layers != nullptr && n_layers >= 1 && n_layers <= 256, "tr_linear_chain_prepare: 1..256 layers");
+  return gemv_chain_s8(kActF16, layers, (int)n_layers, (int)batch, workspace, ws_bytes, 0, nullptr, true);
 }
 
 int tr_linear_chain(int act_dtype, const TrChainLayer* layers, int64_t n_layers, int64_t batch, int flags,
                     void* workspace, size_t ws_bytes, void* stream) {
   TR_REQUIRE(act_dtype == kActF16 || act_dtype == kActBf16, "tr_linear_chain: act_dtype must be F16(1) or BF16(2)");
-  if (check_chain(layers, n_layers, workspace, ws_bytes)) return -1;
-  return gemv_chain(act_dtype, layers, (uint8_t*)workspace + 256, (int)n_layers, (int)batch, (unsigned*)workspace,
-                    flags & TR_LINEAR_PDL, (cudaStream_t)stream, false);
+  TR_REQUIRE(layers != nullptr && n_layers >= 1 && n_layers <= 256, "tr_linear_chain: 1..256 layers");
+  return gemv_chain_s8(act_dtype, layers, (int)n_layers, (int)batch, workspace, ws_bytes, flags, (cudaStream_t)stream,
+                       false);
 }
 
 }  // extern "C"

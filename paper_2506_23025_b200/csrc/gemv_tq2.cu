@@ -759,46 +759,5 @@ int gemv_tq2(int act, const void* w, const void* x, void* y, int64_t ldx, int64_
   return bf ? launch_gemv<__nv_bfloat16, 4, 8>(a, grid, pdl, false, st) : launch_gemv<__half, 4, 8>(a, grid, pdl, false, st);
 }
 
-// A chain of products y_l = x_l W_l^T in ONE persistent cooperative launch (batch <= 8):
-// grid barriers between layers, weight prefetch running ahead across them.
-int gemv_chain(int act, const TrChainLayer* host_layers, void* dev_table, int n_layers, int batch, unsigned* bar,
-               int pdl, cudaStream_t st, bool upload) {
-  if (n_layers < 1 || batch < 1 || batch > 8) {
-    set_error("tr_linear_chain: need 1 <= batch <= 8 and at least one layer");
-    return -1;
-  }
-  GemvArgs a = {};
-  a.layers = (const GemvLayer*)dev_table;
-  a.bar = bar;
-  a.n_layers = n_layers;
-  a.batch = batch;
-  a.nb_max = 0;
-  int tiles_min = 1 << 30, ns = 4;
-  std::vector<GemvLayer> tab((size_t)n_layers);
-  const int grid = sm_count();
-  for (int l = 0; l < n_layers; ++l) {
-    const TrChainLayer& h = host_layers[l];
-    tab[l] = make_layer(h.w, h.x, h.y, h.ldx, h.ldy, (int)h.rows, (int)h.cols);
-    if (tab[l].nb > a.nb_max) a.nb_max = tab[l].nb;
-    if (tab[l].n_tiles < tiles_min) tiles_min = tab[l].n_tiles;
-    const int n = gemv_ns<1, 16>(tab[l].n_tiles, tab[l].nb, grid);
-    if (n < ns) ns = n;
-  }
-  a.ns = ns < 2 ? 2 : ns;
-  if (!xs_fits<1, 16>(batch, a.nb_max, a.ns)) a.ns = 1;   // wide activations: a shallower weight ring
-  a.l0 = tab[0];
-  if (upload) {   // synchronous, outside any stream capture (tr_linear_chain_prepare)
-    cudaError_t e = cudaMemcpy(dev_table, tab.data(), sizeof(GemvLayer) * n_layers, cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) {
-      set_error("tr_linear_chain_prepare: table upload failed: %s", cudaGetErrorString(e));
-      return -1;
-    }
-    return 0;
-  }
-  if (act == kActF16) return launch_gemv<__half, 1, 16>(a, grid, pdl, true, st);
-  return launch_gemv<__nv_bfloat16, 1, 16>(a, grid, pdl, true, st);
-}
-
-size_t gemv_chain_table_bytes(int n_layers) { return sizeof(GemvLayer) * (size_t)n_layers; }
 
 }  // namespace tr

@@ -66,6 +66,20 @@ __device__ __noinline__ uint4 s8_load8_slow(const T* row, int64_t k, int cols) {
   for (int e = 0; e < 8; ++e) tmp[e] = (k + e < cols) ? row[k + e] : Act<T>::from_float(0.0f);
   return *reinterpret_cast<uint4*>(tmp);
 }
+// 8 activations through L2 only (ld.global.cg): for data another CTA of the same launch wrote
+// (the persistent chain), where the non-coherent path could return a stale L1 line
+template <typename T>
+__device__ __noinline__ uint4 s8_load8_cg_slow(const T* row, int64_t k, int cols) {
+  T tmp[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) tmp[e] = (k + e < cols) ? __ldcg(row + k + e) : Act<T>::from_float(0.0f);
+  return *reinterpret_cast<uint4*>(tmp);
+}
+template <typename T>
+__device__ __forceinline__ uint4 s8_load8_cg(const T* row, int64_t k, int cols, int vec) {
+  if (vec && k + 8 <= cols) return __ldcg(reinterpret_cast<const uint4*>(row + k));
+  return s8_load8_cg_slow(row, k, cols);
+}
 template <typename T>
 __device__ __forceinline__ uint4 s8_load8(const T* row, int64_t k, int cols, int vec) {
   if (vec && k + 8 <= cols) {

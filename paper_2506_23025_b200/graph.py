@@ -19,14 +19,63 @@ from .blocks import DType
 from .device import _ACT, TernaryWeight, linear
 
 
+class Chain:
+    """A dependent sequence of TQ2 products run as ONE persistent launch (tr_linear_chain, K6).
+
+    ``ops`` are dicts: w (TernaryWeight), x, y (device tensors), and optionally pre
+    (_lib.PRE_ADD_RMSNORM / PRE_SILU_MUL), delta, gamma, x_out, eps, epi_swiglu, out_f32 --
+    the arguments of device.linear / linear_pre.  Up to 256 products, batch 1-4.  The
+    buffers are bound once (the product table lives in the workspace); ``run()`` enqueues
+    one launch on the current stream (graph-capturable).
+    """
+
+    def __init__(self, ops: list[dict], batch: int, dtype=torch.float16):
+        if not 1 <= len(ops) <= 256:
+            raise ValueError("a chain holds 1..256 products")
+        self.ops = ops
+        self.batch = int(batch)
+        self.dtype = dtype
+        table = []
+        for op in ops:
+            w, x, y = op["w"], op["x"], op["y"]
+            if w.fmt is not DType.TQ2:
+                raise ValueError("tr_linear_chain runs TQ2 weights")
+            flags = (_lib.LINEAR_EPI_SWIGLU if op.get("epi_swiglu") else 0) | \
+                    (_lib.LINEAR_OUT_F32 if op.get("out_f32") else 0)
+            ptr = lambda t: 0 if t is None else t.data_ptr()
+            table.append(_lib.TrChainLayer(w.data.data_ptr(), x.data_ptr(), y.data_ptr(), x.stride(0), y.stride(0),
+                                           w.rows, w.cols, int(op.get("pre", 0)), flags, ptr(op.get("delta")),
+                                           ptr(op.get("gamma")), ptr(op.get("x_out")), float(op.get("eps", 1e-5))))
+        self._table = (_lib.TrChainLayer * len(table))(*table)
+        dev = ops[0]["w"].data.device
+        need = _lib.lib().tr_linear_chain_workspace_size(len(table))
+        self._ws = torch.zeros(need, dtype=torch.uint8, device=dev)
+        torch.cuda.synchronize(dev)
+        _lib.call_nostream("tr_linear_chain_prepare", self._table, len(table), self.batch, self._ws.data_ptr(),
+                           self._ws.numel())
+
+    def run(self, pdl: bool = True, probe: int = 0) -> None:
+        _lib.call("tr_linear_chain", _ACT[self.dtype], self._table, len(self.ops), self.batch,
+                  (_lib.LINEAR_PDL if pdl else 0) | ((probe & 0xF) << 24), self._ws.data_ptr(), self._ws.numel(),
+                  _lib.stream_handle())
+
+    def trace(self) -> torch.Tensor:
+        """Development probe (run(probe=2)): int64 %globaltimer stamps [n_ops, n_ctas, 4] =
+        (op start, inputs ready, staged, stored)."""
+        n = len(self.ops)
+        sms = torch.cuda.get_device_properties(self._ws.device).multi_processor_count
+        tab = 4096 + 104 * n + 16 * n   # (counters | ChainOp 104 B each | ChainW 16 B each)
+        off = (tab + 255) // 256 * 256
+        return self._ws[off: off + n * sms * 32].view(torch.int64).view(n, sms, 4)
+
+
 class LinearStack:
     """y = W_{n-1}( ... W_1(W_0 x)) over TernaryWeights, replayed from one CUDA graph.
 
-    Default: one PDL-chained tr_linear per layer (GEMV or tcgen05 GEMM by batch).
-    ``chain=True`` (batch <= 8, TQ2) runs the whole stack as ONE persistent cooperative
-    launch instead (tr_linear_chain: grid barriers between layers, weights prefetched
-    across them) -- measured slower than the PDL chain in round 1 (11.4 vs 8.1 us per
-    layer on the bench stack), so it is opt-in.
+    ``chain=True`` (batch <= 4, TQ2, <= 256 layers): the whole stack is ONE persistent launch
+    (K6, tr_linear_chain) -- weights stream across layer boundaries while the grid waits for
+    each layer's input.  Otherwise one PDL-chained tr_linear per layer (GEMV or tcgen05 GEMM
+    by batch).  ``chain=None`` picks the chain whenever it applies.
     """
 
     def __init__(self, weights: list[TernaryWeight], batch: int, dtype=torch.float16, pdl: bool = True,
@@ -43,32 +92,24 @@ class LinearStack:
         dev = weights[0].data.device
         self.x = torch.zeros((self.batch, weights[0].cols), dtype=dtype, device=dev)
         self.bufs = [torch.empty((self.batch, w.rows), dtype=dtype, device=dev) for w in weights]
-        if chain is None:
-            chain = False
-        chain = chain and self.batch <= 8 and all(w.fmt is DType.TQ2 for w in weights)
-        self.chain = chain
-        if chain:
-            table = []
-            cur = self.x
+        ok = 1 <= self.batch <= 4 and len(weights) <= 256 and all(w.fmt is DType.TQ2 for w in weights)
+        self.chain = ok if chain is None else (bool(chain) and ok)
+        self._chain = None
+        if self.chain:
+            ops, cur = [], self.x
             for w, out in zip(weights, self.bufs):
-                table.append(_lib.TrChainLayer(w.data.data_ptr(), cur.data_ptr(), out.data_ptr(), cur.stride(0),
-                                               out.stride(0), w.rows, w.cols))
+                ops.append({"w": w, "x": cur, "y": out})
                 cur = out
-            self._table = (_lib.TrChainLayer * len(table))(*table)
-            need = _lib.lib().tr_linear_chain_workspace_size(len(table))
-            self._ws = torch.zeros(need, dtype=torch.uint8, device=dev)
-            _lib.call_nostream("tr_linear_chain_prepare", self._table, len(table), self.batch, self._ws.data_ptr(),
-                               self._ws.numel())
+            try:
+                self._chain = Chain(ops, self.batch, dtype)
+            except _lib.TriRunError:
+                if chain:
+                    raise
+                self.chain = False   # e.g. activations too wide to stage next to the rings
         self.stream = torch.cuda.Stream(device=dev)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.stream(self.stream):
-            try:
-                self._body()                  # warm-up (lazy kernel attribute setup) outside capture
-            except _lib.TriRunError:
-                if not self.chain:
-                    raise
-                self.chain = False            # e.g. activations too wide to stage: per-layer launches
-                self._body()
+            self._body()                      # warm-up (lazy kernel attribute setup) outside capture
             self.stream.synchronize()
             with torch.cuda.graph(self.graph, stream=self.stream):
                 self._body()
@@ -76,8 +117,7 @@ class LinearStack:
 
     def _body(self) -> None:
         if self.chain:
-            _lib.call("tr_linear_chain", _ACT[self.dtype], self._table, len(self.weights), self.batch,
-                      _lib.LINEAR_PDL if self.pdl else 0, self._ws.data_ptr(), self._ws.numel(), _lib.stream_handle())
+            self._chain.run(pdl=self.pdl)
             return
         cur = self.x
         for w, out in zip(self.weights, self.bufs):

@@ -475,9 +475,10 @@ def test_tq1_matches_tq2_same_trits(tp):
 
 # ---------------------------------------------------------------- persistent chain (tr_linear_chain)
 
-@pytest.mark.parametrize("batch", [1, 3, 8])
+@pytest.mark.parametrize("batch", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
 def test_linear_chain_matches_per_layer(tp, batch, dtype):
+    """K6 (one persistent launch) vs one tr_linear per layer, on the BASELINE shapes plus ragged ones."""
     from paper_2506_23025_b200.graph import LinearStack
 
     tdt = getattr(torch, dtype)
@@ -485,21 +486,96 @@ def test_linear_chain_matches_per_layer(tp, batch, dtype):
     shapes = [(4096, 4096), (11008, 4096), (4096, 11008), (300, 4096), (4096, 300), (1000, 4096)]
     ws = [tp.TernaryWeight.from_float(torch.randn(r, c, generator=g, device="cuda") * 0.01) for r, c in shapes]
     x = (torch.rand(batch, 4096, generator=g, device="cuda") * 2 - 1).to(tdt)
-    st = LinearStack(ws, batch=batch, dtype=tdt, chain=True)
-    assert st.chain or batch > 4   # batch 8 x 11008 columns is too wide to stage: per-layer fallback
+    st = LinearStack(ws, batch=batch, dtype=tdt)
+    assert st.chain == (batch <= 4)
     st.x.copy_(x)
     st.replay()
-    st.replay()   # twice: the grid barrier resets itself between launches
+    first = st.out.clone()
+    st.replay()   # again: the arrival counters re-zero themselves at the end of every launch
+    torch.cuda.synchronize()
+    assert torch.equal(first, st.out)
     ref = x
     for w in ws:
-        # the chain runs the fp16 mma.sync GEMV; the per-layer fallback the automatic path
-        ref = tp.linear(ref, w, path="gemv_f16" if st.chain else "auto")
+        ref = tp.linear(ref, w)
+    # same arithmetic; the per-layer launches split boundary tiles between warps differently,
+    # so fp32 partial sums round differently (then propagate through six layers)
+    err = ((st.out.float() - ref.float()).abs().amax(1) / ref.float().abs().amax(1)).max().item()
+    assert err <= (1e-2 if dtype == "float16" else 3e-2), err
+
+
+@pytest.mark.parametrize("batch", [1, 2, 3, 4])
+def test_linear_chain_one_layer_bitwise_vs_gemv(tp, batch):
+    """With the same partition (148 CTAs x 16 warps) a one-product chain is K3-S8 bit for bit."""
+    from paper_2506_23025_b200.graph import Chain
+
+    g = torch.Generator(device="cuda").manual_seed(40 + batch)
+    for rows, cols in ((4096, 4096), (11008, 4096), (4096, 11008)):
+        w = tp.TernaryWeight.from_float(torch.randn(rows, cols, generator=g, device="cuda"))
+        x = (torch.rand(batch, cols, generator=g, device="cuda") * 2 - 1).half()
+        y = torch.empty(batch, rows, dtype=torch.float16, device="cuda")
+        ch = Chain([{"w": w, "x": x, "y": y}], batch)
+        ch.run()
+        ref = tp.linear(x, w, ctas=148 | (1 << 12))   # knob: 148 CTAs, dev bit 0 = the 16-warp variant
+        torch.cuda.synchronize()
+        assert torch.equal(y, ref), (rows, cols)
+
+
+@pytest.mark.parametrize("batch", [1, 3])
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
+def test_linear_chain_decoder_ops(tp, batch, dtype):
+    """A decoder MLP + attention-projection pattern in one chain: add+RMSNorm producer (with the
+    residual store), SwiGLU epilogue, SiLU*up producer, fp32 output -- vs the per-op launches."""
+    from paper_2506_23025_b200 import _lib
+    from paper_2506_23025_b200.device import interleave_gate_up, linear_pre
+    from paper_2506_23025_b200.graph import Chain
+
+    tdt = getattr(torch, dtype)
+    d, f = 1024, 2816
+    g = torch.Generator(device="cuda").manual_seed(7 + batch)
+    rnd = lambda *s: torch.randn(*s, generator=g, device="cuda")
+    Wgu = rnd(2 * f, d) * 0.02
+    w_gu = tp.TernaryWeight.from_float(Wgu)
+    w_gu_il = tp.TernaryWeight.from_float(interleave_gate_up(Wgu, f))
+    w_down = tp.TernaryWeight.from_float(rnd(d, f) * 0.02)
+    w_o = tp.TernaryWeight.from_float(rnd(d, d) * 0.02)
+    h = rnd(batch, d).to(tdt)
+    delta = (rnd(batch, d) * 0.5).to(tdt)
+    gamma = (1 + 0.1 * rnd(d)).to(tdt)
+    # chain: act = swiglu(rmsnorm(h + delta) W_gu^T); down = act W_down^T; gu = rmsnorm(h2 + down) W_gu^T;
+    #        o = silu*up(gu) W_down^T (fp32)
+    h2, act, down, h3, gu = (torch.empty(batch, n, dtype=tdt, device="cuda") for n in (d, f, d, d, 2 * f))
+    o32 = torch.empty(batch, d, dtype=torch.float32, device="cuda")
+    ops = [dict(w=w_gu_il, x=h, y=act, pre=_lib.PRE_ADD_RMSNORM, delta=delta, gamma=gamma, x_out=h2, epi_swiglu=True),
+           dict(w=w_down, x=act, y=down),
+           dict(w=w_gu, x=h2, y=gu, pre=_lib.PRE_ADD_RMSNORM, delta=down, gamma=gamma, x_out=h3),
+           dict(w=w_down, x=gu, y=o32, pre=_lib.PRE_SILU_MUL, out_f32=True)]
+    Chain(ops, batch, tdt).run()
+    r_h2 = torch.empty_like(h2)
+    r_act = linear_pre(h, w_gu_il, _lib.PRE_ADD_RMSNORM, delta, gamma, r_h2, epi_swiglu=True)
+    r_down = tp.linear(r_act, w_down)
+    r_h3 = torch.empty_like(h3)
+    r_gu = linear_pre(r_h2, w_gu, _lib.PRE_ADD_RMSNORM, r_down, gamma, r_h3)
+    r_o = linear_pre(r_gu, w_down, _lib.PRE_SILU_MUL).float()
     torch.cuda.synchronize()
-    assert torch.isfinite(ref).all()
-    # same math; the per-layer launches may pick the 8-warp variant (another warp split of
-    # the boundary tiles), so the comparison is by tolerance
-    a, b = st.out.float(), ref.float()
-    assert ((a - b).abs().amax(1) / b.abs().amax(1)).max().item() <= 5e-3
+    assert torch.equal(h2, r_h2)   # the residual store is exact (x + delta, rounded once)
+    tol = 1e-2 if dtype == "float16" else 3e-2
+    for a_, b_ in ((act, r_act), (down, r_down), (h3, r_h3), (gu, r_gu), (o32, r_o)):
+        err = ((a_.float() - b_.float()).abs().amax(1) / b_.float().abs().amax(1)).max().item()
+        assert err <= tol, err
+
+
+def test_linear_chain_rejects(tp):
+    from paper_2506_23025_b200 import _lib
+    from paper_2506_23025_b200.graph import Chain
+
+    w = tp.TernaryWeight.from_float(torch.randn(256, 512, device="cuda"))
+    x = torch.randn(8, 512, device="cuda").half()
+    y = torch.empty(8, 256, dtype=torch.float16, device="cuda")
+    with pytest.raises(_lib.TriRunError):   # batch 8: not the int8-slice GEMV
+        Chain([{"w": w, "x": x, "y": y}], 8)
+    with pytest.raises(_lib.TriRunError):   # 48 rows are not whole gate/up tile pairs
+        w48 = tp.TernaryWeight.from_float(torch.randn(48, 512, device="cuda"))
+        Chain([{"w": w48, "x": x[:1], "y": y[:1, :24], "epi_swiglu": True}], 1)
 
 
 @pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
