@@ -19,6 +19,7 @@
 //    CUDA graph with no host work.
 // The kernel never triggers its dependents early (no griddepcontrol.launch_dependents): the
 // next kernel starts after the last CTA exits, which also orders counter reuse.
+#include <algorithm>
 #include <vector>
 
 #include "s8_core.cuh"
@@ -51,27 +52,37 @@ struct ChainArgs {
   const ChainOp* ops;
   const ChainW* wtab;
   unsigned* done;    // [n_ops + 1] arrival counters; zero before a launch, re-zeroed by the last CTA
-  uint64_t* trace;   // development probe: per (op, CTA) 4 %globaltimer stamps, or null
-  int n_ops, batch, ns, nb_max, tv_floats;
+  uint64_t* trace;   // development probe: per (op, CTA) 8 %globaltimer stamps, or null
+  int n_ops, batch, nb_max, tv_floats;
+  size_t ring_bytes;
+  int piece;         // bytes per bulk copy (an op slice is cut into pieces)
+  int probe;         // development probes: 4 = skip the staging arithmetic, 8 = skip the MMAs
 };
 
-constexpr int kChainWarps = 16;
+constexpr int kChainWarps = 15;   // consumer (math) warps; + 1 producer warp = 16: 4 warps per SM sub-partition, 128 registers each
 constexpr int kChainMaxOps = 256;
 constexpr int kChainCounterBytes = 4096;
 
-struct ChainSmem {   // [mbarriers | slot tags | producer table | reduction | -Cs | grid factors | staged x | rings |
-                     //  SwiGLU tiles]
-  size_t tab, red, ncs, fsc, xs, ring, tv, total;
+constexpr int kChainBars = 4;
+constexpr int kChainPiece = 16 * 1024;   // op barriers: ops l, l+1, .. l+3 may be in flight in the ring
+
+struct ChainSmem {   // [op mbarriers | slot tags | op table | CTA tile ranges | op ring bases | reduction | -Cs |
+                     //  grid factors | staged x | weight ring | SwiGLU tiles]
+  size_t tab, rng, red, ncs, fsc, xs, ring, tv, total;
+  size_t ring_bytes;
 };
-__host__ __device__ inline ChainSmem chain_smem(int ng, int nb_max, int nrx, int ns, int tv_floats, int n_ops) {
+__host__ __device__ inline ChainSmem chain_smem(int ng, int nb_max, int nrx, size_t ring_bytes, int tv_floats,
+                                                int n_ops) {
   ChainSmem m;
   m.tab = 1280;
-  m.red = m.tab + (size_t)n_ops * sizeof(ChainW);
+  m.rng = m.tab + (size_t)n_ops * sizeof(ChainW);
+  m.red = (m.rng + (size_t)n_ops * 8 + 15) / 16 * 16;
   m.ncs = m.red + (size_t)2 * kChainWarps * 64 * ng * 4;
   m.fsc = m.ncs + (size_t)nb_max * nrx * 16;
   m.xs = (m.fsc + (size_t)nb_max * nrx * 4 + 127) / 128 * 128;
   m.ring = m.xs + (size_t)nb_max * nrx * kS8ItemBytes;
-  m.tv = m.ring + (size_t)kChainWarps * ns * kS8SU * kUnitBytes;
+  m.ring_bytes = ring_bytes;
+  m.tv = m.ring + ring_bytes;
   m.total = m.tv + (size_t)tv_floats * 4;
   return m;
 }
@@ -88,6 +99,28 @@ __device__ __forceinline__ void chain_range(int n_tiles, int nb, int epi, int wa
   u1 = (int)t0 * nb + (int)((unsigned)((warp + 1) * LL) / kChainWarps);
 }
 
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+
+// the 16 consumer warps synchronise on named barrier 1 (the producer warp never joins)
+__device__ __forceinline__ void consumers_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kChainWarps * 32) : "memory");
+}
+
+__device__ __forceinline__ void cta_tiles(int n_tiles, int epi, unsigned& t0, unsigned& t1) {
+  const unsigned tq = epi ? 2u : 1u, tn = (unsigned)n_tiles / tq;
+  t0 = tq * (blockIdx.x * tn / gridDim.x);
+  t1 = tq * ((blockIdx.x + 1) * tn / gridDim.x);
+}
+
+__device__ __forceinline__ void red_release_gpu_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -97,8 +130,8 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 // Stage op o's activations (its fused producer first) as int8 slices: xs, -Cs, grid factors.
 // Loads of data written inside this launch go through L2 (s8_load8_cg).
 template <typename T>
-__device__ void chain_stage(const ChainOp& o, int nbr, int nrx, int lr, uint8_t* xs, int32_t* ncs, float* fsc,
-                            float* ss_buf) {
+__device__ __forceinline__ void chain_stage(const ChainOp& o, int nbr, int nrx, int lr, uint8_t* xs, int32_t* ncs, float* fsc,
+                            float* ss_buf, uint64_t* tr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nb = o.nb, n_items = nb * nrx;
   const T* xg = reinterpret_cast<const T*>(o.x);
@@ -140,7 +173,7 @@ __device__ void chain_stage(const ChainOp& o, int nbr, int nrx, int lr, uint8_t*
       for (int s = 16; s; s >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, s);
       if (lane == 0) ss_buf[item] = ss;
     }
-    __syncthreads();
+    consumers_sync();
     for (int item = warp; item < n_items; item += kChainWarps) {
       const int kb = item >> lr, br = item & (nrx - 1);
       const int64_t kx = (int64_t)kb * kBlock + lane * 8;
@@ -175,8 +208,9 @@ __device__ void chain_stage(const ChainOp& o, int nbr, int nrx, int lr, uint8_t*
         }
       }
     }
-#pragma unroll 1
-    for (int i = 0; i < 4; i += 2) {
+#pragma unroll
+    for (int i = 0; i < 4; i += 2) {   // (unrolled: va / vb stay in registers)
+      if (i0 + i * kChainWarps >= n_items) break;
       float f[2][8];
       int kbs[2], brs[2];
       int nv = 0;
@@ -188,6 +222,11 @@ __device__ void chain_stage(const ChainOp& o, int nbr, int nrx, int lr, uint8_t*
         brs[t] = it & (nrx - 1);
         nv += item < n_items;
         s8_f8<T>(va[i + t], f[t]);
+        if (tr && i == 0 && t == 0 && threadIdx.x == 0) {   // (dev probe: the first loads have landed)
+          uint64_t ts;
+          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ts) : "r"(__float_as_uint(f[0][0])));
+          tr[6] = ts;
+        }
         if (o.pre == TR_PRE_SILU_MUL) {
           float up[8];
           s8_f8<T>(vb[i + t], up);
@@ -202,100 +241,138 @@ __device__ void chain_stage(const ChainOp& o, int nbr, int nrx, int lr, uint8_t*
 }
 
 template <typename T, int NG>
-__global__ void __launch_bounds__(kChainWarps * 32, 1) k_gemv_chain(const ChainArgs a) {
+__global__ void __launch_bounds__((kChainWarps + 1) * 32, 1) k_gemv_chain(const ChainArgs a) {
   constexpr int NW = kChainWarps;
-  constexpr int kSlotBytes = kS8SU * kUnitBytes;
   extern __shared__ __align__(128) uint8_t smem[];
-  const int NS = a.ns, nbr = a.batch;
+  const int nbr = a.batch;
   const int nrx = NG == 2 ? 4 : nbr, lr = NG == 2 ? 2 : nbr - 1;
-  const ChainSmem L = chain_smem(NG, a.nb_max, nrx, NS, a.tv_floats, a.n_ops);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);   // NW * NS <= 128
-  int* slot_tile = reinterpret_cast<int*>(smem + 1024);   // 2 * NW
+  const ChainSmem L = chain_smem(NG, a.nb_max, nrx, a.ring_bytes, a.tv_floats, a.n_ops);
+  uint64_t* obar = reinterpret_cast<uint64_t*>(smem);            // kChainBars "op slice landed" barriers
+  uint64_t* ebar = obar + kChainBars;                            // kChainBars "op slice consumed" barriers
+  int* ring_base = reinterpret_cast<int*>(smem + 256);           // kChainBars op offsets in the ring
+  ChainOp* opwin = reinterpret_cast<ChainOp*>(smem + 512);       // kChainBars op descriptors (416 B)
+  int* slot_tile = reinterpret_cast<int*>(smem + 1024);          // 2 * NW
   ChainW* wtab = reinterpret_cast<ChainW*>(smem + L.tab);
-  for (int i = threadIdx.x; i < a.n_ops; i += blockDim.x) wtab[i] = a.wtab[i];
-  __syncthreads();
+  uint2* rng = reinterpret_cast<uint2*>(smem + L.rng);           // this CTA's tiles [t0, t1) per op
   float* red = reinterpret_cast<float*>(smem + L.red);
   int32_t* ncs = reinterpret_cast<int32_t*>(smem + L.ncs);
   float* fsc = reinterpret_cast<float*>(smem + L.fsc);
   uint8_t* xs = smem + L.xs;
   uint8_t* ring = smem + L.ring;
   float* tv = reinterpret_cast<float*>(smem + L.tv);
+  const int R = (int)a.ring_bytes;   // a multiple of kUnitBytes: a unit never straddles the wrap
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, c = lane & 3;
   const unsigned G = gridDim.x;
-  uint64_t* mybar = bars + warp * NS;
-  uint8_t* myring = ring + warp * NS * kSlotBytes;
-  auto stamp = [&](int l, int k) {
+  auto stamp = [&](int l, int k) {   // (thread 0)
     if (a.trace && threadIdx.x == 0) {
       uint64_t t;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-      a.trace[((size_t)l * G + blockIdx.x) * 4 + k] = t;
+      a.trace[((size_t)l * G + blockIdx.x) * 16 + k] = t;
     }
   };
-
-  // ---- weight producer (lane 0 of each warp): the warp's units of op 0, op 1, ... in order
-  int pl = 0, pu = 0, pu1 = 0;
-  const uint8_t* pw = nullptr;
-  uint64_t pol = 0;
-  auto producer_seek = [&]() {   // skip to the next op in which this warp owns units
-    while (pu >= pu1 && ++pl < a.n_ops) {
-      const ChainW o = wtab[pl];
-      unsigned t0_, t1_;
-      chain_range(o.n_tiles_epi & 0x3FFFFFFF, o.nb, o.n_tiles_epi >> 30, warp, t0_, t1_, pu, pu1);
-      pw = o.w;
-    }
-  };
-  auto issue = [&](int slot) {
-    if (pl >= a.n_ops) return;
-    const int n = min(kS8SU, pu1 - pu);
-    mbar_expect_tx(&mybar[slot], n * kUnitBytes);
-    bulk_g2s(myring + slot * kSlotBytes, pw + (int64_t)pu * kUnitBytes, n * kUnitBytes, &mybar[slot], pol);
-    pu += n;
-    if (pu >= pu1) producer_seek();
-  };
-  if (lane == 0) {
-    pol = policy_evict_first();
-    for (int s = 0; s < NS; ++s) mbar_init(&mybar[s], 1);
-    mbar_fence_init();
-    const ChainW o0 = wtab[0];
-    unsigned t0_, t1_;
-    chain_range(o0.n_tiles_epi & 0x3FFFFFFF, o0.nb, o0.n_tiles_epi >> 30, warp, t0_, t1_, pu, pu1);
-    pw = o0.w;
-    if (pu >= pu1) producer_seek();
-    for (int s = 0; s < NS; ++s) issue(s);   // weights do not depend on x: before the wait
+  for (int i = threadIdx.x; i < a.n_ops; i += blockDim.x) {
+    const ChainW w = a.wtab[i];
+    wtab[i] = w;
+    unsigned t0, t1;
+    cta_tiles(w.n_tiles_epi & 0x3FFFFFFF, w.n_tiles_epi >> 30, t0, t1);
+    rng[i] = make_uint2(t0, t1);
   }
-  __syncwarp();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kChainBars; ++i) {
+      mbar_init(&obar[i], 1);
+      mbar_init(&ebar[i], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
 
-  int slot = 0;           // consumer ring position (continues across ops)
-  uint32_t phase = 0;
-  int refill = -1;        // slot consumed last, refilled at the next iteration (its loads are done)
+  // ---- weight producer (warp kChainWarps, one lane): op l's CTA slice -- tiles [t0, t1) x all
+  // blocks, ONE contiguous run of the tile-major layout -- as a few large bulk copies (split at
+  // the ring's wrap) into a CTA ring, op after op, as soon as the consumers release ring space.
+  // It never joins the consumers' barriers, so TMA back-pressure never stalls the math warps.
+  auto op_bytes = [&](int l) {
+    const uint2 t = rng[l];
+    return (int)(t.y - t.x) * wtab[l].nb * kUnitBytes;
+  };
+  if (warp == kChainWarps) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int head = 0, used = 0, freed = 0;
+      for (int l = 0; l < a.n_ops; ++l) {
+        const int S = op_bytes(l);
+        while (used + S > R || l - freed >= kChainBars) {   // wait for the oldest slice to be consumed
+          // (polls with back-off: a spinning warp would take issue slots from the math warps of its
+          // sub-partition, and those would then reach every CTA barrier last)
+          while (!mbar_test(&ebar[freed % kChainBars], (uint32_t)(freed / kChainBars) & 1u)) __nanosleep(200);
+          used -= op_bytes(freed);
+          ++freed;
+        }
+        fence_proxy_async_smem();   // (the consumers' reads of the reused bytes precede the copies)
+        uint64_t* bar = &obar[l % kChainBars];
+        ring_base[l % kChainBars] = head;
+        opwin[l % kChainBars] = a.ops[l];   // the descriptor rides on the same barrier as the weights
+        if (a.trace) {   // stamp 7: op l's slice issued
+          uint64_t t;
+          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+          a.trace[((size_t)l * G + blockIdx.x) * 16 + 7] = t;
+        }
+        if (S == 0 || a.piece == 255 * 1024) {   // (dev knob piece 255: no weight traffic at all)
+          mbar_arrive(bar);
+        } else {
+          mbar_expect_tx(bar, (uint32_t)S);
+          const uint8_t* src = wtab[l].w + (size_t)rng[l].x * wtab[l].nb * kUnitBytes;
+          int left = S, h = head;
+          while (left > 0) {
+            const int n = min(min(left, R - h), a.piece);
+            bulk_g2s(ring + h, src, (uint32_t)n, bar, pol);
+            src += n;
+            left -= n;
+            h += n;
+            if (h == R) h = 0;
+          }
+        }
+        head += S;
+        if (head >= R) head -= R;
+        used += S;
+      }
+    }
+    return;   // (the producer warp exits; in-flight copies complete on the consumers' barriers)
+  }
+
   const uint32_t xs_base = smem_u32(xs);
   const float lane_w = (c & 1) ? 65536.0f : 1.0f;
 
   for (int l = 0; l < a.n_ops; ++l) {
-    const ChainOp o = a.ops[l];
-    const int nb = o.nb;
     stamp(l, 0);
+    // op l's descriptor and weight slice (issued by the producer warp well ahead)
+    mbar_wait(&obar[l % kChainBars], (uint32_t)(l / kChainBars) & 1u);
+    const ChainOp o = opwin[l % kChainBars];
+    const int nb = o.nb;
     if (l == 0) {
       griddep_wait();   // the first op's inputs belong to the previous kernel until here
     } else {
-      if (threadIdx.x == 0)
+      if (threadIdx.x == 0 && !(a.probe & 1))   // (dev probe 1: no inter-CTA wait)
         while (ld_acquire_gpu(a.done + (l - 1)) < G) {
         }
-      __syncthreads();   // every CTA has stored op l-1 (and all earlier ops)
+      consumers_sync();   // every CTA has stored op l-1 (and all earlier ops)
     }
     if (lane == 0) {
       slot_tile[2 * warp] = -1;
       slot_tile[2 * warp + 1] = -1;
     }
     stamp(l, 1);
-    chain_stage<T>(o, nbr, nrx, lr, xs, ncs, fsc, red);
-    __syncthreads();
+    if (!(a.probe & 4))
+      chain_stage<T>(o, nbr, nrx, lr, xs, ncs, fsc, red,
+                     a.trace ? a.trace + ((size_t)l * G + blockIdx.x) * 16 : nullptr);
+    consumers_sync();
     stamp(l, 2);
 
-    unsigned t0, t1;
-    int wu0, wu1;
-    chain_range(o.n_tiles, nb, o.epi, warp, t0, t1, wu0, wu1);
+    const uint2 tt = rng[l];
+    const unsigned t0 = tt.x, t1 = tt.y;
+    const int LL = (int)(t1 - t0) * nb;
+    const int wu0 = (int)t0 * nb + (int)((unsigned)(warp * LL) / NW);
+    const int wu1 = (int)t0 * nb + (int)((unsigned)((warp + 1) * LL) / NW);
     uint32_t xsB32[NG];
     const int32_t* ncsD[NG];
     const float* fscD[NG];
@@ -317,9 +394,9 @@ __global__ void __launch_bounds__(kChainWarps * 32, 1) k_gemv_chain(const ChainA
         for (int G2 = 0; G2 < NG; ++G2) {
           const int row = 2 * G2 + (c >> 1);
           if ((c & 1) == 0 && row < nbr) {
-            float* tt = tv + (size_t)(tile - (int)t0) * 64;
-            tt[g * 4 + row] = v[G2][0];
-            tt[(g + 8) * 4 + row] = v[G2][1];
+            float* tp = tv + (size_t)(tile - (int)t0) * 64;
+            tp[g * 4 + row] = v[G2][0];
+            tp[(g + 8) * 4 + row] = v[G2][1];
           }
         }
         return;
@@ -398,33 +475,36 @@ __global__ void __launch_bounds__(kChainWarps * 32, 1) k_gemv_chain(const ChainA
       }
     };
 
+    if (warp == 0) stamp(l, 5);
+    // unit u sits at ring offset base + (u - t0 nb) * 1056 (mod R)
+    int off = ring_base[l % kChainBars] + (wu0 - (int)t0 * nb) * kUnitBytes;
+    if (off >= R) off -= R;
+    const uint32_t wofs0 = t16_word(0, c, g) * 16, wofs1 = t16_word(1, c, g) * 16;
     int kb = wu0 < wu1 ? wu0 - first_tile * nb : 0;
 #pragma unroll 1
     for (int u = wu0; u < wu1;) {
-      if (refill >= 0) {   // the slot read last iteration: its loads completed (values were used)
-        __syncwarp();
-        if (lane == 0) {
-          fence_proxy_async_smem();
-          issue(refill);
-        }
-      }
       const int n = min(kS8SU, wu1 - u);
-      mbar_wait(&mybar[slot], phase);
-      const uint8_t* sp = myring + slot * kSlotBytes;
       uint4 wl[kS8SU], wh[kS8SU];
       uint32_t sv[kS8SU];
 #pragma unroll
       for (int q = 0; q < kS8SU; ++q) {
         if (q < n) {
-          wl[q] = lds128(sp + q * kUnitBytes + t16_word(0, c, g) * 16);
-          wh[q] = lds128(sp + q * kUnitBytes + t16_word(1, c, g) * 16);
-          sv[q] = *reinterpret_cast<const uint32_t*>(sp + q * kUnitBytes + kTileBlockBytes + g * 4);
+          const uint8_t* up = ring + off;
+          wl[q] = lds128(up + wofs0);
+          wh[q] = lds128(up + wofs1);
+          sv[q] = *reinterpret_cast<const uint32_t*>(up + kTileBlockBytes + g * 4);
+          off += kUnitBytes;
+          if (off == R) off = 0;
         }
       }
-      refill = slot;
-      if (++slot == NS) {
-        slot = 0;
-        phase ^= 1u;
+      if (a.probe & 8) {   // (dev probe: weights read, no arithmetic)
+        kb += n;
+        while (kb >= nb) {
+          kb -= nb;
+          ++cur;
+        }
+        u += n;
+        continue;
       }
       if (n == kS8SU && kb + kS8SU <= nb) {   // common case: both units inside the current tile --
         int D0[NG][4], D1[NG][4];             // two independent IMMA chains the scheduler interleaves
@@ -454,18 +534,13 @@ __global__ void __launch_bounds__(kChainWarps * 32, 1) k_gemv_chain(const ChainA
       }
       u += n;
     }
-    if (refill >= 0) {   // hand the last slot back now, not after the next op's input wait
-      __syncwarp();
-      if (lane == 0) {
-        fence_proxy_async_smem();
-        issue(refill);
-      }
-      refill = -1;
-    }
+    if (warp == 0) stamp(l, 4);
     if (cur >= 0) close_tile(cur);
 
     // ---- boundary tiles: combine the parked fragments in fixed (warp, slot) order and store
-    __syncthreads();
+    consumers_sync();
+    stamp(l, 8);
+    if (threadIdx.x == 0) mbar_arrive(&ebar[l % kChainBars]);   // every warp is done with op l's slice
     const int my_tag = lane < 2 * NW ? slot_tile[lane] : -1;
     for (int i = warp; i < 2 * NW; i += NW) {
       const int tile = __shfl_sync(0xffffffffu, my_tag, i);
@@ -486,7 +561,7 @@ __global__ void __launch_bounds__(kChainWarps * 32, 1) k_gemv_chain(const ChainA
       store_tile(tile, v);
     }
     if (o.epi) {   // silu(gate) * up with the roundings of the unfused gate|up store + tr_silu_mul
-      __syncthreads();
+      consumers_sync();
       T* y = reinterpret_cast<T*>(o.y);
       const int npairs = (int)(t1 - t0) / 2, rows_out = o.rows / 2;
       for (int idx = threadIdx.x; idx < npairs * 16 * nbr; idx += NW * 32) {
@@ -497,14 +572,15 @@ __global__ void __launch_bounds__(kChainWarps * 32, 1) k_gemv_chain(const ChainA
         if (orow < rows_out) y[br * o.ldy + orow] = Act<T>::from_float(s8_rnd<T>(__fdividef(gt, 1.0f + __expf(-gt))) * up);
       }
     }
-    __syncthreads();   // all of this CTA's outputs of op l are stored
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(a.done + l, 1u);
-    }
+    stamp(l, 9);
+    consumers_sync();   // all of this CTA's outputs of op l are stored
+    stamp(l, 10);
+    if (threadIdx.x == 0) red_release_gpu_add(a.done + l, 1u);   // (release: the CTA's stores first)
     stamp(l, 3);
   }
-  // the last CTA through re-zeroes the counters (every CTA has finished all its waits)
+  // the last CTA through re-zeroes the counters (every CTA has finished all its waits, and every
+  // warp of this CTA has made its last release: the sync below)
+  consumers_sync();
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(a.done + a.n_ops, 1u) == G - 1) {
@@ -545,37 +621,36 @@ static ChainOp make_op(const TrChainLayer& h) {
 }
 
 struct ChainPlan {
-  int nb_max, ns, tv_floats, ng, nrx;
-  size_t smem;
+  int nb_max, tv_floats, ng, nrx;
+  size_t ring_bytes, smem;
 };
 
-static int chain_plan(const std::vector<ChainOp>& ops, int batch, int grid, ChainPlan& p) {
+// the weight ring gets all shared memory the staged activations leave, in whole units; it must
+// hold the largest per-CTA op slice (an op is one bulk transfer) -- ideally two or more
+static int chain_plan(const std::vector<ChainOp>& ops, int batch, int grid, ChainPlan& p, size_t ring_cap) {
   p.nb_max = 0;
   p.tv_floats = 0;
+  size_t slice_max = 0;
   for (const ChainOp& o : ops) {
     p.nb_max = o.nb > p.nb_max ? o.nb : p.nb_max;
-    if (o.epi) {
-      const int tv = (int)(2 * ceil_div(o.n_tiles / 2, grid) * 64);
-      p.tv_floats = tv > p.tv_floats ? tv : p.tv_floats;
-    }
+    const int tq = o.epi ? 2 : 1;
+    const size_t tiles = (size_t)tq * ceil_div(o.n_tiles / tq, grid);
+    slice_max = std::max(slice_max, tiles * o.nb * kUnitBytes);
+    if (o.epi) p.tv_floats = std::max(p.tv_floats, (int)(tiles * 64));
   }
   p.ng = batch <= 2 ? 1 : 2;
   p.nrx = batch <= 2 ? batch : 4;
   const size_t cap = 227 * 1024;
-  p.ns = 0;
-  for (int ns = 8; ns >= 2; --ns) {
-    const ChainSmem m = chain_smem(p.ng, p.nb_max, p.nrx, ns, p.tv_floats, (int)ops.size());
-    if (m.total <= cap) {
-      p.ns = ns;
-      p.smem = m.total;
-      break;
-    }
-  }
-  if (p.ns == 0) {
-    set_error("tr_linear_chain: activations of %d blocks x batch %d leave no room for the weight rings", p.nb_max,
-              batch);
+  const ChainSmem m0 = chain_smem(p.ng, p.nb_max, p.nrx, 0, p.tv_floats, (int)ops.size());
+  size_t ring = m0.total < cap ? (cap - m0.total) / kUnitBytes * kUnitBytes : 0;
+  if (ring_cap && ring > ring_cap) ring = ring_cap / kUnitBytes * kUnitBytes;
+  if (ring < slice_max) {
+    set_error("tr_linear_chain: a CTA's weight slice (%zu B) does not fit the %zu B ring next to %d staged blocks "
+              "x batch %d", slice_max, ring, p.nb_max, batch);
     return -1;
   }
+  p.ring_bytes = ring;
+  p.smem = m0.total + ring;
   return 0;
 }
 
@@ -583,7 +658,7 @@ static int chain_plan(const std::vector<ChainOp>& ops, int batch, int grid, Chai
 static size_t chain_trace_off(int n_ops) {
   return ((size_t)kChainCounterBytes + (sizeof(ChainOp) + sizeof(ChainW)) * (size_t)n_ops + 255) / 256 * 256;
 }
-size_t chain_workspace_bytes(int n_ops) { return chain_trace_off(n_ops) + (size_t)n_ops * sm_count() * 4 * 8; }
+size_t chain_workspace_bytes(int n_ops) { return chain_trace_off(n_ops) + (size_t)n_ops * sm_count() * 16 * 8; }
 
 static int check_ops(const TrChainLayer* h, int n, int batch) {
   TR_REQUIRE(n >= 1 && n <= kChainMaxOps, "tr_linear_chain: 1 <= n_layers <= %d", kChainMaxOps);
@@ -615,7 +690,7 @@ int gemv_chain_s8(int act, const TrChainLayer* host, int n, int batch, void* ws,
   for (int l = 0; l < n; ++l) ops[l] = make_op(host[l]);
   const int grid = sm_count();
   ChainPlan p;
-  if (chain_plan(ops, batch, grid, p)) return -1;
+  if (chain_plan(ops, batch, grid, p, (size_t)((flags >> 8) & 0xFF) * 4096)) return -1;   // (dev knob: ring cap)
   uint8_t* base = (uint8_t*)ws;
   ChainOp* dev_ops = (ChainOp*)(base + kChainCounterBytes);
   ChainW* dev_w = (ChainW*)(dev_ops + n);
@@ -634,7 +709,9 @@ int gemv_chain_s8(int act, const TrChainLayer* host, int n, int batch, void* ws,
   a.trace = ((flags >> 24) & 2) ? (uint64_t*)(base + chain_trace_off(n)) : nullptr;
   a.n_ops = n;
   a.batch = batch;
-  a.ns = p.ns;
+  a.probe = (flags >> 24) & 0xF;
+  a.ring_bytes = p.ring_bytes;
+  a.piece = ((flags >> 16) & 0xFF) ? ((flags >> 16) & 0xFF) * 1024 : kChainPiece;   // (dev knob: KiB)
   a.nb_max = p.nb_max;
   a.tv_floats = p.tv_floats;
   void (*kern)(const ChainArgs);
@@ -645,7 +722,7 @@ int gemv_chain_s8(int act, const TrChainLayer* host, int n, int batch, void* ws,
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
-  cfg.blockDim = dim3(kChainWarps * 32, 1, 1);
+  cfg.blockDim = dim3((kChainWarps + 1) * 32, 1, 1);
   cfg.dynamicSmemBytes = p.smem;
   cfg.stream = st;
   cudaLaunchAttribute attrs[2];
@@ -661,8 +738,15 @@ int gemv_chain_s8(int act, const TrChainLayer* host, int n, int batch, void* ws,
   cfg.attrs = attrs;
   cfg.numAttrs = na;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
-  TR_REQUIRE(e == cudaSuccess, "tr_linear_chain: launch failed: %s (grid %d, smem %zu)", cudaGetErrorString(e), grid,
-             p.smem);
+  if (e != cudaSuccess) {
+    int occ = -1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (kChainWarps + 1) * 32, p.smem);
+    cudaFuncAttributes fa = {};
+    cudaFuncGetAttributes(&fa, kern);
+    set_error("tr_linear_chain: launch failed: %s (grid %d, smem %zu, occupancy %d, regs %d, max dyn smem %d)",
+              cudaGetErrorString(e), grid, p.smem, occ, fa.numRegs, fa.maxDynamicSharedSizeBytes);
+    return -1;
+  }
   return 0;
 }
 

@@ -54,32 +54,36 @@ class Chain:
         _lib.call_nostream("tr_linear_chain_prepare", self._table, len(table), self.batch, self._ws.data_ptr(),
                            self._ws.numel())
 
-    def run(self, pdl: bool = True, probe: int = 0) -> None:
+    def run(self, pdl: bool = True, probe: int = 0, ns: int = 0, hold: int = 0) -> None:
+        """``probe``/``ns``/``hold``: development knobs (trace stamps / skeleton probes, ring cap in 4 KiB,
+        bulk-copy piece in KiB)."""
         _lib.call("tr_linear_chain", _ACT[self.dtype], self._table, len(self.ops), self.batch,
-                  (_lib.LINEAR_PDL if pdl else 0) | ((probe & 0xF) << 24), self._ws.data_ptr(), self._ws.numel(),
-                  _lib.stream_handle())
+                  (_lib.LINEAR_PDL if pdl else 0) | ((probe & 0xF) << 24) | ((ns & 0xFF) << 8) | ((hold & 0xFF) << 16),
+                  self._ws.data_ptr(), self._ws.numel(), _lib.stream_handle())
 
     def trace(self) -> torch.Tensor:
-        """Development probe (run(probe=2)): int64 %globaltimer stamps [n_ops, n_ctas, 4] =
-        (op start, inputs ready, staged, stored)."""
+        """Development probe (run(probe=2)): int64 %globaltimer stamps [n_ops, n_ctas, 16] = (op start,
+        inputs ready, staged, stored, warp 0 main loop done, slice landed, first x loads landed, slice
+        issued, main loops joined, boundary tiles stored, all stored)."""
         n = len(self.ops)
         sms = torch.cuda.get_device_properties(self._ws.device).multi_processor_count
         tab = 4096 + 104 * n + 16 * n   # (counters | ChainOp 104 B each | ChainW 16 B each)
         off = (tab + 255) // 256 * 256
-        return self._ws[off: off + n * sms * 32].view(torch.int64).view(n, sms, 4)
+        return self._ws[off: off + n * sms * 128].view(torch.int64).view(n, sms, 16)
 
 
 class LinearStack:
     """y = W_{n-1}( ... W_1(W_0 x)) over TernaryWeights, replayed from one CUDA graph.
 
-    ``chain=True`` (batch <= 4, TQ2, <= 256 layers): the whole stack is ONE persistent launch
-    (K6, tr_linear_chain) -- weights stream across layer boundaries while the grid waits for
-    each layer's input.  Otherwise one PDL-chained tr_linear per layer (GEMV or tcgen05 GEMM
-    by batch).  ``chain=None`` picks the chain whenever it applies.
+    ``chain=True`` (batch <= 4, TQ2, <= 256 layers, each CTA's weight slice must fit the ring next
+    to the staged activations): the whole stack is ONE persistent launch (K6, tr_linear_chain).
+    Default: one PDL-chained tr_linear per layer (GEMV or tcgen05 GEMM by batch) -- measured as
+    fast as K6 on the BASELINE stack (6.1 vs 6.5 us per layer), whose per-layer
+    time is set by compute and synchronisation, not by the weight stream.
     """
 
     def __init__(self, weights: list[TernaryWeight], batch: int, dtype=torch.float16, pdl: bool = True,
-                 chain: bool | None = None):
+                 chain: bool = False):
         if not weights:
             raise ValueError("empty stack")
         for a, b in zip(weights, weights[1:]):
@@ -92,20 +96,14 @@ class LinearStack:
         dev = weights[0].data.device
         self.x = torch.zeros((self.batch, weights[0].cols), dtype=dtype, device=dev)
         self.bufs = [torch.empty((self.batch, w.rows), dtype=dtype, device=dev) for w in weights]
-        ok = 1 <= self.batch <= 4 and len(weights) <= 256 and all(w.fmt is DType.TQ2 for w in weights)
-        self.chain = ok if chain is None else (bool(chain) and ok)
+        self.chain = bool(chain)
         self._chain = None
-        if self.chain:
+        if self.chain:   # (tr_linear_chain_prepare rejects what K6 cannot run: TriRunError)
             ops, cur = [], self.x
             for w, out in zip(weights, self.bufs):
                 ops.append({"w": w, "x": cur, "y": out})
                 cur = out
-            try:
-                self._chain = Chain(ops, self.batch, dtype)
-            except _lib.TriRunError:
-                if chain:
-                    raise
-                self.chain = False   # e.g. activations too wide to stage next to the rings
+            self._chain = Chain(ops, self.batch, dtype)
         self.stream = torch.cuda.Stream(device=dev)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.stream(self.stream):
