@@ -31,10 +31,10 @@ int gemv_tq2(int act, const void* w, const void* x, void* y, int64_t ldx, int64_
              int cols, int ctas, int pdl, cudaStream_t st, int pre, const void* pre_delta, const void* pre_gamma,
              void* pre_out, float eps, int out_f32);
 size_t gemv_workspace_bytes(int batch, int rows, int cols);
-bool gemv_s8_fits(int batch, int rows, int cols);
+bool gemv_s8_fits(int batch, int rows, int cols, int fmt);
 int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows, int cols,
             int ctas, int pdl, cudaStream_t st, int pre, const void* pre_delta, const void* pre_gamma, void* pre_out,
-            float eps, int cosched, int epi, int out_f32);
+            float eps, int cosched, int epi, int out_f32, int fmt);
 int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
               int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg,
               int out_f32);
@@ -84,12 +84,12 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
   const int knob = (flags >> 8) & 0xFFFF;   // GEMV: CTA count; UMMA: K split (0 = automatic)
   cudaStream_t st = (cudaStream_t)stream;
   const bool aligned = (ldx % 8) == 0 && ((uintptr_t)x & 15) == 0;
-  const bool s8 = batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols);
+  const bool s8 = batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols, fmt);
   if (epi) {   // only the int8-slice GEMV knows the gate/up tile pairing: never fall through to another path
     TR_REQUIRE(fmt == kFmtTq2 && s8 && !(flags & TR_LINEAR_FORCE_UMMA),
                "tr_linear: the SwiGLU epilogue runs on the int8-slice GEMV only (TQ2, batch <= 4)");
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, pdl, st, 0, nullptr, nullptr,
-                   nullptr, 0.0f, (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, 1, 0);
+                   nullptr, 0.0f, (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, 1, 0, kFmtTq2);
   }
   // measured crossover (scripts/dev/gemv_sweep.py): the mma.sync GEMV wins at batch 1-2 and,
   // while it can stage the activations in shared memory, up to 8; the tensor-core GEMM beyond
@@ -99,17 +99,18 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
     use_umma = true;
   }
   if (flags & TR_LINEAR_FORCE_GEMV) use_umma = false;
-  if (fmt == kFmtTq1) {   // 1.6-bit weights are decoded on the fly by the tensor-core kernel only
-    TR_REQUIRE(aligned, "tr_linear: TQ1 needs 16-byte aligned activation rows (ldx %% 8 == 0)");
-    TR_REQUIRE(!(flags & TR_LINEAR_FORCE_GEMV), "tr_linear: TQ1 has no mma.sync GEMV path");
-    use_umma = true;
+  if (fmt == kFmtTq1) {   // 1.6-bit weights: K4 (int8 GEMV, batch 1-4) or the tensor-core GEMM
+    if (flags & TR_LINEAR_FORCE_GEMV)
+      TR_REQUIRE(s8, "tr_linear: the TQ1 GEMV (K4) takes batch 1-4 with activations that fit in shared memory");
+    use_umma = !s8 || (flags & TR_LINEAR_FORCE_UMMA);
+    TR_REQUIRE(!use_umma || aligned, "tr_linear: TQ1 on the tensor cores needs 16-byte aligned activation rows");
   }
   if (use_umma)
     return gemm_umma(fmt, act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, uniform, workspace,
                      ws_bytes, pdl, st, (flags >> 24) & 0xF, out_f32);
   if (s8)
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, pdl, st, 0, nullptr, nullptr,
-                   nullptr, 0.0f, (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, 0, out_f32);
+                   nullptr, 0.0f, (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, 0, out_f32, fmt);
   const size_t esz = 2, ysz = out_f32 ? 4 : 2;
   for (int64_t n0 = 0; n0 < batch; n0 += 32) {
     const int nb_ = (int)(batch - n0 < 32 ? batch - n0 : 32);
@@ -134,12 +135,12 @@ int tr_linear_pre(int fmt, const void* w, const void* x, void* y, int64_t batch,
   TR_REQUIRE(((uintptr_t)w & 15) == 0, "tr_linear_pre: weight buffer must be 16-byte aligned");
   TR_REQUIRE(!(flags & TR_LINEAR_OUT_F32), "tr_linear_pre: TR_LINEAR_OUT_F32 is not supported here");
   if (flags & TR_LINEAR_EPI_SWIGLU)
-    TR_REQUIRE(batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols),
+    TR_REQUIRE(batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols, kFmtTq2),
                "tr_linear_pre: the SwiGLU epilogue runs on the int8-slice GEMV only (batch <= 4)");
-  if (batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols))
+  if (batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols, kFmtTq2))
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, (flags >> 8) & 0xFFFF,
                    flags & TR_LINEAR_PDL, (cudaStream_t)stream, pre_op, delta, gamma, x_out, eps,
-                   (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, (flags & TR_LINEAR_EPI_SWIGLU) ? 1 : 0, 0);
+                   (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, (flags & TR_LINEAR_EPI_SWIGLU) ? 1 : 0, 0, kFmtTq2);
   return gemv_tq2(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, (flags >> 8) & 0xFFFF,
                   flags & TR_LINEAR_PDL, (cudaStream_t)stream, pre_op, delta, gamma, x_out, eps, 0);
 }

@@ -48,12 +48,16 @@ struct S8Args {
   void* pre_out;
   float eps;
   int out_f32;   // TR_LINEAR_OUT_F32: y is float32
+  int fmt;       // kFmtTq2 (K3-S8) or kFmtTq1 (K4)
 };
 
-template <typename T, int NW, int PRE, int NG>
+template <typename T, int NW, int PRE, int NG, int FMT = kFmtTq2>
 __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Args a) {
-  using Cfg = S8Cfg<NW, NG>;
+  static_assert(FMT == kFmtTq2 || PRE == 0, "fused producers are TQ2-only");
+  using Cfg = S8Cfg<NW, NG, FMT>;
   constexpr int kSlotBytes = Cfg::kSlotBytes;
+  constexpr int UB = S8Fmt<FMT>::kUnit;       // bytes per 16 x 256 unit
+  constexpr int IB = S8Fmt<FMT>::kItem;       // staged bytes per (block, batch row)
   extern __shared__ __align__(128) uint8_t smem[];
   // batch rows nbr; staged layout rows nrx (1, 2, or 4 for NG = 2: batch 3-4), log2 lr
   const int NS = a.ns, nbr = a.batch, nb = a.nb;
@@ -100,8 +104,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   auto issue = [&](int slot) {
     if (pu >= wu1) return;
     const int n = min(kS8SU, wu1 - pu);
-    mbar_expect_tx(&mybar[slot], n * kUnitBytes);
-    bulk_g2s(myring + slot * kSlotBytes, a.w + (int64_t)pu * kUnitBytes, n * kUnitBytes, &mybar[slot], pol);
+    mbar_expect_tx(&mybar[slot], n * UB);
+    bulk_g2s(myring + slot * kSlotBytes, a.w + (int64_t)pu * UB, n * UB, &mybar[slot], pol);
     pu += n;
   };
   if (lane == 0) {
@@ -250,7 +254,15 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
               f[t][e] = s8_rnd<T>(s8_rnd<T>(__fdividef(f[t][e], 1.0f + __expf(-f[t][e]))) * up[e]);   // (0 past cols)
           }
         }
-        if (nv > 0) s8_stage_blocks<2>(f, xs, ncs, fsc, nrx, kbs, brs, nv);
+        if constexpr (FMT == kFmtTq1) {
+#pragma unroll
+          for (int t = 0; t < 2; ++t)
+            if (t < nv)
+              s8q1_stage_block(f[t], xs + (size_t)(kbs[t] * nrx + brs[t]) * IB, ncs + (kbs[t] * nrx + brs[t]) * 4,
+                               fsc + kbs[t] * nrx + brs[t]);
+        } else {
+          if (nv > 0) s8_stage_blocks<2>(f, xs, ncs, fsc, nrx, kbs, brs, nv);
+        }
         va[0] = va[2];
         va[1] = va[3];
         if (PRE == 2) {
@@ -279,12 +291,17 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
     const int bB = nBc >> 2, sB = nBc & 3;
     const int swB = ((c >> 1) << 1) | (sB & 1);
     // B fragment base in shared space: the group swizzle (q ^ swB) becomes an XOR on bits 4-5
-    xsB32[G2] = smem_u32(xs + (size_t)bB * kS8ItemBytes + sB * 256 + c * 64) ^ (uint32_t)(swB << 4);
+    // (TQ1: the lane's 18 B' words of slice sB, lane column c)
+    if constexpr (FMT == kFmtTq1)
+      xsB32[G2] = smem_u32(xs + (size_t)bB * IB + (sB * 4 + c) * 80);
+    else
+      xsB32[G2] = smem_u32(xs + (size_t)bB * IB + sB * 256 + c * 64) ^ (uint32_t)(swB << 4);
     const int bD = NG == 1 ? min(c >> 1, nrx - 1) : 2 * G2 + (c >> 1);   // D: slices 2(c&1), +1 of this row
     ncsD[G2] = ncs + bD * 4 + 2 * (c & 1);
     fscD[G2] = fsc + bD;
   }
-  const int kb_shift = 10 + lr;                // log2(nrx * kS8ItemBytes)
+  const int kb_shift = 10 + lr;                // log2(nrx * kS8ItemBytes) (TQ2)
+  const uint32_t kb_stride = (uint32_t)(nrx * IB);
   const float lane_w = (c & 1) ? 65536.0f : 1.0f;
 
   float* tv = reinterpret_cast<float*>(smem + Cfg::smem(nb, nrx, NS));   // (epi) [tile - t0][16 rows][4]
@@ -433,6 +450,34 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
     }
     mbar_wait(&mybar[s], (k >> nslog) & 1);
     const uint8_t* slot = myring + s * kSlotBytes;
+    if constexpr (FMT == kFmtTq1) {   // K4: units decoded by IMAD (F_k of both codes of a pair-group)
+#pragma unroll
+      for (int q = 0; q < kS8SU; ++q) {
+        if (q < n) {
+          if (kb == nb) {   // next tile
+            close_tile(cur);
+#pragma unroll
+            for (int G2 = 0; G2 < NG; ++G2) acc[G2][0] = acc[G2][1] = 0.0f;
+            ++cur;
+            kb = 0;
+          }
+          const uint8_t* up = slot + q * UB;
+          uint32_t xq[NG];
+          int2 cs[NG];
+#pragma unroll
+          for (int G2 = 0; G2 < NG; ++G2) {
+            xq[G2] = xsB32[G2] + (uint32_t)kb * kb_stride;
+            cs[G2] = *reinterpret_cast<const int2*>(ncsD[G2] + (kb << (lr + 2)));
+          }
+          int D[NG][4];
+          q1_unit_mma<NG>(up, g, c, xq, cs, D);
+          epilogue(D, *reinterpret_cast<const uint32_t*>(up + kQ1TileBlockBytes + g * 4), kb);
+          ++kb;
+        }
+      }
+      u += n;
+      continue;
+    }
     uint4 wl[kS8SU], wh[kS8SU];
     uint32_t sv[kS8SU];
 #pragma unroll
@@ -549,42 +594,45 @@ static bool s8_small(int n_tiles, int nb, int grid) {
 
 static int s8_layout_rows(int batch) { return batch <= 2 ? batch : 4; }   // staged rows (NG = 2 pads to 4)
 
-template <int NW, int NG>
+template <int NW, int NG, int FMT = kFmtTq2>
 static size_t s8_smem_plan(int batch, int nb, int n_tiles, int grid, int* ns_out, size_t cap = 227 * 1024) {
   int ns = s8_ns<NW>(n_tiles, nb, grid);
   const int nra = s8_layout_rows(batch);
-  size_t sm = S8Cfg<NW, NG>::smem(nb, nra, ns);
+  size_t sm = S8Cfg<NW, NG, FMT>::smem(nb, nra, ns);
   while (sm > cap && ns > 1) {   // wide activations: a shallower weight ring
     ns >>= 1;
-    sm = S8Cfg<NW, NG>::smem(nb, nra, ns);
+    sm = S8Cfg<NW, NG, FMT>::smem(nb, nra, ns);
   }
   if (ns_out) *ns_out = ns;
   return sm;
 }
 
-template <int NG>
+template <int NG, int FMT>
 static bool s8_fits_ng(int batch, int nb, int n_tiles, int grid) {
   int ns = 0;
-  const size_t sm = s8_small(n_tiles, nb, grid) ? s8_smem_plan<8, NG>(batch, nb, n_tiles, grid, &ns)
-                                                : s8_smem_plan<16, NG>(batch, nb, n_tiles, grid, &ns);
+  const size_t sm = s8_small(n_tiles, nb, grid) ? s8_smem_plan<8, NG, FMT>(batch, nb, n_tiles, grid, &ns)
+                                                : s8_smem_plan<16, NG, FMT>(batch, nb, n_tiles, grid, &ns);
   return sm <= 227 * 1024 && (ns >= 2 || s8_ns<16>(n_tiles, nb, grid) < 2);
 }
 
-// true when the int8-slice GEMV takes this product (batch 1-4, activations fit with a ring of >= 2)
-bool gemv_s8_fits(int batch, int rows, int cols) {
+// true when the int8-slice GEMV (TQ2: K3-S8, TQ1: K4) takes this product (batch 1-4, activations
+// fit with a weight ring of >= 2 slots)
+bool gemv_s8_fits(int batch, int rows, int cols, int fmt) {
   if (batch < 1 || batch > 4) return false;
   const int nb = (int)ceil_div(cols, kBlock), n_tiles = (int)ceil_div(rows, 16);
   const int grid = sm_count() < n_tiles ? sm_count() : n_tiles;
-  return batch <= 2 ? s8_fits_ng<1>(batch, nb, n_tiles, grid) : s8_fits_ng<2>(batch, nb, n_tiles, grid);
+  if (fmt == kFmtTq1)
+    return batch <= 2 ? s8_fits_ng<1, kFmtTq1>(batch, nb, n_tiles, grid) : s8_fits_ng<2, kFmtTq1>(batch, nb, n_tiles, grid);
+  return batch <= 2 ? s8_fits_ng<1, kFmtTq2>(batch, nb, n_tiles, grid) : s8_fits_ng<2, kFmtTq2>(batch, nb, n_tiles, grid);
 }
 
 static size_t s8_tv_bytes(const S8Args& a, int grid) {   // SwiGLU epilogue: tile results of one CTA
   return a.epi ? (size_t)2 * ceil_div(a.n_tiles / 2, grid) * 64 * sizeof(float) : 0;
 }
 
-template <typename T, int NW, int PRE, int NG>
+template <typename T, int NW, int PRE, int NG, int FMT = kFmtTq2>
 static int launch_s8_k(S8Args& a, int grid, int pdl, cudaStream_t st) {
-  auto kern = k_gemv_s8<T, NW, PRE, NG>;
+  auto kern = k_gemv_s8<T, NW, PRE, NG, FMT>;
   static int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -592,8 +640,9 @@ static int launch_s8_k(S8Args& a, int grid, int pdl, cudaStream_t st) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured_dev = dev;
   }
-  const size_t smem = s8_smem_plan<NW, NG>(a.batch, a.nb, a.n_tiles, grid, &a.ns, 227 * 1024 - s8_tv_bytes(a, grid)) +
-                      s8_tv_bytes(a, grid);
+  const size_t smem =
+      s8_smem_plan<NW, NG, FMT>(a.batch, a.nb, a.n_tiles, grid, &a.ns, 227 * 1024 - s8_tv_bytes(a, grid)) +
+      s8_tv_bytes(a, grid);
   if (smem > 227 * 1024) {
     set_error("tr_linear(gemv-s8): %d blocks per row x batch %d need %zu B of shared memory", a.nb, a.batch, smem);
     return -1;
@@ -617,6 +666,7 @@ static int launch_s8_k(S8Args& a, int grid, int pdl, cudaStream_t st) {
 }
 template <typename T, int NW, int NG>
 static int launch_s8_ng(S8Args& a, int grid, int pdl, cudaStream_t st) {   // one kernel per fused producer
+  if (a.fmt == kFmtTq1) return launch_s8_k<T, NW, 0, NG, kFmtTq1>(a, grid, pdl, st);
   if (a.pre == 1) return launch_s8_k<T, NW, 1, NG>(a, grid, pdl, st);
   if (a.pre == 2) return launch_s8_k<T, NW, 2, NG>(a, grid, pdl, st);
   return launch_s8_k<T, NW, 0, NG>(a, grid, pdl, st);
@@ -628,12 +678,17 @@ static int launch_s8(S8Args& a, int grid, int pdl, cudaStream_t st) {
 
 int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows, int cols,
             int ctas, int pdl, cudaStream_t st, int pre, const void* pre_delta, const void* pre_gamma, void* pre_out,
-            float eps, int cosched, int epi, int out_f32) {
-  if (!gemv_s8_fits(batch, rows, cols)) {
+            float eps, int cosched, int epi, int out_f32, int fmt) {
+  if (!gemv_s8_fits(batch, rows, cols, fmt)) {
     set_error("tr_linear(gemv-s8): batch %d x %d columns does not fit the int8-slice GEMV", batch, cols);
     return -1;
   }
+  if (fmt == kFmtTq1 && (pre || epi)) {
+    set_error("tr_linear(gemv-q1): fused producers / epilogues run on TQ2 weights only");
+    return -1;
+  }
   S8Args a = {};
+  a.fmt = fmt;
   a.w = (const uint8_t*)w;
   a.x = x;
   a.y = y;

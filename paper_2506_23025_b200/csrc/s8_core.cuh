@@ -16,9 +16,16 @@ constexpr int kS8SU = 2;
 #endif              // units per ring slot (one bulk copy)
 constexpr int kS8NSMax = 4;
 constexpr int kS8ItemBytes = 1024;    // staged x per (block, batch row): 4 slices x 4 chunks x 16 words
+constexpr int kQ1ItemBytes = 1280;    // TQ1: 4 slices x 4 lane columns x 80 B (18 words of 9 MMAs + pad)
 
-template <int NW, int NG = 1> struct S8Cfg {   // NG MMA groups of 2 batch rows
-  static constexpr int kSlotBytes = kS8SU * kUnitBytes;
+template <int FMT> struct S8Fmt {      // TQ2 (T16 units) or TQ1 (T16-Q1 units)
+  static constexpr int kUnit = FMT == kFmtTq1 ? kQ1UnitBytes : kUnitBytes;
+  static constexpr int kItem = FMT == kFmtTq1 ? kQ1ItemBytes : kS8ItemBytes;
+  static constexpr int kTileBlock = FMT == kFmtTq1 ? kQ1TileBlockBytes : kTileBlockBytes;
+};
+
+template <int NW, int NG = 1, int FMT = kFmtTq2> struct S8Cfg {   // NG MMA groups of 2 batch rows
+  static constexpr int kSlotBytes = kS8SU * S8Fmt<FMT>::kUnit;
   static constexpr size_t kRedOff = 1024;                         // [mbarriers | slot tags]
   static constexpr size_t kRedBytes = (size_t)2 * NW * 64 * NG * 4;   // 2 parked tiles per warp x 64 NG floats
   static constexpr size_t kCsOff = kRedOff + kRedBytes;           // -Cs: nb x nrx x 4 int32
@@ -27,7 +34,7 @@ template <int NW, int NG = 1> struct S8Cfg {   // NG MMA groups of 2 batch rows
     return (f_off(nb, nrx) + (size_t)nb * nrx * 4 + 127) / 128 * 128;
   }
   __host__ __device__ static size_t ring_off(int nb, int nrx) {
-    return xs_off(nb, nrx) + (size_t)nb * nrx * kS8ItemBytes;
+    return xs_off(nb, nrx) + (size_t)nb * nrx * S8Fmt<FMT>::kItem;
   }
   __host__ __device__ static size_t smem(int nb, int nrx, int ns) {
     return ring_off(nb, nrx) + (size_t)NW * ns * kSlotBytes;
@@ -194,5 +201,169 @@ __device__ __forceinline__ void imma_c(int (&d)[4], const uint32_t (&a)[4], uint
 }
 __device__ __forceinline__ uint32_t u4c(const uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 
+
+// ---- K4: the TQ1 (1.6 bit) GEMV on the same int8 tensor-core path ----------------------------
+//
+// T16-Q1 rows hold 26 pair-groups (A_g, B_g): base-3 codes of columns 10g + {0,2,4,6,8} and
+// 10g + {1,3,5,7,9} (common.cuh).  Algorithm 1 (reference _kernels.pyx:73-87)
+// gives digit k (k = 1..5) of code c as d_k = F_k - 3 F_{k-1}, F_k = floor(3^k c / 256), F_0 = 0
+// (s_k = 3^k c mod 256 by induction, and 3^k c = 768 F_{k-1} + 3 s_{k-1}).  Summation by parts
+// moves the subtraction onto the activations:
+//     sum_k d_k x_k = sum_k F_k (x_k - 3 x_{k+1}),   x_6 := 0,
+// with x_k the activation of digit k's column.  F_k <= 242 is a u8 MMA operand, and with
+// R = A_g | B_g << 16 one IMAD R * 3^k yields F_k of both codes in bytes 1 and 3 (3^5 * 255 <
+// 2^16: the 16-bit lanes never carry into each other) -- 5 IMADs per 10 weights, one PRMT per 4
+// MMA operand bytes, no digit extraction.  Staging turns x into B'_k = x~_k - 3 x~_{k+2 columns}
+// on the integer grid (exact), sliced into int8 as in K3-S8, and the trit offset is folded as
+// before: D = sum F B' - sum x~ (= sum (d - 1) x~).
+//
+// K-slot order.  Lane column c of the MMA fragments owns pair-groups [G0(c), G0(c) + 7) of its
+// two rows, G0 = {0, 7, 14, 20} (7, 7, 6, 6 groups); result rho = 5 gl + (k - 1) of local group
+// gl, packed two per A register: register m = {F(2m).A, F(2m).B, F(2m+1).A, F(2m+1).B}.  Nine
+// MMAs (288 K slots) cover a row's 260 digits; slots past a lane's groups get B' = 0, so the
+// bytes a lane decodes past its own groups (harmless reads inside the unit) never count.
+__host__ __device__ inline int q1_g0(int c) { return c == 0 ? 0 : c == 1 ? 7 : c == 2 ? 14 : 20; }
+__host__ __device__ inline int q1_ng(int c) { return c < 2 ? 7 : 6; }
+
+// Stage one (block, batch row) item for K4 (whole warp; lane holds columns 8 lane .. + 7):
+// x~ on the block's integer grid, -Cs of the x~ slices, the grid factor 2^(ex - 23), and the 288
+// B' slots as int8 slices at [slice s][lane column c][word m] (80 B rows, 16-B aligned).
+__device__ __forceinline__ void s8q1_stage_block(const float (&f)[8], uint8_t* item, int32_t* ncs_item,
+                                                 float* fsc_item) {
+  const int lane = threadIdx.x & 31;
+  float mx = 0.0f;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) mx = fmaxf(mx, fabsf(f[e]));
+  const unsigned mb = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
+  int ex = (int)((mb >> 23) & 0xFF) - 127;
+  ex = ex < -90 ? -90 : ex;
+  const float q = __int_as_float((150 - ex) << 23);   // 2^(23 - ex)
+  int xi[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) xi[e] = __float2int_rn(f[e] * q);
+  // -Cs: per slice, the sum over the block of the balanced int8 slices of x~
+  int cs[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t Z[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) Z[i] = ((uint32_t)xi[4 * h + i] + 0x80808080u) ^ 0x80808080u;
+    const uint32_t t0 = __byte_perm(Z[0], Z[1], 0x5140), t1 = __byte_perm(Z[0], Z[1], 0x7362);
+    const uint32_t t2 = __byte_perm(Z[2], Z[3], 0x5140), t3 = __byte_perm(Z[2], Z[3], 0x7362);
+    cs[0] = __dp4a((int)__byte_perm(t0, t2, 0x5410), 0x01010101, cs[0]);
+    cs[1] = __dp4a((int)__byte_perm(t0, t2, 0x7632), 0x01010101, cs[1]);
+    cs[2] = __dp4a((int)__byte_perm(t1, t3, 0x5410), 0x01010101, cs[2]);
+    cs[3] = __dp4a((int)__byte_perm(t1, t3, 0x7632), 0x01010101, cs[3]);
+  }
+#pragma unroll
+  for (int s = 0; s < 4; ++s) cs[s] = __reduce_add_sync(0xffffffffu, cs[s]);
+  // x~ as int32 scratch in the item's own bytes (columns 256, 257 read as 0)
+  int* scr = reinterpret_cast<int*>(item);
+  *reinterpret_cast<int4*>(scr + 8 * lane) = make_int4(xi[0], xi[1], xi[2], xi[3]);
+  *reinterpret_cast<int4*>(scr + 8 * lane + 4) = make_int4(xi[4], xi[5], xi[6], xi[7]);
+  if (lane == 0) {
+    scr[256] = 0;
+    scr[257] = 0;
+  }
+  __syncwarp();
+  // 72 quads (lane column c', register m): four B' slots each -> one word per slice
+  uint32_t W[3][4];
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    const int qd = lane + 32 * p;
+    const int cq = qd / 18, m = qd - 18 * cq;
+    uint32_t Z[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int rho = 2 * m + (b >> 1);
+      const int gl = (rho * 13) >> 6, k1 = rho - 5 * gl;   // rho / 5, rho % 5 (rho < 64)
+      const int col = 10 * (q1_g0(cq & 3) + gl) + 2 * k1 + (b & 1);
+      const bool valid = qd < 72 && rho < 5 * q1_ng(cq & 3) && col < 256;
+      const int x1 = valid ? scr[col] : 0;
+      const int x2 = (valid && k1 < 4) ? scr[col + 2] : 0;
+      Z[b] = ((uint32_t)(x1 - 3 * x2) + 0x80808080u) ^ 0x80808080u;
+    }
+    const uint32_t t0 = __byte_perm(Z[0], Z[1], 0x5140), t1 = __byte_perm(Z[0], Z[1], 0x7362);
+    const uint32_t t2 = __byte_perm(Z[2], Z[3], 0x5140), t3 = __byte_perm(Z[2], Z[3], 0x7362);
+    W[p][0] = __byte_perm(t0, t2, 0x5410);
+    W[p][1] = __byte_perm(t0, t2, 0x7632);
+    W[p][2] = __byte_perm(t1, t3, 0x5410);
+    W[p][3] = __byte_perm(t1, t3, 0x7632);
+  }
+  __syncwarp();   // every lane has read the scratch before the words overwrite it
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    const int qd = lane + 32 * p;
+    if (qd < 72) {
+      const int cq = qd / 18, m = qd - 18 * cq;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) *reinterpret_cast<uint32_t*>(item + (s * 4 + cq) * 80 + m * 4) = W[p][s];
+    }
+  }
+  if (lane == 0) {
+    *reinterpret_cast<int4*>(ncs_item) = make_int4(-cs[0], -cs[1], -cs[2], -cs[3]);
+    *fsc_item = __int_as_float((127 + ex - 23) << 23);   // 2^(ex - 23)
+  }
+}
+
+// One T16-Q1 unit (16 rows x 256 columns) against one staged block: 9 u8 x s8 MMAs per group of
+// two batch rows.  up: the unit in shared memory; xq[G2]: shared address of this lane's 18 B'
+// words (slice sB, lane column c) for the block; cs: the trit offsets -Cs of its D columns.
+template <int NG>
+__device__ __forceinline__ void q1_unit_mma(const uint8_t* up, int g, int c, const uint32_t (&xq)[NG],
+                                            const int2 (&cs)[NG], int (&D)[NG][4]) {
+  const int wo = (c * 14) >> 2;   // first 32-bit word of byte 2 G0(c): 0, 3, 7, 10
+  const uint32_t* r0 = reinterpret_cast<const uint32_t*>(up + kQ1RowBytes * g) + wo;
+  const uint32_t* r1 = reinterpret_cast<const uint32_t*>(up + kQ1RowBytes * (g + 8)) + wo;
+  uint32_t w0[5], w1[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    w0[i] = r0[i];
+    w1[i] = r1[i];
+  }
+  const uint32_t sh = (c == 1) ? 16u : 0u;   // lane column 1 starts mid-word (byte 14)
+  uint32_t R0[7], R1[7];                     // pair-group registers A_g | B_g << 16
+#pragma unroll
+  for (int gl = 0; gl < 7; ++gl) {
+    const int i = gl >> 1;
+    const uint32_t a0 = __funnelshift_r(w0[i], w0[i + 1], sh), a1 = __funnelshift_r(w1[i], w1[i + 1], sh);
+    R0[gl] = __byte_perm(a0, 0u, (gl & 1) ? 0x4342 : 0x4140);
+    R1[gl] = __byte_perm(a1, 0u, (gl & 1) ? 0x4342 : 0x4140);
+  }
+  uint32_t xb[NG][18];
+#pragma unroll
+  for (int G2 = 0; G2 < NG; ++G2) {
+#pragma unroll
+    for (int i4 = 0; i4 < 4; ++i4) {
+      const uint4 v = ld_shared_v4u(xq[G2] + 16 * i4);
+      xb[G2][4 * i4] = v.x;
+      xb[G2][4 * i4 + 1] = v.y;
+      xb[G2][4 * i4 + 2] = v.z;
+      xb[G2][4 * i4 + 3] = v.w;
+    }
+    uint32_t lo, hi;
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];\n" : "=r"(lo), "=r"(hi) : "r"(xq[G2] + 64));
+    xb[G2][16] = lo;
+    xb[G2][17] = hi;
+  }
+  constexpr uint32_t kPow3[5] = {3u, 9u, 27u, 81u, 243u};
+  auto res = [&](const uint32_t (&R)[7], int rho) -> uint32_t {   // F of both codes in bytes 1, 3
+    return rho < 35 ? R[rho / 5] * kPow3[rho % 5] : 0u;
+  };
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    const uint32_t A[4] = {__byte_perm(res(R0, 4 * i), res(R0, 4 * i + 1), 0x7531),
+                           __byte_perm(res(R1, 4 * i), res(R1, 4 * i + 1), 0x7531),
+                           __byte_perm(res(R0, 4 * i + 2), res(R0, 4 * i + 3), 0x7531),
+                           __byte_perm(res(R1, 4 * i + 2), res(R1, 4 * i + 3), 0x7531)};
+#pragma unroll
+    for (int G2 = 0; G2 < NG; ++G2) {
+      if (i == 0)
+        imma_c(D[G2], A, xb[G2][0], xb[G2][1], cs[G2].x, cs[G2].y, cs[G2].x, cs[G2].y);
+      else
+        imma(D[G2], A, xb[G2][2 * i], xb[G2][2 * i + 1]);
+    }
+  }
+}
 
 }  // namespace tr

@@ -748,6 +748,75 @@ def test_gemv_s8_vs_oracle(tp, dtype, kind, rows, cols, batch, per_block):
         assert rel_err(y16[fin], ref[fin]) <= tol
 
 
+def _rand_packed_tq1(rng, rows, cols, per_block):
+    T = (rng.integers(0, 3, size=(rows, cols)) - 1).astype(np.float32)
+    gam = np.float16(0.02 * (1 + rng.uniform(0, 1, size=(rows, 1)))).astype(np.float32)
+    W = gam * T
+    if per_block:
+        f = rng.choice([1.0, 0.5, 0.25], size=(rows, -(-cols // 256))).astype(np.float32)
+        W = W * np.repeat(f, 256, axis=1)[:, :cols]
+    return orc.pack_matrix(W, orc.TQ1)
+
+
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
+@pytest.mark.parametrize("kind", ["uniform", "range", "zeros", "tiny", "huge", "rows"])
+@pytest.mark.parametrize("rows,cols", [(1, 5), (37, 1500), (300, 777), (640, 8192)])
+@pytest.mark.parametrize("batch", [1, 2, 3, 4])
+@pytest.mark.parametrize("per_block", [False, True])
+def test_gemv_tq1_vs_oracle(tp, dtype, kind, rows, cols, batch, per_block):
+    """K4: the TQ1 GEMV (Algorithm-1 digits via F_k = floor(3^k c / 256), summation by parts onto
+    the activations) vs the float64 oracle, which decodes TQ1 by the canonical division formula."""
+    if kind in ("range", "rows") and rows == 1:
+        pytest.skip("one 5-term output: it can be all sub-grid terms (range) or an fp16 subnormal (rows)")
+    rng = np.random.default_rng(rows + cols + batch + len(kind) + 7)
+    payload, scales = _rand_packed_tq1(rng, rows, cols, per_block)
+    w = tp.PackedMatrix(rows=rows, cols=cols, fmt=tp.DType.TQ1, payload=payload, scales=scales).to_device()
+    x = _s8_inputs(rng, kind, batch, cols, dtype)
+    y = tp.linear(x, w, path="gemv").float().cpu().numpy()
+    ref = _oracle_ref(payload, scales, cols, orc.TQ1, x.float().cpu().numpy())
+    fin = np.isfinite(ref).all(axis=1) & (np.abs(ref).max(axis=1) < (6.5e4 if dtype == "float16" else 3e38))
+    tol = 2e-3 if dtype == "float16" else 6e-3
+    if dtype == "float16":   # rows whose outputs are fp16 subnormals: within one subnormal ulp (2^-24)
+        sub = np.abs(ref).max(axis=1) < 2.0 ** -14
+        if sub.any():
+            assert np.abs(y[sub] - ref[sub]).max() <= 2.0 ** -24
+        fin &= ~sub
+    err = rel_err(y[fin], ref[fin]) if fin.any() else 0.0
+    assert err <= tol, f"rel err {err:.3e}"
+
+
+def test_gemv_tq1_matches_tq2_same_trits_exact(tp):
+    """Integer activations, +-1/0 trits, scale 1: every block sum is exact on both GEMVs -> the TQ1
+    GEMV (K4) and the TQ2 one (K3-S8) agree bit for bit, and the TQ1 GEMV with the tcgen05 path."""
+    rng = np.random.default_rng(123)
+    for rows, cols in ((64, 4096), (300, 1500)):
+        W = (rng.integers(0, 3, size=(rows, cols)) - 1).astype(np.float32)
+        W[:, 0] = 1.0   # every block has a non-zero: scale 1 everywhere
+        w1 = tp.pack_matrix(W, tp.DType.TQ1).to_device()
+        w2 = tp.pack_matrix(W, tp.DType.TQ2).to_device()
+        for batch in (1, 2, 3, 4):
+            x = torch.from_numpy(rng.integers(-8, 9, size=(batch, cols)).astype(np.float32)).half().cuda()
+            a = tp.linear(x, w1, path="gemv")
+            b = tp.linear(x, w2, path="gemv")
+            c = tp.linear(x, w1, path="umma")
+            assert torch.equal(a, b) and torch.equal(a, c), (rows, cols, batch)
+
+
+def test_gemv_tq1_noncanonical_codes(tp):
+    """The reference decodes the 13 non-canonical TQ1 bytes by Algorithm 1; the
+    repack keeps that meaning, so the GEMV on such payloads matches the reference kernel's gemm."""
+    rng = np.random.default_rng(5)
+    rows, cols = 32, 512
+    payload = rng.integers(0, 256, size=(rows, 2, 52)).astype(np.uint8)
+    payload[:, :, 51] = rng.choice([0, 81, 162, 243 - 1], size=(rows, 2))   # tail code: only element 255 real
+    scales = np.full((rows, 2), 1.0, np.float16)
+    pm = tp.PackedMatrix(rows=rows, cols=cols, fmt=tp.DType.TQ1, payload=payload, scales=scales)
+    x = torch.from_numpy(rng.integers(-4, 5, size=(2, cols)).astype(np.float32)).half().cuda()
+    y = tp.linear(x, pm.to_device(), path="gemv").float().cpu().numpy()
+    ref = orc.gemm(payload, scales, cols, orc.TQ1, x.float().cpu().numpy())   # Algorithm-1 digits, exact here
+    np.testing.assert_array_equal(y, ref)
+
+
 def test_gemv_s8_exact_integer_cases(tp):
     # integer activations and +-1 weights with scale 1: every block sum is exact -> bitwise results
     rng = np.random.default_rng(5)
