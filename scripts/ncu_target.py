@@ -1,4 +1,5 @@
-"""Minimal launcher for ncu captures: rows cols batch [ctas] -> rotating-copy linear calls."""
+"""Minimal launcher for ncu captures: rows cols batch [ctas] -> rotating-copy linear calls.
+FMT=TQ1 in the environment packs 1.6-bit weights (K4 / K5 TQ1 paths)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -10,7 +11,7 @@ copies = max(2, min(32, -(-3 * 126 * 2**20 // wb)))
 def weight():   # the bench's synthetic weights: random trits, per-channel fp16 gamma
     T = torch.randint(-1, 2, (rows, cols), device="cuda").float()
     gam = (0.02 * (1 + torch.rand((rows, 1), device="cuda"))).half().float()
-    return tp.TernaryWeight.from_float(gam * T)
+    return tp.TernaryWeight.from_float(gam * T, getattr(tp.DType, os.environ.get("FMT", "TQ2")))
 
 
 ws = [weight() for _ in range(copies)]
