@@ -50,7 +50,7 @@ def parse():
     p.add_argument("--replicas", type=int, default=32)
     p.add_argument("--sweep", default="1,2,4,8,16,32,64,128")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
-    p.add_argument("--extras", default="decode,tq1,tp70b,boundary",
+    p.add_argument("--extras", default="bf16,decode,tq1,tp70b,boundary",
                    help="extra sections on rank 0 at N=1: decode (configs[2]), tq1 (configs[3]), tp70b (configs[4]), "
                         "boundary (the unmodified reference's linear.gemm on backend 'cuda', configs[0])")
     return p.parse_args()
@@ -232,13 +232,14 @@ def uniform_x(batch, cols, seed, dtype=None):
     return (torch.rand((batch, cols), generator=g, device="cuda") * 2 - 1).to(dtype or torch.float16)
 
 
-def dense_stack(weights, batch):
+def dense_stack(weights, batch, dtype=None):
     """PyTorch fp16 (cuBLAS) baseline on the dequantized weights of the same stack, CUDA-graphed,
-    on the same seeded U(-1, 1) activations as the ternary stack."""
+    on the same seeded U(-1, 1) activations as the ternary stack (bf16 with dtype=torch.bfloat16)."""
     import torch
 
-    dws = [w.dequantize(torch.float16) for w in weights]
-    x = uniform_x(batch, dws[0].shape[1], 4242 + batch)
+    dtype = dtype or torch.float16
+    dws = [w.dequantize(dtype) for w in weights]
+    x = uniform_x(batch, dws[0].shape[1], 4242 + batch, dtype)
     s = torch.cuda.Stream()
     g = torch.cuda.CUDAGraph()
 
@@ -319,12 +320,27 @@ def run_boundary():
 
 
 def run_extras(args, stack_ws):
-    """configs[2] decode tokens/s, configs[3] TQ1 8192^2, configs[4] 70B layer shapes (1 GPU + TP shards)."""
+    """configs[2] decode tokens/s, configs[3] TQ1 8192^2, configs[4] 70B layer shapes (1 GPU + TP shards),
+    and the configs[1] stack with bf16 activations next to cuBLAS bf16."""
     import torch
     import paper_2506_23025_b200 as tp
+    from paper_2506_23025_b200.graph import LinearStack
 
     out = {}
     want = set(args.extras.split(","))
+    if "bf16" in want:
+        res = []
+        for b in (1, 4, 16, 128):
+            st = LinearStack(stack_ws, batch=b, dtype=torch.bfloat16)
+            st.x.copy_(uniform_x(b, st.x.shape[1], 4242 + b, torch.bfloat16))
+            t = timed_graph(st.replay, 20, 3, None) / 20
+            g, dws = dense_stack(stack_ws, b, torch.bfloat16)
+            td = timed_graph(g.replay, 10, 2, None) / 10
+            res.append({"batch": b, "ms": round(t, 4), "gbs": round(st.algorithmic_bytes() / t / 1e6, 1),
+                        "cublas_bf16_ms": round(td, 4), "speedup_vs_bf16": round(td / t, 2)})
+            del st, g, dws
+            torch.cuda.empty_cache()
+        out["bf16_stack"] = res
     del stack_ws
     torch.cuda.empty_cache()
     if "boundary" in want:
@@ -403,6 +419,99 @@ def run_extras(args, stack_ws):
     return out
 
 
+def run_tp70b(rank, world, dist, batches=(1, 16), steps=50):
+    """configs[4] across the ranks of this job: the 70B MLP pair -- up (rows 28672 x cols 8192,
+    column-parallel: rank i owns 256-aligned output rows) then down (rows 8192 x cols 28672,
+    row-parallel: rank i owns the matching 256-blocks of K, fp32 partials) -- and the all-reduce of
+    the fp32 partials, all inside the timed region (CUDA graph when capture works).  Reports the
+    step (shards + all-reduce), the shards alone and the all-reduce alone, max over ranks (device
+    time).  All-reduce: NCCL, and the symmetric-memory one-shot kernel when this torch build and
+    the NVLink topology provide it (A/B)."""
+    import torch
+    import paper_2506_23025_b200 as tp
+    from paper_2506_23025_b200.parallel import shard_bounds
+
+    up_rows, d = 28672, 8192
+    r0, r1 = shard_bounds(up_rows, world, rank, 256)
+    g = torch.Generator(device="cuda").manual_seed(99 + rank)
+
+    def weight(rows, cols):
+        T = torch.randint(0, 3, (rows, cols), generator=g, device="cuda", dtype=torch.int8).float() - 1
+        gam = (0.02 * (1 + torch.rand((rows, 1), generator=g, device="cuda"))).half().float()
+        return tp.TernaryWeight.from_float(gam * T)
+
+    w_up, w_down = weight(r1 - r0, d), weight(d, r1 - r0)
+    torch.cuda.empty_cache()
+    symm = None
+    if dist is not None:
+        try:
+            import torch.distributed._symmetric_memory as symm_mem
+
+            symm = symm_mem
+        except Exception:
+            symm = None
+
+    def timed(fn, reps):
+        s = torch.cuda.Stream()
+        graph = None
+        with torch.cuda.stream(s):
+            fn()
+            s.synchronize()
+            try:
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=s):
+                    fn()
+            except Exception:
+                graph = None
+        torch.cuda.synchronize()
+        run = graph.replay if graph is not None else fn
+        ms = timed_graph(run, reps, 5, dist) / reps
+        return ms * 1e3, graph is not None
+
+    res = {"world": world, "shard_rows": [r0, r1], "up": f"{r1 - r0}x{d}", "down": f"{d}x{r1 - r0}", "batches": {}}
+    for b in batches:
+        x = uniform_x(b, d, 500 + b)   # identical on every rank
+        h = torch.empty((b, r1 - r0), dtype=torch.float16, device="cuda")
+        part = torch.empty((b, d), dtype=torch.float32, device="cuda")
+        ent = {}
+
+        def shards():
+            tp.linear(x, w_up, out=h)
+            tp.linear(h, w_down, out=part, out_dtype=torch.float32)
+
+        ent["shards_us"], _ = timed(shards, steps)
+        if dist is not None:   # (under torchrun; at one rank the collectives still run, as a floor)
+            def nccl_ar():
+                dist.all_reduce(part)
+
+            def step_nccl():
+                shards()
+                dist.all_reduce(part)
+
+            ent["allreduce_nccl_us"], g1 = timed(nccl_ar, steps)
+            ent["step_nccl_us"], g2 = timed(step_nccl, steps)
+            ent["graph"] = bool(g1 and g2)
+            if symm is not None:
+                try:
+                    buf = symm.empty((b, d), dtype=torch.float32, device="cuda")
+                    gname = dist.group.WORLD.group_name
+                    symm.rendezvous(buf, gname)
+
+                    def step_symm():
+                        tp.linear(x, w_up, out=h)
+                        tp.linear(h, w_down, out=buf, out_dtype=torch.float32)
+                        torch.ops.symm_mem.one_shot_all_reduce(buf, "sum", gname)
+
+                    ent["step_symm_one_shot_us"], _ = timed(step_symm, steps)
+                except Exception as e:   # pragma: no cover - topology / build dependent
+                    ent["symm_one_shot"] = f"unavailable: {type(e).__name__}: {str(e)[:120]}"
+        ent["allreduce_bytes"] = b * d * 4
+        res["batches"][str(b)] = {k: (round(v, 2) if isinstance(v, float) else v) for k, v in ent.items()}
+    del w_up, w_down
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_ours(args, rank, world, dist):
     import torch
     import paper_2506_23025_b200 as tp
@@ -452,6 +561,12 @@ def run_ours(args, rank, world, dist):
             torch.cuda.empty_cache()
 
     extras = run_extras(args, ws) if (rank == 0 and world == 1 and args.extras) else {}
+    if "tp70b" in args.extras.split(","):   # every rank: the tensor-parallel MLP across this job's GPUs
+        del ws
+        torch.cuda.empty_cache()
+        tp70 = run_tp70b(rank, world, dist)
+        if rank == 0:
+            extras["tp70b_mlp"] = tp70
 
     line = None
     if rank == 0:
@@ -500,7 +615,7 @@ def main():
         return
     import torch
 
-    if world > 1:
+    if world > 1 or "LOCAL_RANK" in os.environ:   # (under torchrun: NCCL even at one rank)
         import torch.distributed as tdist
 
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
