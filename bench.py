@@ -573,7 +573,9 @@ def run_ours(args, rank, world, dist):
         cpu = CpuReference(os.cpu_count() or 1).sample(args.cpu_seconds)
         traffic = None
         kernel_name = "k_gemv_s8"
-        prof = os.path.join(ROOT, "profiles", "r01_ncu_full_summary.json")
+        prof = os.path.join(ROOT, "profiles", "r02_ncu_full_summary.json")
+        if not os.path.exists(prof):
+            prof = os.path.join(ROOT, "profiles", "r01_ncu_full_summary.json")
         if os.path.exists(prof):   # one `ncu --set full` capture of the GEMV (scripts/profile_round.sh)
             summ = json.load(open(prof))
             g = summ.get("gemv") or summ.get("k_gemv_tq2", {})

@@ -115,31 +115,17 @@ def _weights(payload, scales):
         return dp, ds
 
 
-_TLS = threading.local()
-
-
-def _thread_stream() -> torch.cuda.Stream:
-    """One CUDA stream per calling thread: linear.gemm(threads=N)'s row ranges run concurrently."""
-    s = getattr(_TLS, "stream", None)
-    if s is None:
-        s = _TLS.stream = torch.cuda.Stream()
-    return s
-
-
 def _gemm(fmt: int, payload, scales, x, out, row0: int, row1: int) -> None:
     rows, nb = scales.shape
     batch = x.shape[0]
     if row1 <= row0 or batch == 0:
         return
-    p, s = _weights(payload, scales)   # (uploaded on the current stream, synchronously)
-    st = _thread_stream()
-    st.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(st):
-        xd = _dev(np.asarray(x, np.float32))
-        o = torch.empty((batch, rows), dtype=torch.float32, device="cuda")
-        _lib.call("tr_gemm_exact", fmt, p.data_ptr(), s.data_ptr(), xd.data_ptr(), o.data_ptr(), rows, nb, batch,
-                  int(row0), int(row1), _lib.stream_handle())
-        out[:, row0:row1] = o[:, row0:row1].cpu().numpy()
+    p, s = _weights(payload, scales)
+    xd = _dev(np.asarray(x, np.float32))
+    o = torch.empty((batch, rows), dtype=torch.float32, device="cuda")
+    _run("tr_gemm_exact", fmt, p.data_ptr(), s.data_ptr(), xd.data_ptr(), o.data_ptr(), rows, nb, batch,
+         int(row0), int(row1))
+    out[:, row0:row1] = o[:, row0:row1].cpu().numpy()
 
 
 def gemm_tq2(payload, scales, x, out, row0, row1):

@@ -29,14 +29,23 @@ def raw(rep):
 keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__cycles_active.avg", "sm__cycles_elapsed.avg",
         "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__grid_size", "launch__block_size",
         "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 summ = {}
+import os
+
 for name, rep, shape in [("gemv", "gpurun_out/prof_gemv.ncu-rep", "rows 11008 x cols 4096, batch 1, fp16"),
-                         ("umma", "gpurun_out/prof_umma.ncu-rep", "rows 11008 x cols 4096, batch 128, fp16")]:
+                         ("umma", "gpurun_out/prof_umma.ncu-rep", "rows 11008 x cols 4096, batch 128, fp16"),
+                         ("gemv_tq1", "gpurun_out/prof_q1.ncu-rep", "TQ1 rows 8192 x cols 8192, batch 1, fp16"),
+                         ("chain", "gpurun_out/prof_chain.ncu-rep",
+                          "K6 chain, 8 replicas of (4096x4096, 11008x4096, 4096x11008), batch 1, fp16")]:
+    if not os.path.exists(rep):
+        continue
     m = raw(rep)
     e = {"kernel": (m.get("Kernel Name") or m.get("Function Name") or "").split("(")[0]}
     e.update({k: m.get(k) for k in keys})
