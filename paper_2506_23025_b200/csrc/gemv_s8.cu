@@ -74,14 +74,18 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   uint64_t* mybar = bars + warp * NS;
   uint8_t* myring = ring + warp * NS * kSlotBytes;
   uint64_t* trace = (a.dbg & 2) ? reinterpret_cast<uint64_t*>(a.y) : nullptr;
-  auto stamp = [&](int k) {   // CTA stamps [blockIdx][0..7], warp stamps [148*8 + (blockIdx*NW + warp)*4 + k]
+  // (dev probe dbg&2) CTA stamps [blockIdx][0..7] = %globaltimer (ns); warp stamps
+  // [148*8 + (blockIdx*NW + warp)*4 + k-8] = SM clock cycles since the warp left griddepcontrol.wait
+  // (k = 8 staged, 9 main loop done, 10 stored, 11 first activation loads landed)
+  long long wait_clk = 0;
+  auto stamp = [&](int k) {
     if (trace && lane == 0) {
       uint64_t t;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
       if (k < 8) {
         if (warp == 0) trace[blockIdx.x * 8 + k] = t;
       } else {
-        trace[148 * 8 + (blockIdx.x * NW + warp) * 4 + (k - 8)] = t;
+        trace[148 * 8 + (blockIdx.x * NW + warp) * 4 + (k - 8)] = (uint64_t)(clock64() - wait_clk);
       }
     }
   };
@@ -116,17 +120,20 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
     slot_tile[2 * warp + 1] = -1;
   }
   // weights do not depend on the previous kernel: prefetch before griddepcontrol.wait
-  // (dev knob dbg&4: after it; dbg&8: one slot before, the rest after)
+  // (dev knobs dbg&12: 4 = whole ring before the wait, 8 = one slot before and the rest after the
+  // first activation loads, 12 = one slot before and the rest after staging)
   // Long per-warp ranges: only the first slot goes out before the wait -- the rest follows the
   // activation loads, which would otherwise queue behind a deep ring fill (measured: -4..-10% on
   // 9216x3072, 18432x3072, 11008x4096, 4096x11008; short ranges keep the whole ring in flight)
-  const int pre_slots = (a.dbg & 4) ? 0 : ((a.dbg & 8) || LL >= S8_PRE1_UNITS * NW) ? 1 : NS;
-  const bool ring_after_staging = (a.dbg & 12) == 12;   // dev probe: the whole ring after x is staged
+  const bool ring_after_staging = (a.dbg & 12) == 12;   // dev probe: one slot before, the rest after staging
+  // (dbg&12 == 4: the whole ring before the wait, whatever the range)
+  const int pre_slots = ((a.dbg & 12) == 4) ? NS : ((a.dbg & 8) || LL >= S8_PRE1_UNITS * NW) ? 1 : NS;
   if (lane == 0)
     for (int s = 0; s < pre_slots; ++s) issue(s);
   __syncwarp();
   griddep_launch_dependents();
   griddep_wait();   // x belongs to the previous kernel until here
+  if (trace) wait_clk = clock64();
   stamp(1);
   // the rest of the ring is issued right after this warp's first activation loads, so those
   // loads are not queued behind the weight stream
@@ -246,6 +253,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
           brs[t] = it & (nrx - 1);
           nv += item < n_items;
           s8_f8<T>(va[t], f[t]);
+          if (trace && i0 == warp && i == 0 && t == 0) {   // (dev probe: first loads landed)
+            asm volatile("" ::"f"(f[0][0]));
+            stamp(11);
+          }
           if (PRE == 2) {
             float up[8];
             s8_f8<T>(vb[t], up);
@@ -276,7 +287,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   stamp(8);
   __syncthreads();
   if (ring_after_staging && lane == 0)
-    for (int s = 0; s < NS; ++s) issue(s);
+    for (int s = pre_slots; s < NS; ++s) issue(s);
   stamp(2);
 
   // ---- main loop: units [wu0, wu1), tile by tile
