@@ -54,6 +54,39 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
       ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc));
 }
+// The 16 MMAs of one 256-column block (A: 16 x 8 TMEM columns from a_tmem; B: the block's four
+// 128B-swizzled 64-K atoms at b_smem, N rows each), issued by one elected lane in one asm block.
+// The first MMA accumulates iff acc0; the rest always do.
+template <int N>
+__device__ __forceinline__ void mma_block16(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_smem, uint32_t idesc,
+                                            int acc0) {
+  constexpr uint64_t kHi = (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+  uint64_t dsc[16];
+#pragma unroll
+  for (int kk = 0; kk < 16; ++kk)
+    dsc[kk] = kHi | (uint64_t)(((b_smem + (uint32_t)((kk >> 2) * N * 128 + (kk & 3) * 32)) >> 4) & 0x3FFFu);
+  asm volatile(
+      "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %19, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %2, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], %4, %2, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], %5, %2, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], %6, %2, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], %7, %2, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], %8, %2, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], %9, %2, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], %10, %2, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], %11, %2, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+72], %12, %2, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+80], %13, %2, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+88], %14, %2, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+96], %15, %2, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+104], %16, %2, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+112], %17, %2, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+120], %18, %2, 1;\n}\n"
+      ::"r"(d_tmem), "r"(a_tmem), "r"(idesc), "l"(dsc[0]), "l"(dsc[1]), "l"(dsc[2]), "l"(dsc[3]), "l"(dsc[4]),
+        "l"(dsc[5]), "l"(dsc[6]), "l"(dsc[7]), "l"(dsc[8]), "l"(dsc[9]), "l"(dsc[10]), "l"(dsc[11]), "l"(dsc[12]),
+        "l"(dsc[13]), "l"(dsc[14]), "l"(dsc[15]), "r"(acc0));
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
                "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n"
@@ -169,7 +202,9 @@ struct UmmaArgs {
   int rows, nb, batch;
   int m_tiles, n_tiles, ks;
   int uniform;        // every row has one scale for all its blocks
-  int dbg;            // development probes: 1 = skip MMAs, 2 = skip decode/TMEM stores
+  int dbg;            // development probes: 1 = skip MMAs, 2 = skip decode/TMEM stores, 4 = CTA 0 clock
+                      // trace into y (no output): per block, MMA warp [0] activations landed [1] A
+                      // decoded [2] MMAs issued; decode warp 0 [3] A buffer free [4] TMEM stores done
   int map3d;          // activations described by the 3-D tensor map (one TMA request per block)
   int out_f32;        // TR_LINEAR_OUT_F32: y is float32
 };
@@ -186,11 +221,20 @@ struct UmmaCfg {
   // N = 128: three 64 KB activation stages and two weight stages (exactly 227 KB).  The
   // activation ring's turnaround (commit -> refill -> landed) bounds the block rate, so its
   // depth matters more than the weight ring's
-  static constexpr int KS = N <= 32 ? 4 : 2;                 // 256-blocks per weight stage
-  static constexpr int RW = N <= 32 ? 4 : (N == 128 && UMMA_N128_RB == 3) ? 2 : 3;   // weight stages
+#ifndef UMMA_KS_SMALL
+#define UMMA_KS_SMALL 4
+#endif
+#ifndef UMMA_RW_SMALL
+#define UMMA_RW_SMALL 4
+#endif
+#ifndef UMMA_RB16
+#define UMMA_RB16 4
+#endif
+  static constexpr int KS = N <= 32 ? UMMA_KS_SMALL : 2;     // 256-blocks per weight stage
+  static constexpr int RW = N <= 32 ? UMMA_RW_SMALL : (N == 128 && UMMA_N128_RB == 3) ? 2 : 3;   // weight stages
   // (N = 32, 64: the spare shared memory goes to activation stages as well: +0.5-1.2% at b = 32-64;
   // N = 16 measured no gain from 8)
-  static constexpr int RB = N <= 16 ? 4 : N <= 64 ? 5 : UMMA_N128_RB;   // activation stages (one block each)
+  static constexpr int RB = N <= 16 ? UMMA_RB16 : N <= 64 ? 5 : UMMA_N128_RB;   // activation stages (one block each)
   static constexpr int kStageWBytes = 8 * KS * UB;          // 128 rows x KS blocks
   static constexpr int kStageBBytes = N * 512;               // N rows x 256 K (4 swizzled 64-K atoms)
   static constexpr int kMaxA = 3;                            // TMEM A buffers (128 columns = one block each)
@@ -328,22 +372,25 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
     constexpr uint32_t kFmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
     constexpr uint32_t idesc = (1u << 4) | (kFmt << 7) | (kFmt << 10) | ((uint32_t)(N >> 3) << 17) |
                                ((uint32_t)(kRowsPerCta >> 4) << 24);
+    // shared-window address of the activation stages from the (uniform) dynamic-smem base, so the
+    // MMA descriptors are computed in uniform registers rather than moved there once per MMA
+    const uint32_t sB32 = ((smem_u32(smem_raw) + 1023u) & ~1023u) + (uint32_t)Cfg::kBOff;
     {   // the whole warp runs the loop; each MMA / commit is issued by one elected lane
       for (int i = 0; i < nblk; ++i) {
         const int s = i % RB, ab = i % NA, db = i & 1;
         mbar_wait(&full_b[s], (i / RB) & 1);         // activations landed
+        if ((a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64)
+          reinterpret_cast<long long*>(a.y)[i * 8 + 0] = clock64();
         mbar_wait(&a_full[ab], (i / NA) & 1);        // trits decoded into TMEM
+        if ((a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64)
+          reinterpret_cast<long long*>(a.y)[i * 8 + 1] = clock64();
         if (per_block) mbar_wait(&d_empty[db], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = per_block ? tD + db * N : tD;
-        const uint8_t* b = sB + s * kStageB;
-        if (!(a.dbg & 1)) {
-#pragma unroll
-          for (int kk = 0; kk < 16; ++kk) {
-            const uint64_t bd = desc_sw128(b + (kk >> 2) * N * 128 + (kk & 3) * 32);
-            mma_ts(d, tA + ab * 128 + kk * 8, bd, idesc, (kk > 0 || (!per_block && i > 0)) ? 1 : 0);
-          }
-        }
+        if (!(a.dbg & 1))   // 16 MMAs (K = 256), one elect, descriptors in uniform registers
+          mma_block16<N>(d, tA + ab * 128, sB32 + s * kStageB, idesc, (!per_block && i > 0) ? 1 : 0);
+        if ((a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64)
+          reinterpret_cast<long long*>(a.y)[i * 8 + 2] = clock64();
         mma_commit(&empty_b[s]);                     // activation stage reusable once these MMAs finish
         mma_commit(&a_empty[ab]);                    // TMEM A buffer reusable
         if (per_block || i == nblk - 1) mma_commit(&d_full[per_block ? db : 0]);
@@ -402,6 +449,8 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
       }
       if (i == 0) s_first = s_cur;
       mbar_wait(&a_empty[ab], ((i / NA) & 1) ^ 1);      // MMA of block i-NA done with this A buffer
+      if ((a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0 && i < 64)
+        reinterpret_cast<long long*>(a.y)[i * 8 + 3] = clock64();
       tc_fence_after();
       if constexpr (FMT == kFmtTq1) {
         if (!(a.dbg & 2)) {
@@ -428,6 +477,8 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
         tmem_st32(tA + lane_off + ab * 128 + (2 * half_k + cc) * 32, col);
       }
       tmem_wait_st();
+      if ((a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0 && i < 64)
+        reinterpret_cast<long long*>(a.y)[i * 8 + 4] = clock64();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&a_full[ab]);
@@ -443,7 +494,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
     const int row = mt * kRowsPerCta + r;
     const int n0 = nt * N + half_k * NH;
     if (a.ks == 1) {
-      if (row < a.rows)
+      if (row < a.rows && !(a.dbg & 4))
 #pragma unroll
         for (int e = 0; e < NH; ++e)
           if (n0 + e < a.batch) store_y<T>(a.y, (int64_t)(n0 + e) * a.ldy + row, acc[e], a.out_f32);
