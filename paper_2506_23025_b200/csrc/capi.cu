@@ -39,13 +39,27 @@ int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t l
               int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg,
               int out_f32);
 size_t umma_workspace_bytes(int batch, int rows, int cols);
+int umma_blocks_per_cta(int batch, int rows, int cols);
 bool gemv_stages_x(int batch, int rows, int cols);
 int gemv_chain_s8(int act, const TrChainLayer* host, int n, int batch, void* ws, size_t ws_bytes, int flags,
                   cudaStream_t st, bool upload);
 size_t chain_workspace_bytes(int n_ops);
 
-// batch at which the tensor-core (tcgen05) GEMM takes over from the mma.sync GEMV
-constexpr int64_t kUmmaMinBatch = 9;
+// GEMV / tensor-core GEMM crossover, measured per shape at batch 2-12 (scripts/dev/crossover.py,
+// DESIGN.md section 4 "Dispatch"): the GEMVs restage every activation row in every CTA, so their
+// cost grows with batch x cols; K5 costs about the same for any batch up to 16 but pays a fixed
+// ~3.5 us per CTA and spreads poorly when a shape has few 128-row tiles.
+//  * batch <= 2: the int8-slice GEMV;
+//  * batch 3-4: the int8-slice GEMV while K <= 4096 columns, else K5;
+//  * batch 5-8: the fp16 GEMV only for K <= 4096 columns on shapes K5 spreads badly (>= 12
+//    blocks per CTA, e.g. 11008 x 4096), else K5;
+//  * batch >= 9: K5.
+static bool prefer_umma(int64_t batch, int64_t rows, int64_t cols) {
+  if (batch <= 2) return false;
+  if (batch <= 4) return cols > 4096;
+  if (batch <= 8) return cols > 4096 || umma_blocks_per_cta((int)batch, (int)rows, (int)cols) < 12;
+  return true;
+}
 
 }  // namespace tr
 
@@ -84,16 +98,16 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
   const int knob = (flags >> 8) & 0xFFFF;   // GEMV: CTA count; UMMA: K split (0 = automatic)
   cudaStream_t st = (cudaStream_t)stream;
   const bool aligned = (ldx % 8) == 0 && ((uintptr_t)x & 15) == 0;
-  const bool s8 = batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols, fmt);
+  const bool s8 = batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols, fmt) &&
+                  (fmt == kFmtTq2 || !prefer_umma(batch, rows, cols) || (flags & TR_LINEAR_FORCE_GEMV));
   if (epi) {   // only the int8-slice GEMV knows the gate/up tile pairing: never fall through to another path
     TR_REQUIRE(fmt == kFmtTq2 && s8 && !(flags & TR_LINEAR_FORCE_UMMA),
                "tr_linear: the SwiGLU epilogue runs on the int8-slice GEMV only (TQ2, batch <= 4)");
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, pdl, st, 0, nullptr, nullptr,
                    nullptr, 0.0f, (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, 1, 0, kFmtTq2);
   }
-  // measured crossover (scripts/dev/gemv_sweep.py): the mma.sync GEMV wins at batch 1-2 and,
-  // while it can stage the activations in shared memory, up to 8; the tensor-core GEMM beyond
-  bool use_umma = aligned && (batch >= kUmmaMinBatch || (batch >= 3 && !gemv_stages_x((int)batch, (int)rows, (int)cols)));
+  bool use_umma = aligned && (prefer_umma(batch, rows, cols) ||
+                               (batch >= 3 && batch <= 8 && !gemv_stages_x((int)batch, (int)rows, (int)cols)));
   if (flags & TR_LINEAR_FORCE_UMMA) {
     TR_REQUIRE(aligned, "tr_linear: the tensor-core path needs 16-byte aligned activation rows");
     use_umma = true;

@@ -580,6 +580,13 @@ static UmmaPlan plan_umma(int batch, int rows, int cols, int ks_force, int sms) 
   return p;
 }
 
+// 256-blocks of K each K5 CTA walks for this product (its split-K share): the dispatcher's
+// measure of how well the tensor-core GEMM spreads a shape over the SMs
+int umma_blocks_per_cta(int batch, int rows, int cols) {
+  const UmmaPlan p = plan_umma(batch, rows, cols, 0, sm_count());
+  return (int)ceil_div(ceil_div(cols, kBlock), p.ks);
+}
+
 size_t umma_workspace_bytes(int batch, int rows, int cols) {
   size_t ws = 0;
   for (int ks = 0; ks <= 16; ++ks) {
