@@ -387,8 +387,21 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
         if (per_block) mbar_wait(&d_empty[db], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = per_block ? tD + db * N : tD;
-        if (!(a.dbg & 1))   // 16 MMAs (K = 256), one elect, descriptors in uniform registers
-          mma_block16<N>(d, tA + ab * 128, sB32 + s * kStageB, idesc, (!per_block && i > 0) ? 1 : 0);
+#ifndef UMMA_MMA_ASM16
+#define UMMA_MMA_ASM16 32   // widest N issued as one asm block (measured: +3% at N = 16, -4% at N >= 64)
+#endif
+        if (!(a.dbg & 1)) {
+          if (N <= UMMA_MMA_ASM16) {   // 16 MMAs (K = 256) from one asm block, one elect
+            mma_block16<N>(d, tA + ab * 128, sB32 + s * kStageB, idesc, (!per_block && i > 0) ? 1 : 0);
+          } else {
+            const uint8_t* b = sB + s * kStageB;
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) {
+              const uint64_t bd = desc_sw128(b + (kk >> 2) * N * 128 + (kk & 3) * 32);
+              mma_ts(d, tA + ab * 128 + kk * 8, bd, idesc, (kk > 0 || (!per_block && i > 0)) ? 1 : 0);
+            }
+          }
+        }
         if ((a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64)
           reinterpret_cast<long long*>(a.y)[i * 8 + 2] = clock64();
         mma_commit(&empty_b[s]);                     // activation stage reusable once these MMAs finish

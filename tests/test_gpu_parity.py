@@ -229,8 +229,16 @@ def test_linear_padding_neutrality_and_batch_order(tp):
     x = torch.from_numpy(rng.normal(size=(5, 300)).astype(np.float32)).half().cuda()
     xpad = torch.zeros(5, 512, dtype=torch.float16, device="cuda")
     xpad[:, :300] = x
-    y = tp.linear(x, tp.pack_matrix(W, tp.DType.TQ2).to_device())
-    ypad = tp.linear(xpad, tp.pack_matrix(Wpad, tp.DType.TQ2).to_device())
+    # (per kernel: 300-column rows are not 16-byte aligned, so the automatic dispatch may take the
+    # GEMV for x and the tensor-core GEMM for the padded twin -- different but each exact-order sums)
+    for path, b in (("gemv", 5), ("gemv", 2), ("auto", 2)):
+        y = tp.linear(x[:b], tp.pack_matrix(W, tp.DType.TQ2).to_device(), path=path)
+        ypad = tp.linear(xpad[:b], tp.pack_matrix(Wpad, tp.DType.TQ2).to_device(), path=path)
+        assert torch.equal(y, ypad), (path, b)
+    xa = torch.zeros(5, 304, dtype=torch.float16, device="cuda")[:, :300]   # 16-byte aligned rows
+    xa.copy_(x)
+    y = tp.linear(xa, tp.pack_matrix(W, tp.DType.TQ2).to_device(), path="umma")
+    ypad = tp.linear(xpad, tp.pack_matrix(Wpad, tp.DType.TQ2).to_device(), path="umma")
     assert torch.equal(y, ypad)
     perm = torch.tensor([3, 0, 4, 1, 2], device="cuda")
     w = tp.pack_matrix(W, tp.DType.TQ2).to_device()
