@@ -106,10 +106,31 @@ class CpuReference:
             times.append(time.perf_counter() - t0)
         med = statistics.median(times)
         return {"value": round(self.nbytes / med / 1e9, 4), "unit": "GB/s", "cores": self.threads,
-                "kind": self.kind,
+                "kind": self.kind, "host_cpu": host_cpu(),
                 "sample": f"{len(times)} passes of one replica (4096x4096, 11008x4096, 4096x11008 TQ2) at batch 1 "
                           f"(median {med * 1e3:.1f} ms/pass), {self.threads} host threads, reference "
                           f"gemm_tq2 under the linear.gemm row-sharding harness"}
+
+
+def host_cpu():
+    """The host CPU the CPU baselines run on: model name, logical CPUs, physical cores."""
+    model, phys = "unknown", set()
+    try:
+        cur = {}
+        for line in open("/proc/cpuinfo"):
+            if ":" in line:
+                k, v = (t.strip() for t in line.split(":", 1))
+                cur[k] = v
+                if k == "model name":
+                    model = v
+            elif cur:
+                phys.add((cur.get("physical id"), cur.get("core id")))
+                cur = {}
+        if cur:
+            phys.add((cur.get("physical id"), cur.get("core id")))
+    except OSError:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count(), "physical_cores": len(phys) or None}
 
 
 def run_reference(args, rank):
@@ -124,7 +145,7 @@ def run_reference(args, rank):
         ref.one_pass()
     dt = time.perf_counter() - t0
     value = round(ref.nbytes * args.steps / dt / 1e9, 4)
-    cpu = {"value": value, "unit": "GB/s", "cores": ref.threads, "kind": ref.kind,
+    cpu = {"value": value, "unit": "GB/s", "cores": ref.threads, "kind": ref.kind, "host_cpu": host_cpu(),
            "sample": f"{args.steps} timed passes of one replica of the stack at batch 1 (each step a bounded "
                      f"sample of the llama_linear_stack workload), {ref.threads} threads"}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
@@ -540,7 +561,8 @@ def run_ours(args, rank, world, dist):
     e2e_ms = timed_graph(lambda: stack.run_host(x_host, y_host), args.steps, args.warmup, dist) / args.steps
     e2e = {"value": round(world * nbytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
            "h2d_bytes_per_step": x_host.numel() * 2, "d2h_bytes_per_step": y_host.numel() * 2,
-           "ms_per_step": round(e2e_ms, 4)}
+           "ms_per_step": round(e2e_ms, 4),
+           "method": "per step: pinned H2D of x, graph replay, D2H of y, host synchronize (the caller holds y)"}
 
     # ---- batch sweep vs cuBLAS fp16 (rank-local)
     sweep = []

@@ -88,15 +88,17 @@ TR_API int tr_quantize_pack(int fmt, const float* W, int64_t rows, int64_t cols,
                             uint16_t* scales_f16, void* stream);
 /* bytes of the device ("T16") layout of a rows x cols matrix (-1 if unsupported) */
 TR_API int64_t tr_layout_bytes(int fmt, int64_t rows, int64_t cols);
-/* PackedMatrix (linear.py:29-95: payload + scales) -> device layout; bit-exactly invertible */
+/* PackedMatrix (linear.py:29-95: payload + scales) -> device layout; bit-exactly invertible.
+ * dst_bytes: the size of dst (>= tr_layout_bytes(fmt, rows, cols), else -1 and nothing is written) */
 TR_API int tr_repack(int fmt, const uint8_t* payload, const uint16_t* scales_f16, int64_t rows, int64_t cols,
-                     void* dst, void* stream);
+                     void* dst, size_t dst_bytes, void* stream);
 /* device layout -> PackedMatrix payload + scales (exact inverse of tr_repack) */
 /* TPK1 container (container.py:73-82, 167-242) -> device tiles in one pass: records = the
  * data section of one TQ2/TQ1 tensor on the device, rows x ceil(cols/256) records of
  * payload (64|52 B) followed by its binary16 scale (66|54 B each, no padding). */
-TR_API int tr_repack_records(int fmt, const uint8_t* records, int64_t rows, int64_t cols, void* dst, void* stream);
-TR_API int tr_unrepack(int fmt, const void* src, int64_t rows, int64_t cols, uint8_t* payload,
+TR_API int tr_repack_records(int fmt, const uint8_t* records, int64_t rows, int64_t cols, void* dst,
+                             size_t dst_bytes, void* stream);
+TR_API int tr_unrepack(int fmt, const void* src, int64_t rows, int64_t cols, size_t src_bytes, uint8_t* payload,
                        uint16_t* scales_f16, void* stream);
 /* linear.py:177-198 dequantize_matrix, to a dense fp16/bf16 [rows, cols] matrix
  * (values scale*(d-1) are exact in fp16); feeds the cuBLAS baseline. */

@@ -58,11 +58,11 @@ _SIGS = {
     "tr_gemm_exact": ([_int, _c_p, _c_p, _c_p, _c_p, _i64, _i64, _i64, _i64, _i64, _c_p], _int),
     "tr_quantize_pack": ([_int, _c_p, _i64, _i64, _c_p, _c_p, _c_p], _int),
     "tr_layout_bytes": ([_int, _i64, _i64], _i64),
-    "tr_repack": ([_int, _c_p, _c_p, _i64, _i64, _c_p, _c_p], _int),
-    "tr_unrepack": ([_int, _c_p, _i64, _i64, _c_p, _c_p, _c_p], _int),
+    "tr_repack": ([_int, _c_p, _c_p, _i64, _i64, _c_p, ctypes.c_size_t, _c_p], _int),
+    "tr_unrepack": ([_int, _c_p, _i64, _i64, ctypes.c_size_t, _c_p, _c_p, _c_p], _int),
     "tr_dequant_dense": ([_int, _c_p, _c_p, _i64, _i64, _int, _c_p, _c_p], _int),
     "tr_linear_workspace_size": ([_int, _i64, _i64, _i64], ctypes.c_size_t),
-    "tr_repack_records": ([_int, _c_p, _i64, _i64, _c_p, _c_p], _int),
+    "tr_repack_records": ([_int, _c_p, _i64, _i64, _c_p, ctypes.c_size_t, _c_p], _int),
     "tr_linear": ([_int, _c_p, _c_p, _c_p, _i64, _i64, _i64, _int, _i64, _i64, _int, _c_p, ctypes.c_size_t,
                    _c_p], _int),
     "tr_linear_pre": ([_int, _c_p, _c_p, _c_p, _i64, _i64, _i64, _int, _i64, _i64, _int, _int, _c_p, _c_p, _c_p,

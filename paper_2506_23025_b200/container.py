@@ -151,7 +151,7 @@ def record_to_device(rec: TensorRecord, device="cuda"):
     data = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     with torch.cuda.device(dev):
         _lib.call("tr_repack_records", int(rec.dtype), records.data_ptr(), rows, cols, data.data_ptr(),
-                  _lib.stream_handle())
+                  data.numel(), _lib.stream_handle())
     nb, pb = -(-cols // BLOCK_ELEMENTS), rec.dtype.payload_bytes
     sbytes = records.view(rows, nb, pb + 2)[:, :, pb:]   # the scales' two bytes, in place
     s = (sbytes[..., 0].to(torch.int32) | (sbytes[..., 1].to(torch.int32) << 8))

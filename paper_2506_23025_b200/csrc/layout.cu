@@ -190,10 +190,12 @@ int64_t tr_layout_bytes(int fmt, int64_t rows, int64_t cols) {
   return -1;
 }
 
-static int repack_from(int fmt, const RepackSrc& src, int64_t rows, int64_t cols, void* dst, cudaStream_t st,
-                       const char* what) {
+static int repack_from(int fmt, const RepackSrc& src, int64_t rows, int64_t cols, void* dst, size_t dst_bytes,
+                       cudaStream_t st, const char* what) {
   TR_REQUIRE(fmt == kFmtTq2 || fmt == kFmtTq1, "%s: fmt must be TQ2 (2) or TQ1 (3), got %d", what, fmt);
   TR_REQUIRE(rows >= 1 && cols >= 1, "%s: matrix must be non-empty", what);
+  TR_REQUIRE(dst_bytes >= (size_t)tr_layout_bytes(fmt, rows, cols), "%s: dst holds %zu bytes, the layout needs %lld",
+             what, dst_bytes, (long long)tr_layout_bytes(fmt, rows, cols));
   TR_REQUIRE(((uintptr_t)dst & 15) == 0 && ((uintptr_t)src.sbase & 1) == 0, "%s: misaligned buffers", what);
   const int64_t nb = ceil_div(cols, kBlock);
   if (fmt == kFmtTq1) {
@@ -211,21 +213,24 @@ static int repack_from(int fmt, const RepackSrc& src, int64_t rows, int64_t cols
 }
 
 int tr_repack(int fmt, const uint8_t* payload, const uint16_t* scales_f16, int64_t rows, int64_t cols, void* dst,
-              void* stream) {
+              size_t dst_bytes, void* stream) {
   const RepackSrc src = {payload, fmt == kFmtTq1 ? kTq1Payload : kTq2Payload, (const uint8_t*)scales_f16, 2};
-  return repack_from(fmt, src, rows, cols, dst, (cudaStream_t)stream, "tr_repack");
+  return repack_from(fmt, src, rows, cols, dst, dst_bytes, (cudaStream_t)stream, "tr_repack");
 }
 
-int tr_repack_records(int fmt, const uint8_t* records, int64_t rows, int64_t cols, void* dst, void* stream) {
+int tr_repack_records(int fmt, const uint8_t* records, int64_t rows, int64_t cols, void* dst, size_t dst_bytes,
+                      void* stream) {
   const int64_t pb = fmt == kFmtTq1 ? kTq1Payload : kTq2Payload;
   const RepackSrc src = {records, pb + 2, records + pb, pb + 2};
-  return repack_from(fmt, src, rows, cols, dst, (cudaStream_t)stream, "tr_repack_records");
+  return repack_from(fmt, src, rows, cols, dst, dst_bytes, (cudaStream_t)stream, "tr_repack_records");
 }
 
-int tr_unrepack(int fmt, const void* src, int64_t rows, int64_t cols, uint8_t* payload, uint16_t* scales_f16,
-                void* stream) {
+int tr_unrepack(int fmt, const void* src, int64_t rows, int64_t cols, size_t src_bytes, uint8_t* payload,
+                uint16_t* scales_f16, void* stream) {
   TR_REQUIRE(fmt == kFmtTq2 || fmt == kFmtTq1, "tr_unrepack: fmt must be TQ2 (2) or TQ1 (3), got %d", fmt);
   TR_REQUIRE(rows >= 1 && cols >= 1, "tr_unrepack: matrix must be non-empty");
+  TR_REQUIRE(src_bytes >= (size_t)tr_layout_bytes(fmt, rows, cols), "tr_unrepack: src holds %zu bytes, the layout "
+             "needs %lld", src_bytes, (long long)tr_layout_bytes(fmt, rows, cols));
   if (fmt == kFmtTq1) {
     const int64_t nb = ceil_div(cols, kBlock);
     const int grid = (int)(ceil_div(rows * nb, 128) > 148 * 32 ? 148 * 32 : ceil_div(rows * nb, 128));

@@ -70,7 +70,7 @@ class TernaryWeight:
             raise NotImplementedError(f"{fmt.name} has no device layout yet")
         data = torch.empty(nbytes, dtype=torch.uint8, device=payload.device)
         _lib.call("tr_repack", int(fmt), payload.data_ptr(), scales_f16.data_ptr(), rows, cols, data.data_ptr(),
-                  _lib.stream_handle())
+                  data.numel(), _lib.stream_handle())
         s = scales_f16.view(torch.int16).reshape(rows, -1)
         uniform = bool((s == s[:, :1]).all())
         return cls(data, rows, cols, fmt, uniform_scale=uniform)
@@ -110,7 +110,8 @@ class TernaryWeight:
         nb = self.blocks_per_row
         payload = torch.empty((self.rows, nb, self.fmt.payload_bytes), dtype=torch.uint8, device=self.data.device)
         scales = torch.empty((self.rows, nb), dtype=torch.float16, device=self.data.device)
-        _lib.call("tr_unrepack", int(self.fmt), self.data.data_ptr(), self.rows, self.cols, payload.data_ptr(),
+        _lib.call("tr_unrepack", int(self.fmt), self.data.data_ptr(), self.rows, self.cols, self.data.numel(),
+                  payload.data_ptr(),
                   scales.data_ptr(), _lib.stream_handle())
         return payload, scales
 

@@ -145,7 +145,9 @@ class LinearStack:
         self.graph.replay()
 
     def run_host(self, x_host: torch.Tensor, y_host: torch.Tensor) -> None:
-        """End-to-end: pinned host x -> device, graph replay, device -> pinned host y (async on the current stream)."""
+        """End-to-end, as a caller sees it: pinned host x -> device, graph replay, device -> pinned host
+        y, and the host waits until y is there (returns with the result readable)."""
         self.x.copy_(x_host, non_blocking=True)
         self.graph.replay()
         y_host.copy_(self.out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
