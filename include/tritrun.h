@@ -182,6 +182,13 @@ TR_API int tr_rope_kv(int act_dtype, const void* qkv, const int64_t* pos, const 
 TR_API int tr_attn_decode(int act_dtype, const void* qkv, const int64_t* pos, const void* cos_t, const void* sin_t,
                           void* k_cache, void* v_cache, void* out, int64_t heads, int64_t head_dim, int64_t max_seq,
                           float scale, void* stream);
+/* tr_attn_decode for any cache length (split-KV: 128 keys per CTA, partial softmaxes merged in a
+ * second kernel); workspace: tr_attn_decode_workspace_size bytes of device memory (no init needed) */
+TR_API size_t tr_attn_decode_workspace_size(int64_t heads, int64_t head_dim, int64_t max_seq);
+TR_API int tr_attn_decode_split(int act_dtype, const void* qkv, const int64_t* pos, const void* cos_t,
+                                const void* sin_t, void* k_cache, void* v_cache, void* out, int64_t heads,
+                                int64_t head_dim, int64_t max_seq, float scale, void* workspace, size_t ws_bytes,
+                                void* stream);
 /* gu [T, 2F] = (gate | up) -> out [T, F] = silu(gate) * up */
 TR_API int tr_silu_mul(int act_dtype, const void* gu, void* out, int64_t tokens, int64_t ff, void* stream);
 /* greedy decode step: idx = argmax(logits [vocab]) (lowest index among ties); out_tokens[pos[0]] = idx

@@ -245,6 +245,142 @@ __global__ void __launch_bounds__(128) k_attn_decode(const T* __restrict__ qkv, 
   out[(int64_t)hh * D + tid] = Act<T>::from_float(r);
 }
 
+// Long caches (max_seq > 128): split-KV decode attention.  CTA (head hh, chunk c) scores keys
+// [128 c, 128 c + 128) ∩ [0, pos] (thread t <-> key 128 c + t) and leaves a partial softmax
+// {max, sum, sum_k e_k v_k[0..D)} in the workspace; the CTA whose chunk holds pos also rotates
+// this token's key and appends k/v to the caches.  k_attn_combine merges the partials of a head
+// (rescaling each by exp(m_c - M)).  Same roundings as k_attn_decode for q, k and the output.
+template <typename T, int D>
+__global__ void __launch_bounds__(128) k_attn_split(const T* __restrict__ qkv, const int64_t* __restrict__ pos,
+                                                    const T* __restrict__ cs, const T* __restrict__ sn,
+                                                    T* __restrict__ kc, T* __restrict__ vc, float* __restrict__ ws,
+                                                    int H, int S, float scale) {
+  static_assert(D == 128, "one key per thread, 4 dims per lane");
+  __shared__ __align__(16) T vs[128][D];
+  __shared__ __align__(16) T kp[D];
+  __shared__ float qs[D];
+  __shared__ float sc[128];
+  __shared__ float part[4][D];
+  __shared__ float red[32];
+  const int hh = blockIdx.x, ch = blockIdx.y, NC = gridDim.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  float* wp = ws + ((int64_t)hh * NC + ch) * (D + 2);
+  griddep_wait();
+  griddep_launch_dependents();
+  const int64_t p64 = pos[0];
+  const int c0 = ch * 128;
+  if (p64 < 0 || p64 >= S || c0 > p64) {   // no keys of this chunk are live (or pos is past the cache)
+    if (tid == 0) {
+      wp[0] = -INFINITY;
+      wp[1] = 0.0f;
+    }
+    wp[2 + tid] = 0.0f;
+    return;
+  }
+  const int p = (int)p64;
+  const int nk = (p - c0 + 1) < 128 ? (p - c0 + 1) : 128;   // live keys in this chunk
+  const bool own = p - c0 < 128;                              // this chunk holds the token itself
+  const T* kb = kc + ((int64_t)hh * S + c0) * D;
+  const T* vb = vc + ((int64_t)hh * S + c0) * D;
+  for (int c = tid; c < nk * (D / 8); c += 128) {
+    if (!(own && c / (D / 8) == p - c0)) cp_async16(&vs[c / (D / 8)][(c % (D / 8)) * 8], vb + (int64_t)c * 8);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  uint4 kv[D / 8];
+  if (tid < nk && !(own && tid == p - c0)) {
+    const uint4* kr = reinterpret_cast<const uint4*>(kb + (int64_t)tid * D);
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) kv[j] = kr[j];
+  }
+  if (tid < D / 2) {
+    const float c = to_f(cs[(int64_t)p * (D / 2) + tid]), s = to_f(sn[(int64_t)p * (D / 2) + tid]);
+    const float q1 = to_f(qkv[hh * D + 2 * tid]), q2 = to_f(qkv[hh * D + 2 * tid + 1]);
+    qs[2 * tid] = to_f(Act<T>::from_float(q1 * c - q2 * s));
+    qs[2 * tid + 1] = to_f(Act<T>::from_float(q1 * s + q2 * c));
+    if (own) {
+      const float k1 = to_f(qkv[(H + hh) * D + 2 * tid]), k2 = to_f(qkv[(H + hh) * D + 2 * tid + 1]);
+      const T v1 = qkv[(2 * H + hh) * D + 2 * tid], v2 = qkv[(2 * H + hh) * D + 2 * tid + 1];
+      const T r1 = Act<T>::from_float(k1 * c - k2 * s), r2 = Act<T>::from_float(k1 * s + k2 * c);
+      kp[2 * tid] = r1;
+      kp[2 * tid + 1] = r2;
+      vs[p - c0][2 * tid] = v1;
+      vs[p - c0][2 * tid + 1] = v2;
+      T* ko = kc + ((int64_t)hh * S + p) * D;
+      ko[2 * tid] = r1;
+      ko[2 * tid + 1] = r2;
+      T* vo = vc + ((int64_t)hh * S + p) * D;
+      vo[2 * tid] = v1;
+      vo[2 * tid + 1] = v2;
+    }
+  }
+  __syncthreads();
+  float v = -INFINITY;
+  if (tid < nk) {
+    if (own && tid == p - c0) {
+#pragma unroll
+      for (int j = 0; j < D / 8; ++j) kv[j] = reinterpret_cast<const uint4*>(kp)[j];
+    }
+    float acc = 0.0f;
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) {
+      float kf[8];
+      unpack8<T>(kv[j], kf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc += qs[8 * j + e] * kf[e];
+    }
+    v = acc * scale;
+  }
+  float m = v;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  m = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  const float e = tid < nk ? __expf(v - m) : 0.0f;
+  sc[tid] = e;
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  const float z = block_sum(e, red);
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  for (int s0 = warp; s0 < nk; s0 += 4) {
+    const uint2 vv = *reinterpret_cast<const uint2*>(&vs[s0][4 * lane]);
+    const T* ve = reinterpret_cast<const T*>(&vv);
+    const float w = sc[s0];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] += w * to_f(ve[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) part[warp][4 * lane + q] = acc[q];
+  __syncthreads();
+  wp[2 + tid] = (part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid]);
+  if (tid == 0) {
+    wp[0] = m;
+    wp[1] = z;
+  }
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(128) k_attn_combine(const float* __restrict__ ws, const int64_t* __restrict__ pos,
+                                                      T* __restrict__ out, int NC, int S) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int hh = blockIdx.x, tid = threadIdx.x;
+  const float* wh = ws + (int64_t)hh * NC * (D + 2);
+  if (pos[0] < 0 || pos[0] >= S) {
+    out[(int64_t)hh * D + tid] = Act<T>::from_float(0.0f);
+    return;
+  }
+  float M = -INFINITY;
+  for (int c = 0; c < NC; ++c) M = fmaxf(M, wh[c * (D + 2)]);
+  float L = 0.0f, a = 0.0f;
+  for (int c = 0; c < NC; ++c) {   // chunk order: fixed, deterministic
+    const float mc = wh[c * (D + 2)];
+    if (mc == -INFINITY) continue;
+    const float f = __expf(mc - M);
+    L += wh[c * (D + 2) + 1] * f;
+    a += wh[c * (D + 2) + 2 + tid] * f;
+  }
+  out[(int64_t)hh * D + tid] = Act<T>::from_float(a / L);
+}
+
 // Greedy decode bookkeeping in one kernel (one CTA of 1024 threads): idx = argmax(logits)
 // (lowest index among equal maxima), out_tokens[pos] = idx, tok = idx, pos += 1, and the next
 // token's embedding row h_next = embed[idx] -- replacing argmax + index_copy + add + the
@@ -430,6 +566,38 @@ int tr_attn_decode(int act, const void* qkv, const int64_t* pos, const void* cos
                               (const __nv_bfloat16*)sin_t, (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache,
                               (__nv_bfloat16*)out, (int)heads, (int)max_seq, scale)));
   return check_launch("tr_attn_decode");
+}
+
+size_t tr_attn_decode_workspace_size(int64_t heads, int64_t head_dim, int64_t max_seq) {
+  if (heads < 1 || head_dim != 128 || max_seq < 1) return 0;
+  return (size_t)heads * ceil_div(max_seq, 128) * (head_dim + 2) * sizeof(float);
+}
+
+int tr_attn_decode_split(int act, const void* qkv, const int64_t* pos, const void* cos_t, const void* sin_t,
+                         void* k_cache, void* v_cache, void* out, int64_t heads, int64_t head_dim, int64_t max_seq,
+                         float scale, void* workspace, size_t ws_bytes, void* stream) {
+  TR_REQUIRE(head_dim == 128, "tr_attn_decode_split: head_dim must be 128");
+  TR_REQUIRE(heads >= 1 && max_seq >= 1 && max_seq < (1LL << 24), "tr_attn_decode_split: bad heads / max_seq");
+  TR_REQUIRE(workspace && ws_bytes >= tr_attn_decode_workspace_size(heads, head_dim, max_seq),
+             "tr_attn_decode_split: workspace too small (tr_attn_decode_workspace_size)");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nc = (int)ceil_div(max_seq, 128);
+  float* ws = (float*)workspace;
+  TR_ACT_DISPATCH(act,
+                  (launch_pdl(k_attn_split<__half, 128>, dim3((int)heads, nc), dim3(128), 0, st, (const __half*)qkv,
+                              pos, (const __half*)cos_t, (const __half*)sin_t, (__half*)k_cache, (__half*)v_cache, ws,
+                              (int)heads, (int)max_seq, scale)),
+                  (launch_pdl(k_attn_split<__nv_bfloat16, 128>, dim3((int)heads, nc), dim3(128), 0, st,
+                              (const __nv_bfloat16*)qkv, pos, (const __nv_bfloat16*)cos_t,
+                              (const __nv_bfloat16*)sin_t, (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, ws,
+                              (int)heads, (int)max_seq, scale)));
+  if (check_launch("tr_attn_decode_split")) return -1;
+  TR_ACT_DISPATCH(act,
+                  (launch_pdl(k_attn_combine<__half, 128>, dim3((int)heads), dim3(128), 0, st, (const float*)ws, pos,
+                              (__half*)out, nc, (int)max_seq)),
+                  (launch_pdl(k_attn_combine<__nv_bfloat16, 128>, dim3((int)heads), dim3(128), 0, st,
+                              (const float*)ws, pos, (__nv_bfloat16*)out, nc, (int)max_seq)));
+  return check_launch("tr_attn_decode_split(combine)");
 }
 
 int tr_silu_mul(int act, const void* gu, void* out, int64_t tokens, int64_t ff, void* stream) {

@@ -105,6 +105,8 @@ class TernaryDecoder:
         self.norm_out = torch.ones(d, device=self.device, dtype=dtype)
         H, D, S = cfg.n_heads, cfg.head_dim, cfg.max_seq
         self.k_cache = torch.zeros((L, H, S, D), device=self.device, dtype=dtype)
+        self._attn_ws = torch.empty(max(1, _lib.lib().tr_attn_decode_workspace_size(H, D, S)), dtype=torch.uint8,
+                                    device=self.device)
         self.v_cache = torch.zeros((L, H, S, D), device=self.device, dtype=dtype)
         inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, D, 2, device=self.device).float() / D))
         ang = torch.arange(S, device=self.device).float()[:, None] * inv[None, :]
@@ -227,8 +229,14 @@ class TernaryDecoder:
                              cfg.eps, pdl=True, cosched=cs[0])
             cur = 1 - cur
             att = torch.empty((1, d), device=self.device, dtype=self.dtype)
-            _lib.call("tr_attn_decode", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(), self.sin.data_ptr(),
-                      self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(), H, D, S, D ** -0.5, st)
+            if S <= 128:   # one CTA per head holds the whole cache
+                _lib.call("tr_attn_decode", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(),
+                          self.sin.data_ptr(), self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(),
+                          H, D, S, D ** -0.5, st)
+            else:          # split-KV over 128-key chunks, partial softmaxes merged
+                _lib.call("tr_attn_decode_split", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(),
+                          self.sin.data_ptr(), self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(),
+                          H, D, S, D ** -0.5, self._attn_ws.data_ptr(), self._attn_ws.numel(), st)
             o = linear(att, lw["o"], pdl=True, cosched=cs[1])
             if self.gate_up_il is not None:   # SwiGLU in the gate|up GEMV's epilogue
                 act_ = linear_pre(hs[cur], self.gate_up_il[i], _lib.PRE_ADD_RMSNORM, o, self.norm_mlp[i],

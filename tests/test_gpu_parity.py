@@ -387,6 +387,43 @@ def test_decoder_fused_glue_matches_torch_glue(tp, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
+def test_decoder_long_cache_split_attention(tp, dtype):
+    """max_seq > 128: decode attention runs split-KV (tr_attn_decode_split) -- vs the unfused torch
+    glue (SDPA over the cache) at positions inside, at and across 128-key chunk boundaries."""
+    from paper_2506_23025_b200.decoder import DecoderConfig, TernaryDecoder
+
+    tdt = getattr(torch, dtype)
+    cfg = DecoderConfig(d_model=512, n_layers=2, n_heads=4, d_ff=1536, vocab=1000, max_seq=640)
+    fused = TernaryDecoder(cfg, seed=5, dtype=tdt)
+    ref = TernaryDecoder(cfg, weights=fused.weights, fused=False, dtype=tdt)
+    tol = 2e-2 if dtype == "bfloat16" else 5e-3
+    T0 = 126
+    prompt = torch.randint(0, cfg.vocab, (T0,), device="cuda")
+    pos = torch.arange(T0, device="cuda")
+    fused.forward(prompt, pos)
+    ref.forward(prompt, pos)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    p = T0
+    for step in range(8):   # positions 126..133: the chunk boundary at 128
+        t1 = torch.randint(0, cfg.vocab, (1,), device="cuda", generator=g)
+        p1 = torch.tensor([p], device="cuda")
+        a, b = fused.forward(t1, p1).float(), ref.forward(t1, p1).float()
+        assert ((a - b).abs().max() / b.abs().max()).item() <= tol, p
+        p += 1
+    # far into the cache: jump both to position 511 (fill the skipped rows identically first)
+    fused.k_cache[:, :, p:511].copy_(ref.k_cache[:, :, p:511].normal_(0, 0.5))
+    fused.v_cache[:, :, p:511].copy_(ref.v_cache[:, :, p:511].normal_(0, 0.5))
+    for p in (511, 512, 639):
+        t1 = torch.randint(0, cfg.vocab, (1,), device="cuda", generator=g)
+        p1 = torch.tensor([p], device="cuda")
+        a, b = fused.forward(t1, p1).float(), ref.forward(t1, p1).float()
+        assert ((a - b).abs().max() / b.abs().max()).item() <= tol, p
+        if p == 512:
+            fused.k_cache[:, :, 513:639].copy_(ref.k_cache[:, :, 513:639].normal_(0, 0.5))
+            fused.v_cache[:, :, 513:639].copy_(ref.v_cache[:, :, 513:639].normal_(0, 0.5))
+
+
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
 def test_greedy_next_kernel(tp, dtype):
     from paper_2506_23025_b200 import _lib
     from paper_2506_23025_b200.device import _ACT
@@ -431,6 +468,26 @@ def test_decoder_graph_decode_matches_eager_greedy(tp):
 
 
 # ---------------------------------------------------------------- TQ1 (1.6-bit) decoded on the fly (config 4)
+
+@pytest.mark.parametrize("fmt", [2, 3])
+@pytest.mark.parametrize("path,batch", [("gemv", 1), ("gemv", 3), ("gemv_f16", 6), ("umma", 16), ("auto", 40)])
+def test_linear_out_f32_every_path(tp, fmt, path, batch):
+    """TR_LINEAR_OUT_F32 (row-parallel partials): the fp32 accumulators on every kernel, equal to the
+    fp16 output before its final rounding (the fp16 result is their RNE rounding), vs the oracle."""
+    if fmt == 3 and path == "gemv_f16":
+        pytest.skip("TQ1 has no fp16 mma.sync GEMV")
+    rng = np.random.default_rng(fmt * 100 + batch)
+    rows, cols = 300, 1536
+    payload, scales = (_rand_packed_tq1 if fmt == 3 else _rand_packed)(rng, rows, cols, True)
+    w = tp.PackedMatrix(rows=rows, cols=cols, fmt=tp.DType(fmt), payload=payload, scales=scales).to_device()
+    x = torch.from_numpy(rng.uniform(-1, 1, size=(batch, cols)).astype(np.float32)).half().cuda()
+    y32 = tp.linear(x, w, path=path, out_dtype=torch.float32)
+    y16 = tp.linear(x, w, path=path)
+    assert y32.dtype == torch.float32
+    assert torch.equal(y32.half(), y16)
+    ref = _oracle_ref(payload, scales, cols, fmt, x.float().cpu().numpy())
+    assert rel_err(y32.cpu().numpy(), ref) <= 1e-4
+
 
 def test_repack_rejects_small_buffers(tp):
     """tr_repack / tr_repack_records / tr_unrepack take the device buffer size and refuse short ones
