@@ -50,13 +50,14 @@ size_t chain_workspace_bytes(int n_ops);
 // cost grows with batch x cols; K5 costs about the same for any batch up to 16 but pays a fixed
 // ~3.5 us per CTA and spreads poorly when a shape has few 128-row tiles.
 //  * batch <= 2: the int8-slice GEMV;
-//  * batch 3-4: the int8-slice GEMV while K <= 4096 columns, else K5;
+//  * batch 3-4: the int8-slice GEMV while K <= 4096 columns, or K <= 8192 on shapes K5 spreads
+//    badly (>= 12 blocks per CTA: 8192 x 8192 measured 12.3 vs 14.4 us), else K5;
 //  * batch 5-8: the fp16 GEMV only for K <= 4096 columns on shapes K5 spreads badly (>= 12
 //    blocks per CTA, e.g. 11008 x 4096), else K5;
 //  * batch >= 9: K5.
 static bool prefer_umma(int64_t batch, int64_t rows, int64_t cols) {
   if (batch <= 2) return false;
-  if (batch <= 4) return cols > 4096;
+  if (batch <= 4) return !(cols <= 4096 || (cols <= 8192 && umma_blocks_per_cta((int)batch, (int)rows, (int)cols) >= 12));
   if (batch <= 8) return cols > 4096 || umma_blocks_per_cta((int)batch, (int)rows, (int)cols) < 12;
   return true;
 }

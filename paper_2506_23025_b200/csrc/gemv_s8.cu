@@ -131,6 +131,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   if (lane == 0)
     for (int s = 0; s < pre_slots; ++s) issue(s);
   __syncwarp();
+  if constexpr (FMT == kFmtTq1) {   // K4's B' slot table in the (still unused) reduction buffer
+    s8q1_slot_table(reinterpret_cast<int*>(red));
+    __syncthreads();
+  }
   griddep_launch_dependents();
   griddep_wait();   // x belongs to the previous kernel until here
   if (trace) wait_clk = clock64();
@@ -148,6 +152,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
 
   // ---- stage the activations as int8 slices (fused producer first when asked)
   const T* xg = reinterpret_cast<const T*>(a.x);
+
   if (PRE == 1) {   // x = rmsnorm(x + delta) * gamma; CTA 0 stores x + delta (the residual)
     float* ss_buf = red;   // nb * nrx partial sums of squares
     const T* gam = reinterpret_cast<const T*>(a.pre_gamma);
@@ -270,7 +275,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
           for (int t = 0; t < 2; ++t)
             if (t < nv)
               s8q1_stage_block(f[t], xs + (size_t)(kbs[t] * nrx + brs[t]) * IB, ncs + (kbs[t] * nrx + brs[t]) * 4,
-                               fsc + kbs[t] * nrx + brs[t]);
+                               fsc + kbs[t] * nrx + brs[t], reinterpret_cast<const int*>(red));
         } else {
           if (nv > 0) s8_stage_blocks<2>(f, xs, ncs, fsc, nrx, kbs, brs, nv);
         }

@@ -228,8 +228,21 @@ __host__ __device__ inline int q1_ng(int c) { return c < 2 ? 7 : 6; }
 // Stage one (block, batch row) item for K4 (whole warp; lane holds columns 8 lane .. + 7):
 // x~ on the block's integer grid, -Cs of the x~ slices, the grid factor 2^(ex - 23), and the 288
 // B' slots as int8 slices at [slice s][lane column c][word m] (80 B rows, 16-B aligned).
+// Slot table of the B' staging: entry (p, b) of lane L = column | valid << 16 | has-next << 17 of byte b
+// of quad lane + 32 p (lane column c' = quad / 18, register m = quad % 18).  384 ints, one pass.
+__device__ __forceinline__ void s8q1_slot_table(int* tab) {
+  for (int i = threadIdx.x; i < 12 * 32; i += blockDim.x) {
+    const int pb = i >> 5, lane = i & 31, p = pb >> 2, b = pb & 3;
+    const int qd = lane + 32 * p, cq = qd / 18, m = qd - 18 * cq;
+    const int rho = 2 * m + (b >> 1), gl = rho / 5, k1 = rho - 5 * gl;
+    const int col = 10 * (q1_g0(cq & 3) + gl) + 2 * k1 + (b & 1);
+    const bool valid = qd < 72 && rho < 5 * q1_ng(cq & 3) && col < 256;
+    tab[i] = (valid ? col : 0) | (valid ? 1 << 16 : 0) | ((valid && k1 < 4 && col + 2 < 256) ? 1 << 17 : 0);
+  }
+}
+
 __device__ __forceinline__ void s8q1_stage_block(const float (&f)[8], uint8_t* item, int32_t* ncs_item,
-                                                 float* fsc_item) {
+                                                 float* fsc_item, const int* tab) {
   const int lane = threadIdx.x & 31;
   float mx = 0.0f;
 #pragma unroll
@@ -261,26 +274,19 @@ __device__ __forceinline__ void s8q1_stage_block(const float (&f)[8], uint8_t* i
   int* scr = reinterpret_cast<int*>(item);
   *reinterpret_cast<int4*>(scr + 8 * lane) = make_int4(xi[0], xi[1], xi[2], xi[3]);
   *reinterpret_cast<int4*>(scr + 8 * lane + 4) = make_int4(xi[4], xi[5], xi[6], xi[7]);
-  if (lane == 0) {
-    scr[256] = 0;
-    scr[257] = 0;
-  }
   __syncwarp();
-  // 72 quads (lane column c', register m): four B' slots each -> one word per slice
+  // 72 quads (lane column c', register m): four B' slots each -> one word per slice.  The slot ->
+  // column map depends on the lane only: read from the table s8q1_slot_table built once per CTA.
   uint32_t W[3][4];
 #pragma unroll
   for (int p = 0; p < 3; ++p) {
-    const int qd = lane + 32 * p;
-    const int cq = qd / 18, m = qd - 18 * cq;
     uint32_t Z[4];
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int rho = 2 * m + (b >> 1);
-      const int gl = (rho * 13) >> 6, k1 = rho - 5 * gl;   // rho / 5, rho % 5 (rho < 64)
-      const int col = 10 * (q1_g0(cq & 3) + gl) + 2 * k1 + (b & 1);
-      const bool valid = qd < 72 && rho < 5 * q1_ng(cq & 3) && col < 256;
-      const int x1 = valid ? scr[col] : 0;
-      const int x2 = (valid && k1 < 4) ? scr[col + 2] : 0;
+      const int e = tab[(p * 4 + b) * 32 + lane];   // col | valid << 16 | has-next << 17
+      const int col = e & 0xFFFF;
+      const int x1 = (e >> 16) & 1 ? scr[col] : 0;
+      const int x2 = (e >> 17) & 1 ? scr[col + 2] : 0;
       Z[b] = ((uint32_t)(x1 - 3 * x2) + 0x80808080u) ^ 0x80808080u;
     }
     const uint32_t t0 = __byte_perm(Z[0], Z[1], 0x5140), t1 = __byte_perm(Z[0], Z[1], 0x7362);
