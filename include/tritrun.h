@@ -170,6 +170,20 @@ TR_API int tr_linear_chain(int act_dtype, const TrChainLayer* layers, int64_t n_
 
 /* ---- decoder-layer glue (configs[2] decode stack; no reference analogue) ---------- */
 
+/* One decode token's attention block input side in ONE kernel: x = rmsnorm(h + delta) * gamma (h + delta
+ * stored to h_out), qkv_out [3, H, D] = x W_qkv^T (TQ2 device layout, rows 3 H D, cols H D), then
+ * tr_attn_decode on qkv_out (rotary, cache append at pos[0], softmax attention) -> att_out [H, D].
+ * Six CTAs share each head's 24 tiles; the last to finish runs the head's attention.  Same
+ * roundings as tr_linear_pre + tr_attn_decode.  head_dim 128, max_seq <= 128, batch 1.
+ * workspace: tr_qkv_attn_decode_workspace_size(heads) bytes of per-head arrival counters, zeroed
+ * once by the caller; every launch leaves them zero again (one launch in flight per workspace). */
+TR_API size_t tr_qkv_attn_decode_workspace_size(int64_t heads);
+TR_API int tr_qkv_attn_decode(int act_dtype, const void* w_qkv, const void* h, const void* delta, const void* gamma,
+                              void* h_out, float eps, void* qkv_out, const int64_t* pos, const void* cos_t,
+                              const void* sin_t, void* k_cache, void* v_cache, void* att_out, int64_t heads,
+                              int64_t head_dim, int64_t max_seq, float scale, void* workspace, size_t ws_bytes,
+                              int flags, void* stream);
+
 /* h[r] += delta[r] (delta may be NULL); y[r] = h[r] * rsqrt(mean(h[r]^2) + eps) * w; rows x d */
 TR_API int tr_add_rmsnorm(int act_dtype, void* h, const void* delta, const void* w, void* y, int64_t rows,
                           int64_t d, float eps, void* stream);

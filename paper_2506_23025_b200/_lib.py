@@ -77,6 +77,9 @@ _SIGS = {
                        _int),
     "tr_silu_mul": ([_int, _c_p, _c_p, _i64, _i64, _c_p], _int),
     "tr_attn_decode_workspace_size": ([_i64, _i64, _i64], ctypes.c_size_t),
+    "tr_qkv_attn_decode_workspace_size": ([_i64], ctypes.c_size_t),
+    "tr_qkv_attn_decode": ([_int, _c_p, _c_p, _c_p, _c_p, _c_p, ctypes.c_float, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
+                            _c_p, _i64, _i64, _i64, ctypes.c_float, _c_p, ctypes.c_size_t, _int, _c_p], _int),
     "tr_attn_decode_split": ([_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _i64, _i64, _i64, ctypes.c_float, _c_p,
                               ctypes.c_size_t, _c_p], _int),
 }

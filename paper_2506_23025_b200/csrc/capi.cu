@@ -40,6 +40,10 @@ int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t l
               int out_f32);
 size_t umma_workspace_bytes(int batch, int rows, int cols);
 int umma_blocks_per_cta(int batch, int rows, int cols);
+int gemv_qkv_attn(int act, const void* w, const void* h, const void* delta, const void* gamma, void* h_out,
+                  float eps, void* qkv, const int64_t* pos, const void* cos_t, const void* sin_t, void* k_cache,
+                  void* v_cache, void* att_out, int heads, int head_dim, int max_seq, float scale, void* counters,
+                  int pdl, int dbg, cudaStream_t st);
 bool gemv_stages_x(int batch, int rows, int cols);
 int gemv_chain_s8(int act, const TrChainLayer* host, int n, int batch, void* ws, size_t ws_bytes, int flags,
                   cudaStream_t st, bool upload);
@@ -158,6 +162,24 @@ int tr_linear_pre(int fmt, const void* w, const void* x, void* y, int64_t batch,
                    (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, (flags & TR_LINEAR_EPI_SWIGLU) ? 1 : 0, 0, kFmtTq2);
   return gemv_tq2(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, (flags >> 8) & 0xFFFF,
                   flags & TR_LINEAR_PDL, (cudaStream_t)stream, pre_op, delta, gamma, x_out, eps, 0);
+}
+
+size_t tr_qkv_attn_decode_workspace_size(int64_t heads) { return heads > 0 ? (size_t)heads * 4 : 0; }
+
+int tr_qkv_attn_decode(int act_dtype, const void* w_qkv, const void* h, const void* delta, const void* gamma,
+                       void* h_out, float eps, void* qkv_out, const int64_t* pos, const void* cos_t,
+                       const void* sin_t, void* k_cache, void* v_cache, void* att_out, int64_t heads,
+                       int64_t head_dim, int64_t max_seq, float scale, void* workspace, size_t ws_bytes, int flags,
+                       void* stream) {
+  TR_REQUIRE(heads >= 1 && ws_bytes >= tr_qkv_attn_decode_workspace_size(heads),
+             "tr_qkv_attn_decode: workspace of %zu bytes, %zu needed", ws_bytes,
+             tr_qkv_attn_decode_workspace_size(heads > 0 ? heads : 1));
+  TR_REQUIRE(act_dtype == kActF16 || act_dtype == kActBf16, "tr_qkv_attn_decode: act_dtype must be F16(1) or BF16(2)");
+  TR_REQUIRE(((uintptr_t)w_qkv & 15) == 0, "tr_qkv_attn_decode: weight buffer must be 16-byte aligned");
+  TR_REQUIRE(heads >= 1 && heads * head_dim < (1 << 24), "tr_qkv_attn_decode: bad heads");
+  return gemv_qkv_attn(act_dtype, w_qkv, h, delta, gamma, h_out, eps, qkv_out, pos, cos_t, sin_t, k_cache, v_cache,
+                       att_out, (int)heads, (int)head_dim, (int)max_seq, scale, workspace, flags & TR_LINEAR_PDL,
+                       (flags >> 16) & 0xfff, (cudaStream_t)stream);   // (bits 16..27: dev probes)
 }
 
 size_t tr_linear_chain_workspace_size(int64_t n_layers) {

@@ -23,6 +23,7 @@
 //  * per block: two slices combine in int32, one I2F + FFMA per row applies the block scale
 //    and the block grid 2^(e-29); the two slice pairs meet by one shuffle when a tile closes.
 // Weight streaming, tile ownership and the deterministic boundary-tile reduction are K3's.
+#include "attn_core.cuh"
 #include "s8_core.cuh"
 
 namespace tr {
@@ -49,9 +50,21 @@ struct S8Args {
   float eps;
   int out_f32;   // TR_LINEAR_OUT_F32: y is float32
   int fmt;       // kFmtTq2 (K3-S8) or kFmtTq1 (K4)
+  // ATT = 1 (tr_qkv_attn_decode): y is one token's qkv [3, H, 128]; CTA b serves head b / (3 m): its
+  // q, k or v section ((b % 3m) / m), 8 / m tiles of it; the head's last CTA to finish runs its attention
+  const int64_t* att_pos;
+  const void* att_cos;
+  const void* att_sin;
+  void* att_kc;
+  void* att_vc;
+  void* att_out;
+  int att_heads, att_seq;
+  float att_scale;
+  unsigned* att_cnt;   // per-head arrival counters (zero between launches)
+  int att_m;           // CTAs per q / k / v section of a head (1, 2, 4 or 8)
 };
 
-template <typename T, int NW, int PRE, int NG, int FMT = kFmtTq2>
+template <typename T, int NW, int PRE, int NG, int FMT = kFmtTq2, int ATT = 0>
 __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Args a) {
   static_assert(FMT == kFmtTq2 || PRE == 0, "fused producers are TQ2-only");
   using Cfg = S8Cfg<NW, NG, FMT>;
@@ -96,8 +109,13 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   // the first weight copies)
   // (SwiGLU epilogue: whole gate / up tile pairs per CTA)
   const unsigned tq = a.epi ? 2u : 1u, tn = (unsigned)a.n_tiles / tq;
-  const unsigned t0 = tq * (blockIdx.x * tn / gridDim.x);
-  const unsigned t1 = tq * ((blockIdx.x + 1) * tn / gridDim.x);
+  unsigned t0 = tq * (blockIdx.x * tn / gridDim.x);
+  unsigned t1 = tq * ((blockIdx.x + 1) * tn / gridDim.x);
+  if (ATT && !(a.dbg & 64)) {   // head-major: the 3 m CTAs of a head are neighbours in the grid (dbg 64: probe)
+    const unsigned m = (unsigned)a.att_m, hh = blockIdx.x / (3u * m), r = blockIdx.x % (3u * m);
+    t0 = (r / m) * 8u * (unsigned)a.att_heads + hh * 8u + (r % m) * (8u / m);
+    t1 = t0 + 8u / m;
+  }
   const int LL = (int)(t1 - t0) * nb;
   const int wu0 = (int)t0 * nb + (int)((unsigned)(warp * LL) / NW);
   const int wu1 = (int)t0 * nb + (int)((unsigned)((warp + 1) * LL) / NW);
@@ -134,6 +152,20 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   if constexpr (FMT == kFmtTq1) {   // K4's B' slot table in the (still unused) reduction buffer
     s8q1_slot_table(reinterpret_cast<int*>(red));
     __syncthreads();
+  }
+  if constexpr (ATT) {   // the head's cached keys / values (written a decode step ago) -> L2 under the GEMV
+    if (blockIdx.x % (3 * a.att_m) == 0 && threadIdx.x == 32 && !(a.dbg & 16)) {
+      int ps = (int)*reinterpret_cast<const volatile int64_t*>(a.att_pos);   // speculative (see k_attn_decode)
+      ps = ps < 0 ? 0 : (ps > a.att_seq ? a.att_seq : ps);
+      if (ps > 0) {
+        const int64_t off = (int64_t)(blockIdx.x / (3 * a.att_m)) * a.att_seq * 128 * sizeof(T);
+        const uint32_t bytes = (uint32_t)ps * 128u * sizeof(T);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"((const uint8_t*)a.att_kc + off), "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"((const uint8_t*)a.att_vc + off), "r"(bytes)
+                     : "memory");
+      }
+    }
   }
   griddep_launch_dependents();
   griddep_wait();   // x belongs to the previous kernel until here
@@ -187,6 +219,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
           dv = s8_load8(reinterpret_cast<const T*>(a.pre_delta) + br * a.ldx, kx, a.cols, a.x_vec);
       }
       s8_f8<T>(xv, f);
+      if (trace && ii == 0) {   // (dev probe: first loads landed)
+        asm volatile("" ::"f"(f[0]));
+        stamp(11);
+      }
       if (a.pre_delta) {
         float d[8];
         s8_f8<T>(dv, d);
@@ -211,7 +247,13 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
       for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
       if (lane == 0) ss_buf[item] = ss;
     }
+#ifdef S8_PRE_PROBE
+    stamp(9);
+#endif
     __syncthreads();
+#ifdef S8_PRE_PROBE
+    stamp(10);
+#endif
     for (int item = warp, ii = 0; item < nb * nrx; item += NW, ++ii) {
       const int kb = item >> lr, br = item & (nrx - 1);
       const int64_t kx = (int64_t)kb * kBlock + lane * 8;
@@ -546,7 +588,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
     }
     u += n;
   }
+#ifndef S8_PRE_PROBE
   stamp(9);
+#endif
   if (cur >= 0) close_tile(cur);
 
   // ---- boundary tiles: combine the parked fragments in fixed (warp, slot) order and store
@@ -582,8 +626,27 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
         y[br * a.ldy + orow] = Act<T>::from_float(s8_rnd<T>(__fdividef(gt, 1.0f + __expf(-gt))) * up);
     }
   }
+#ifndef S8_PRE_PROBE
   stamp(10);
+#endif
   if (warp == 0) stamp(3);
+  if constexpr (ATT) {   // the last of the head's 3 m CTAs to store its rows runs the head's attention
+    volatile int& last = slot_tile[0];   // (free by now; a static __shared__ would eat into the 227 KB opt-in)
+    const unsigned hh = blockIdx.x / (3u * (unsigned)a.att_m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned c;
+      asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;\n" : "=r"(c) : "l"(a.att_cnt + hh) : "memory");
+      last = c == 3u * (unsigned)a.att_m - 1u;
+      if (last) a.att_cnt[hh] = 0;   // (all arrivals are in; the next launch reads it after griddepcontrol.wait)
+    }
+    __syncthreads();
+    if (last && threadIdx.x < 128)
+      attn::attn_head_128<T>(reinterpret_cast<const T*>(a.y), a.att_pos, reinterpret_cast<const T*>(a.att_cos),
+                             reinterpret_cast<const T*>(a.att_sin), reinterpret_cast<T*>(a.att_kc),
+                             reinterpret_cast<T*>(a.att_vc), reinterpret_cast<T*>(a.att_out), a.att_heads, a.att_seq,
+                             (int)hh, a.att_scale, xs, threadIdx.x, 2);
+  }
 }
 
 // ------------------------------------------------------------------------------------ host
@@ -690,6 +753,92 @@ static int launch_s8_ng(S8Args& a, int grid, int pdl, cudaStream_t st) {   // on
 template <typename T, int NW>
 static int launch_s8(S8Args& a, int grid, int pdl, cudaStream_t st) {
   return a.batch <= 2 ? launch_s8_ng<T, NW, 1>(a, grid, pdl, st) : launch_s8_ng<T, NW, 2>(a, grid, pdl, st);
+}
+
+// Fused decode QKV projection + attention (tr_qkv_attn_decode): the add + RMSNorm producer and the
+// int8-slice GEMV of K3-S8 with the tiles dealt head-major (3 m CTAs per head, each inside one of its
+// q / k / v sections); each CTA counts itself in (atom.acq_rel) and the head's last CTA runs that
+// head's attention, so no separate attention kernel -- and no kernel boundary -- follows the
+// projection.  (Measured: the head-major deal beats the plain even split over all SMs, where every
+// head waits on CTAs from three distant parts of the grid.)
+template <typename T, int NW>
+static int launch_qkv_attn(S8Args& a, int pdl, cudaStream_t st) {
+  auto kern = k_gemv_s8<T, NW, 1, 1, kFmtTq2, 1>;
+  static int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    TR_REQUIRE(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) == cudaSuccess,
+               "tr_qkv_attn_decode: cannot opt in to 227 KB of shared memory");
+    configured_dev = dev;
+  }
+  // m CTAs per q / k / v section of a head: the largest of 8, 4, 2, 1 with 3 m H CTAs in one wave
+  // (H = 24: m = 2, 144 CTAs of 4 tiles; more heads than 49 run 3 H CTAs in several waves)
+  int m = 8;
+  while (m > 1 && 3 * m * a.att_heads > sm_count()) m >>= 1;
+  a.att_m = m;
+  const int grid = 3 * m * a.att_heads;
+  const size_t smem = s8_smem_plan<NW, 1, kFmtTq2>(1, a.nb, a.n_tiles, grid, &a.ns);
+  const size_t att_need = S8Cfg<NW, 1, kFmtTq2>::xs_off(a.nb, 1) + attn::kSmemBytes;
+  const size_t smem_all = smem > att_need ? smem : att_need;
+  TR_REQUIRE(smem_all <= 227 * 1024, "tr_qkv_attn_decode: %zu B of shared memory", smem_all);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(NW * 32, 1, 1);
+  cfg.dynamicSmemBytes = smem_all;
+  cfg.stream = st;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+  TR_REQUIRE(e == cudaSuccess, "tr_qkv_attn_decode: launch failed: %s (grid %d, smem %zu)", cudaGetErrorString(e),
+             grid, smem_all);
+  return 0;
+}
+
+int gemv_qkv_attn(int act, const void* w, const void* h, const void* delta, const void* gamma, void* h_out,
+                  float eps, void* qkv, const int64_t* pos, const void* cos_t, const void* sin_t, void* k_cache,
+                  void* v_cache, void* att_out, int heads, int head_dim, int max_seq, float scale, void* counters,
+                  int pdl, int dbg, cudaStream_t st) {
+  TR_REQUIRE(head_dim == 128, "tr_qkv_attn_decode: head_dim must be 128");
+  TR_REQUIRE(heads >= 1 && max_seq >= 1 && max_seq <= 128, "tr_qkv_attn_decode: 1 <= max_seq <= 128");
+  TR_REQUIRE(gamma != nullptr && h_out != nullptr, "tr_qkv_attn_decode: RMSNorm needs gamma and the residual output");
+  const int d = heads * head_dim;
+  S8Args a = {};
+  a.fmt = kFmtTq2;
+  a.w = (const uint8_t*)w;
+  a.x = h;
+  a.y = qkv;
+  a.ldx = d;
+  a.ldy = 3 * d;
+  a.rows = 3 * d;
+  a.cols = d;
+  a.nb = (int)ceil_div(d, kBlock);
+  a.n_tiles = (int)ceil_div(3 * d, 16);
+  a.x_vec = (((uintptr_t)h | (uintptr_t)(delta ? delta : h) | (uintptr_t)gamma | (uintptr_t)h_out) % 16) == 0 ? 1 : 0;
+  a.batch = 1;
+  a.pre = 1;
+  a.pre_delta = delta;
+  a.pre_gamma = gamma;
+  a.pre_out = h_out;
+  a.eps = eps;
+  a.att_pos = pos;
+  a.att_cos = cos_t;
+  a.att_sin = sin_t;
+  a.att_kc = k_cache;
+  a.att_vc = v_cache;
+  a.att_out = att_out;
+  a.att_heads = heads;
+  a.att_seq = max_seq;
+  a.att_scale = scale;
+  a.dbg = dbg;
+  a.att_cnt = (unsigned*)counters;
+  TR_REQUIRE(counters != nullptr, "tr_qkv_attn_decode: needs the zeroed counter workspace");
+  if (dbg & 256)   // dev probe: 8 warps
+    return act == kActF16 ? launch_qkv_attn<__half, 8>(a, pdl, st) : launch_qkv_attn<__nv_bfloat16, 8>(a, pdl, st);
+  return act == kActF16 ? launch_qkv_attn<__half, 16>(a, pdl, st) : launch_qkv_attn<__nv_bfloat16, 16>(a, pdl, st);
 }
 
 int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows, int cols,

@@ -119,10 +119,26 @@ class TernaryDecoder:
         self._positions = torch.arange(S, device=self.device)
         # TR_LINEAR_COSCHEDULE per decode GEMV (qkv, o, gate_up, down): 8-warp CTAs (measured)
         self.cosched = (False, False, False, False)
+        # decode QKV GEMV + attention as one kernel (tr_qkv_attn_decode): off by default -- measured
+        # slower inside the decode chain (its 16-warp CTAs keep the following o
+        # projection from launching early); use_fused_attention(True) switches it on
+        self.fused_attn = False
+        self._fused_attn_ok = (not dense and fused and D == 128 and S <= 128
+                               and all(lw["qkv"].fmt is DType.TQ2 for lw in weights["layers"]))
+        self._qkv_attn_ws = torch.zeros(_lib.lib().tr_qkv_attn_decode_workspace_size(H), dtype=torch.uint8,
+                                        device=self.device)   # per-head arrival counters (stay zero)
         self._prefill_graphs = {}
         self.graph = None
         self._host_pos = 0
         self.graph_multi = None    # STEPS_PER_GRAPH decode steps in one graph (no replay boundaries)
+
+    def use_fused_attention(self, on: bool = True) -> None:
+        """Decode steps run add + RMSNorm -> QKV GEMV -> attention as one kernel (tr_qkv_attn_decode);
+        needs TQ2 QKV weights, head_dim 128 and max_seq <= 128.  Re-captures the decode graph."""
+        if on and not self._fused_attn_ok:
+            raise ValueError("fused QKV + attention needs ternary TQ2 QKV weights, head_dim 128 and max_seq <= 128")
+        self.fused_attn = bool(on)
+        self.graph = self.graph_multi = None
 
     # -- building blocks ----------------------------------------------------------------
     def _lin(self, x, w):
@@ -225,19 +241,21 @@ class TernaryDecoder:
             lw = self.lin[i]
             # residual stream ping-pongs: the GEMV reads hs[cur] and stores hs[cur] + delta to hs[1 - cur]
             cs = self.cosched
-            qkv = linear_pre(hs[cur], lw["qkv"], _lib.PRE_ADD_RMSNORM, delta, self.norm_attn[i], hs[1 - cur],
-                             cfg.eps, pdl=True, cosched=cs[0])
-            cur = 1 - cur
             att = torch.empty((1, d), device=self.device, dtype=self.dtype)
-            if S <= 128:   # one CTA per head holds the whole cache
-                _lib.call("tr_attn_decode", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(),
-                          self.sin.data_ptr(), self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(),
-                          H, D, S, D ** -0.5, st)
-            else:          # split-KV over 128-key chunks, partial softmaxes merged
-                _lib.call("tr_attn_decode_split", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(),
-                          self.sin.data_ptr(), self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(),
-                          H, D, S, D ** -0.5, self._attn_ws.data_ptr(), self._attn_ws.numel(), st)
-            o = linear(att, lw["o"], pdl=True, cosched=cs[1])
+            if self.fused_attn:   # add + RMSNorm -> QKV GEMV -> rotary, cache append, attention: one kernel
+                qkv = torch.empty((1, 3 * d), device=self.device, dtype=self.dtype)
+                w = lw["qkv"]
+                _lib.call("tr_qkv_attn_decode", act, w.data.data_ptr(), hs[cur].data_ptr(),
+                          0 if delta is None else delta.data_ptr(), self.norm_attn[i].data_ptr(),
+                          hs[1 - cur].data_ptr(), cfg.eps, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(),
+                          self.sin.data_ptr(), self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(),
+                          att.data_ptr(), H, D, S, D ** -0.5, self._qkv_attn_ws.data_ptr(),
+                          self._qkv_attn_ws.numel(), _lib.LINEAR_PDL, st)
+                cur = 1 - cur
+                o = linear(att, lw["o"], pdl=True, cosched=cs[1])
+            else:
+                o = self._qkv_attn_unfused(i, hs, cur, delta, pos, att)
+                cur = 1 - cur
             if self.gate_up_il is not None:   # SwiGLU in the gate|up GEMV's epilogue
                 act_ = linear_pre(hs[cur], self.gate_up_il[i], _lib.PRE_ADD_RMSNORM, o, self.norm_mlp[i],
                                   hs[1 - cur], cfg.eps, pdl=True, cosched=cs[2], epi_swiglu=True)
@@ -252,6 +270,22 @@ class TernaryDecoder:
         _lib.call("tr_add_rmsnorm", act, hs[cur].data_ptr(), delta.data_ptr(), self.norm_out.data_ptr(), xn.data_ptr(),
                   1, d, cfg.eps, st)
         return F.linear(xn, self.weights["lm_head"])[0]
+
+    def _qkv_attn_unfused(self, i, hs, cur, delta, pos, att):
+        """QKV GEMV with the add + RMSNorm producer, then the attention kernel; returns o."""
+        cfg, act, st, lw, cs = self.cfg, _ACT[self.dtype], _lib.stream_handle(), self.lin[i], self.cosched
+        H, D, S = cfg.n_heads, cfg.head_dim, cfg.max_seq
+        qkv = linear_pre(hs[cur], lw["qkv"], _lib.PRE_ADD_RMSNORM, delta, self.norm_attn[i], hs[1 - cur],
+                         cfg.eps, pdl=True, cosched=cs[0])
+        if S <= 128:   # one CTA per head holds the whole cache
+            _lib.call("tr_attn_decode", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(),
+                      self.sin.data_ptr(), self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(),
+                      H, D, S, D ** -0.5, st)
+        else:          # split-KV over 128-key chunks, partial softmaxes merged
+            _lib.call("tr_attn_decode_split", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(),
+                      self.sin.data_ptr(), self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(),
+                      H, D, S, D ** -0.5, self._attn_ws.data_ptr(), self._attn_ws.numel(), st)
+        return linear(att, lw["o"], pdl=True, cosched=cs[1])
 
     # -- serving --------------------------------------------------------------------------
     def prefill(self, prompt: torch.Tensor, graph: bool = True) -> None:

@@ -979,3 +979,87 @@ def test_tpk1_load_to_device_matches_reference(tp):
     assert m["layers.0.attn.qkv"].uniform_scale and not m["layers.0.mlp.down"].uniform_scale
     assert torch.equal(m["embed"].cpu(), torch.from_numpy(g["embed"]))
     assert torch.equal(m["norm"].cpu(), torch.from_numpy(g["norm"]))
+
+
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
+@pytest.mark.parametrize("heads", [4, 24])
+def test_qkv_attn_decode_matches_unfused(tp, dtype, heads):
+    """tr_qkv_attn_decode (add + RMSNorm -> QKV GEMV -> rotary, cache append, attention in one cluster
+    kernel) against tr_linear_pre + tr_attn_decode on the same inputs: the residual output bitwise,
+    q / k / v, the appended cache rows and the attention output within the GEMV's accumulation
+    tolerance; position past the cache writes nothing and outputs zeros."""
+    from paper_2506_23025_b200 import _lib
+    from paper_2506_23025_b200.device import _ACT, linear_pre
+
+    tdt = getattr(torch, dtype)
+    act, st = _ACT[tdt], _lib.stream_handle()
+    D, S = 128, 128
+    d = heads * D
+    g = torch.Generator(device="cuda").manual_seed(heads)
+    T = torch.randint(-1, 2, (3 * d, d), device="cuda", generator=g).float()
+    w = tp.TernaryWeight.from_float(0.02 * T)
+    h = torch.randn((1, d), device="cuda", generator=g).to(tdt)
+    delta = (0.5 * torch.randn((1, d), device="cuda", generator=g)).to(tdt)
+    gamma = (1 + 0.1 * torch.randn(d, device="cuda", generator=g)).to(tdt)
+    ang = torch.arange(S, device="cuda").float()[:, None] * (1e-4 ** (torch.arange(0, D, 2, device="cuda") / D))
+    cos, sin = ang.cos().to(tdt), ang.sin().to(tdt)
+    kc0 = (0.5 * torch.randn((heads, S, D), device="cuda", generator=g)).to(tdt)
+    vc0 = (0.5 * torch.randn((heads, S, D), device="cuda", generator=g)).to(tdt)
+    tol = 2e-2 if dtype == "bfloat16" else 4e-3
+    ws = torch.zeros(_lib.lib().tr_qkv_attn_decode_workspace_size(heads), dtype=torch.uint8, device="cuda")
+    for p in (0, 1, 37, 127, 128):
+        pos = torch.tensor([p], device="cuda")
+        kc_f, vc_f, kc_u, vc_u = kc0.clone(), vc0.clone(), kc0.clone(), vc0.clone()
+        ho_f, ho_u = torch.empty_like(h), torch.empty_like(h)
+        qkv_f = torch.empty((1, 3 * d), device="cuda", dtype=tdt)
+        att_f, att_u = torch.empty((1, d), device="cuda", dtype=tdt), torch.empty((1, d), device="cuda", dtype=tdt)
+        _lib.call("tr_qkv_attn_decode", act, w.data.data_ptr(), h.data_ptr(), delta.data_ptr(), gamma.data_ptr(),
+                  ho_f.data_ptr(), 1e-5, qkv_f.data_ptr(), pos.data_ptr(), cos.data_ptr(), sin.data_ptr(),
+                  kc_f.data_ptr(), vc_f.data_ptr(), att_f.data_ptr(), heads, D, S, D ** -0.5, ws.data_ptr(),
+                  ws.numel(), 0, st)
+        qkv_u = linear_pre(h, w, _lib.PRE_ADD_RMSNORM, delta, gamma, ho_u, 1e-5)
+        _lib.call("tr_attn_decode", act, qkv_u.data_ptr(), pos.data_ptr(), cos.data_ptr(), sin.data_ptr(),
+                  kc_u.data_ptr(), vc_u.data_ptr(), att_u.data_ptr(), heads, D, S, D ** -0.5, st)
+        torch.cuda.synchronize()
+        assert torch.equal(ho_f, ho_u)
+        assert not ws.any()   # the arrival counters are left zero
+        rel = lambda a, b: ((a.float() - b.float()).abs().max() / b.float().abs().max().clamp_min(1e-6)).item()
+        assert rel(qkv_f, qkv_u) <= tol
+        assert rel(att_f, att_u) <= tol, p
+        if p >= S:
+            assert torch.equal(kc_f, kc0) and torch.equal(vc_f, vc0)
+            assert not att_f.float().abs().any()
+        else:
+            others = torch.ones(S, dtype=torch.bool, device="cuda")
+            others[p] = False
+            assert torch.equal(kc_f[:, others], kc0[:, others]) and torch.equal(vc_f[:, others], vc0[:, others])
+            assert rel(kc_f[:, p], kc_u[:, p]) <= tol and rel(vc_f[:, p], vc_u[:, p]) <= tol
+
+
+def test_decoder_fused_attention_matches_unfused(tp):
+    """The decoder's fused QKV + attention decode step (max_seq <= 128) against the two-kernel
+    step on shared weights: logits through prefill + greedy decode, graph replay included."""
+    from paper_2506_23025_b200.decoder import DecoderConfig, TernaryDecoder
+
+    cfg = DecoderConfig(d_model=768, n_layers=2, n_heads=6, d_ff=2048, vocab=1000, max_seq=128)
+    a = TernaryDecoder(cfg, seed=8)
+    b = TernaryDecoder(cfg, weights=a.weights)
+    a.use_fused_attention(True)
+    assert a.fused_attn and not b.fused_attn
+    with pytest.raises(ValueError):
+        TernaryDecoder(DecoderConfig(d_model=768, n_layers=1, n_heads=6, d_ff=2048, vocab=100, max_seq=256),
+                       seed=1).use_fused_attention(True)
+    prompt = torch.randint(0, cfg.vocab, (9,), device="cuda")
+    pos = torch.arange(9, device="cuda")
+    la, lb = a.forward(prompt, pos).float(), b.forward(prompt, pos).float()
+    for p in range(9, 20):
+        t1 = torch.argmax(lb).view(1)
+        p1 = torch.tensor([p], device="cuda")
+        la, lb = a.forward(t1, p1).float(), b.forward(t1, p1).float()
+        assert ((la - lb).abs().max() / lb.abs().max()).item() <= 5e-3, p
+    for m in (a, b):   # graph decode (8-step graph + single-step remainder)
+        m.reset()
+        m.prefill(prompt)
+        m.decode(11)
+    torch.cuda.synchronize()
+    assert torch.equal(a.out_tokens[9:20], b.out_tokens[9:20])
