@@ -237,10 +237,20 @@ __device__ __forceinline__ void s8q1_slot_table(int* tab) {
     const int rho = 2 * m + (b >> 1), gl = rho / 5, k1 = rho - 5 * gl;
     const int col = 10 * (q1_g0(cq & 3) + gl) + 2 * k1 + (b & 1);
     const bool valid = qd < 72 && rho < 5 * q1_ng(cq & 3) && col < 256;
-    tab[i] = (valid ? col : 0) | (valid ? 1 << 16 : 0) | ((valid && k1 < 4 && col + 2 < 256) ? 1 << 17 : 0);
+    const bool next = valid && k1 < 4 && col + 2 < 256;
+    // byte offsets into the staging scratch (column c at word (c & 3) * 64 + (c >> 2)); 1024 is a
+    // zero word, so slots without a column (or without a next digit) read 0 branch-free
+    const int o1 = valid ? 4 * ((col & 3) * 64 + (col >> 2)) : 1024;
+    const int o2 = next ? 4 * (((col + 2) & 3) * 64 + ((col + 2) >> 2)) : 1024;
+    tab[i] = o1 | (o2 << 16);
   }
 }
 
+__device__ __forceinline__ uint32_t s8_lds32(uint32_t addr) {
+  uint32_t r;
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(r) : "r"(addr) : "memory");
+  return r;
+}
 __device__ __forceinline__ void s8q1_stage_block(const float (&f)[8], uint8_t* item, int32_t* ncs_item,
                                                  float* fsc_item, const int* tab) {
   const int lane = threadIdx.x & 31;
@@ -270,11 +280,15 @@ __device__ __forceinline__ void s8q1_stage_block(const float (&f)[8], uint8_t* i
   }
 #pragma unroll
   for (int s = 0; s < 4; ++s) cs[s] = __reduce_add_sync(0xffffffffu, cs[s]);
-  // x~ as int32 scratch in the item's own bytes (columns 256, 257 read as 0)
+  // x~ as int32 scratch in the item's own bytes, column c at word (c & 3) * 64 + (c >> 2): the slot
+  // gather below reads columns ~4 apart across lanes, which this layout spreads over the banks
+  // (26 shared-memory wavefronts per block instead of 62)
   int* scr = reinterpret_cast<int*>(item);
-  *reinterpret_cast<int4*>(scr + 8 * lane) = make_int4(xi[0], xi[1], xi[2], xi[3]);
-  *reinterpret_cast<int4*>(scr + 8 * lane + 4) = make_int4(xi[4], xi[5], xi[6], xi[7]);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) scr[(e & 3) * 64 + 2 * lane + (e >> 2)] = xi[e];
+  if (lane == 0) scr[256] = 0;   // the zero word (item bytes 1024..1027; overwritten only after the gather)
   __syncwarp();
+  const uint32_t scr32 = smem_u32(item);
   // 72 quads (lane column c', register m): four B' slots each -> one word per slice.  The slot ->
   // column map depends on the lane only: read from the table s8q1_slot_table built once per CTA.
   uint32_t W[3][4];
@@ -283,10 +297,9 @@ __device__ __forceinline__ void s8q1_stage_block(const float (&f)[8], uint8_t* i
     uint32_t Z[4];
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int e = tab[(p * 4 + b) * 32 + lane];   // col | valid << 16 | has-next << 17
-      const int col = e & 0xFFFF;
-      const int x1 = (e >> 16) & 1 ? scr[col] : 0;
-      const int x2 = (e >> 17) & 1 ? scr[col + 2] : 0;
+      const uint32_t e = (uint32_t)tab[(p * 4 + b) * 32 + lane];   // byte offsets of x~[col], x~[col + 2]
+      const int x1 = (int)s8_lds32(scr32 + (e & 0xFFFFu));
+      const int x2 = (int)s8_lds32(scr32 + (e >> 16));
       Z[b] = ((uint32_t)(x1 - 3 * x2) + 0x80808080u) ^ 0x80808080u;
     }
     const uint32_t t0 = __byte_perm(Z[0], Z[1], 0x5140), t1 = __byte_perm(Z[0], Z[1], 0x7362);

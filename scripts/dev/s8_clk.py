@@ -7,7 +7,8 @@ import paper_2506_23025_b200 as tp
 rows, cols, L = int(sys.argv[1]), int(sys.argv[2]), 6
 NW = int(sys.argv[3]) if len(sys.argv) > 3 else 16
 extra = (1 if NW == 16 else 0) | (int(sys.argv[4]) if len(sys.argv) > 4 else 0)   # + ring-order probe bits 4/8
-ws = [tp.TernaryWeight.from_float(torch.randint(-1, 2, (rows, cols), device="cuda").float() * 0.02) for _ in range(L)]
+fmt = getattr(tp.DType, os.environ.get("FMT", "TQ2"))
+ws = [tp.TernaryWeight.from_float(torch.randint(-1, 2, (rows, cols), device="cuda").float() * 0.02, fmt) for _ in range(L)]
 x = torch.randn(1, cols, device="cuda").half() * 0.01
 n = 148 * 8 * 4 + 148 * NW * 4 * 4 + rows + 64
 ybig = [torch.zeros(1, n, device="cuda", dtype=torch.half) for _ in range(L)]

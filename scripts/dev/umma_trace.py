@@ -12,7 +12,7 @@ x = (torch.rand(b, cols, device="cuda") * 2 - 1).half()
 ys = [torch.zeros(b, rows, dtype=torch.float16, device="cuda") for _ in ws]
 for rep in range(3):
     for w, y in zip(ws, ys):
-        tp.linear(x, w, out=y, path="umma", _probe=4, pdl=True)
+        tp.linear(x, w, out=y, path="umma", _probe=4 | int(os.environ.get("PROBE", "0")), pdl=True)
 torch.cuda.synchronize()
 t = ys[-1].view(torch.int64).flatten()[: 64 * 8].cpu().numpy().reshape(64, 8)[:, :5].astype(np.float64)
 nb = cols // 256
