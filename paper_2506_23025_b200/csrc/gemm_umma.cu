@@ -207,8 +207,6 @@ struct UmmaArgs {
                       // decoded [2] MMAs issued; decode warp 0 [3] A buffer free [4] TMEM stores done
   int map3d;          // activations described by the 3-D tensor map (one TMA request per block)
   int out_f32;        // TR_LINEAR_OUT_F32: y is float32
-  int sk;             // stream-K: the (tile, block) items, tile-major, split evenly over the grid
-  int kq;             // stream-K: partial-sum slots per tile (most CTAs that can share one tile)
 };
 
 template <typename T, int N, int FMT>
@@ -291,24 +289,8 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
   const int mt = blockIdx.x % a.m_tiles;
   const int nt = (blockIdx.x / a.m_tiles) % a.n_tiles;
   const int kslice = blockIdx.x / (a.m_tiles * a.n_tiles);
-  // this CTA's blocks: segment A = tile mtA, blocks [kbA, kbA + sA); in stream-K mode a CTA may
-  // carry on into segment B = tile mtA + 1, blocks [0, nblk - sA) (items i >= sA)
-  int mtA, kbA, nblk, sA;
-  if (a.sk) {
-    const int W = a.m_tiles * a.nb;
-    const int i0 = (int)((int64_t)blockIdx.x * W / gridDim.x), i1 = (int)((int64_t)(blockIdx.x + 1) * W / gridDim.x);
-    mtA = i0 / a.nb;
-    kbA = i0 - mtA * a.nb;
-    nblk = i1 - i0;
-    sA = min(nblk, a.nb - kbA);
-  } else {
-    mtA = mt;
-    kbA = (int)((int64_t)kslice * a.nb / a.ks);
-    nblk = (int)((int64_t)(kslice + 1) * a.nb / a.ks) - kbA;
-    sA = nblk;
-  }
-  auto item_mt = [&](int i) { return i < sA ? mtA : mtA + 1; };
-  auto item_kb = [&](int i) { return i < sA ? kbA + i : i - sA; };
+  const int kb0 = (int)((int64_t)kslice * a.nb / a.ks), kb1 = (int)((int64_t)(kslice + 1) * a.nb / a.ks);
+  const int nblk = kb1 - kb0;
   const int nws = (nblk + KS - 1) / KS;   // weight stages
   const bool per_block = !a.uniform;
 
@@ -341,7 +323,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   // TMEM: NA A buffers of 128 columns, then the accumulator(s): 2 x N (per-block, double
   // buffered) or N (uniform scale, one accumulator over all K)
-  const int dcols = (per_block || a.sk) ? 2 * N : N;   // (stream-K: one accumulator per segment)
+  const int dcols = per_block ? 2 * N : N;
   const int NA = (512 - dcols) / 128 < Cfg::kMaxA ? (512 - dcols) / 128 : Cfg::kMaxA;
   const uint32_t tA = tmem, tD = tmem + NA * 128;
   griddep_launch_dependents();
@@ -351,27 +333,24 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmx) : "memory");
       const uint64_t pol = policy_evict_first();
-      auto issue_w = [&](int si) {   // weight stage si: items [si KS, si KS + c) of the CTA's 8 tiles
+      const uint8_t* wbase = a.w + ((int64_t)mt * 8 * a.nb + kb0) * UB;
+      auto issue_w = [&](int si) {   // weight stage si: blocks [si KS, si KS + c) of the CTA's 8 tiles
         const int s = si % RW, c = min(KS, nblk - si * KS);
         mbar_expect_tx(&full_w[s], 8 * c * UB);
-        for (int j = 0; j < c;) {   // runs inside one tile row group (two when a stage spans segments)
-          const int i = si * KS + j, run = i < sA ? min(c - j, sA - i) : c - j;
-          const uint8_t* src = a.w + ((int64_t)item_mt(i) * 8 * a.nb + item_kb(i)) * UB;
 #pragma unroll 1
-          for (int t = 0; t < 8; ++t)
-            bulk_g2s(sW + s * kStageW + (t * KS + j) * UB, src + (int64_t)t * a.nb * UB, run * UB, &full_w[s], pol);
-          j += run;
-        }
+        for (int t = 0; t < 8; ++t)
+          bulk_g2s(sW + s * kStageW + t * KS * UB, wbase + ((int64_t)t * a.nb + si * KS) * UB, c * UB, &full_w[s],
+                   pol);
       };
       auto issue_b = [&](int i) {
         const int s = i % RB;
         mbar_expect_tx(&full_b[s], kStageB);
         if (a.map3d) {
-          tma_load_3d(sB + s * kStageB, &tmx, 0, nt * N, item_kb(i) * 4, &full_b[s]);
+          tma_load_3d(sB + s * kStageB, &tmx, 0, nt * N, (kb0 + i) * 4, &full_b[s]);
         } else {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            tma_load_2d(sB + s * kStageB + q * N * 128, &tmx, item_kb(i) * kBlock + q * 64, nt * N, &full_b[s]);
+            tma_load_2d(sB + s * kStageB + q * N * 128, &tmx, (kb0 + i) * kBlock + q * 64, nt * N, &full_b[s]);
         }
       };
       int nw_ = nws < RW ? nws : RW, nb_ = nblk < RB ? nblk : RB;
@@ -407,21 +386,19 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
           reinterpret_cast<long long*>(a.y)[i * 8 + 1] = clock64();
         if (per_block) mbar_wait(&d_empty[db], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
-        const int seg = i >= sA;
-        const uint32_t d = per_block ? tD + db * N : tD + seg * N;
-        const int acc0 = (!per_block && i != 0 && i != sA) ? 1 : 0;   // a segment's first MMA starts D
+        const uint32_t d = per_block ? tD + db * N : tD;
 #ifndef UMMA_MMA_ASM16
 #define UMMA_MMA_ASM16 32   // widest N issued as one asm block (measured: +3% at N = 16, -4% at N >= 64)
 #endif
         if (!(a.dbg & 1)) {
           if (N <= UMMA_MMA_ASM16) {   // 16 MMAs (K = 256) from one asm block, one elect
-            mma_block16<N>(d, tA + ab * 128, sB32 + s * kStageB, idesc, acc0);
+            mma_block16<N>(d, tA + ab * 128, sB32 + s * kStageB, idesc, (!per_block && i > 0) ? 1 : 0);
           } else {
             const uint8_t* b = sB + s * kStageB;
 #pragma unroll
             for (int kk = 0; kk < 16; ++kk) {
               const uint64_t bd = desc_sw128(b + (kk >> 2) * N * 128 + (kk & 3) * 32);
-              mma_ts(d, tA + ab * 128 + kk * 8, bd, idesc, (kk > 0 || acc0) ? 1 : 0);
+              mma_ts(d, tA + ab * 128 + kk * 8, bd, idesc, (kk > 0 || (!per_block && i > 0)) ? 1 : 0);
             }
           }
         }
@@ -429,8 +406,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
           reinterpret_cast<long long*>(a.y)[i * 8 + 2] = clock64();
         mma_commit(&empty_b[s]);                     // activation stage reusable once these MMAs finish
         mma_commit(&a_empty[ab]);                    // TMEM A buffer reusable
-        if (per_block) mma_commit(&d_full[db]);
-        else if (i == sA - 1 || i == nblk - 1) mma_commit(&d_full[seg]);   // a segment's accumulator done
+        if (per_block || i == nblk - 1) mma_commit(&d_full[per_block ? db : 0]);
       }
     }
   } else {
@@ -444,7 +420,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
     float acc[NH];
 #pragma unroll
     for (int i = 0; i < NH; ++i) acc[i] = 0.0f;
-    float s_prev = 0.0f, s_first = 0.0f, s_first1 = 0.0f;
+    float s_prev = 0.0f, s_first = 0.0f;
     const uint32_t sW32 = smem_u32(sW) + tl * KS * UB;
 
     auto epilogue_block = [&](int i, float s) {        // acc += s * D_i (this thread's half of N)
@@ -485,7 +461,6 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
         if (lane == 0) mbar_arrive(&empty_w[s]);
       }
       if (i == 0) s_first = s_cur;
-      if (i == sA) s_first1 = s_cur;   // (stream-K: the second segment's rows)
       mbar_wait(&a_empty[ab], ((i / NA) & 1) ^ 1);      // MMA of block i-NA done with this A buffer
       if ((a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0 && i < 64)
         reinterpret_cast<long long*>(a.y)[i * 8 + 3] = clock64();
@@ -523,63 +498,39 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
       if (per_block && i > 0) epilogue_block(i - 1, s_prev);
       s_prev = s_cur;
     }
-    if (nblk > 0 && per_block) epilogue_block(nblk - 1, s_prev);
+    if (nblk > 0) {
+      if (per_block) epilogue_block(nblk - 1, s_prev);
+      else epilogue_block(0, s_first);   // the single accumulator (committed after the last block)
+    }
     griddep_wait();
-    // ---- store, per segment: a whole tile's K in this CTA -> y; else fp32 partials + the tile's
-    // last CTA sums them in contributor order (deterministic whatever the arrival order)
+    // ---- store: whole K in this CTA -> y; else partials + last-CTA reduction (fixed slice order)
+    const int row = mt * kRowsPerCta + r;
     const int n0 = nt * N + half_k * NH;
-    const int nseg = (a.sk && nblk > sA) ? 2 : 1;
-    for (int sg = 0; sg < nseg; ++sg) {
-      const int mts = sg ? mtA + 1 : mtA;
-      if (!per_block && nblk > 0) {   // the segment's accumulator (committed after its last block)
-        if (sg) {
+    if (a.ks == 1) {
+      if (row < a.rows && !(a.dbg & 4))
 #pragma unroll
-          for (int e = 0; e < NH; ++e) acc[e] = 0.0f;
-        }
-        epilogue_block(sg, sg ? s_first1 : s_first);
-      }
-      const int row = mts * kRowsPerCta + r;
-      int np = 1, q = 0, stride = 1;   // contributors to this tile, this CTA's index, slots per tile
-      if (a.sk) {
-        const int kb_lo = sg ? 0 : kbA, kb_hi = sg ? nblk - sA : kbA + sA;
-        if (kb_lo != 0 || kb_hi != a.nb) {   // owner(item) = ((item + 1) G - 1) / W
-          const int64_t W = (int64_t)a.m_tiles * a.nb, G = gridDim.x, t0 = (int64_t)mts * a.nb;
-          const int first = (int)(((t0 + 1) * G - 1) / W), last = (int)(((t0 + a.nb) * G - 1) / W);
-          np = last - first + 1;
-          q = (int)blockIdx.x - first;
-          stride = a.kq;
-        }
-      } else if (a.ks > 1) {
-        np = a.ks;
-        q = kslice;
-        stride = a.ks;
-      }
-      const int tile_mn = nt * a.m_tiles + mts;
-      if (np == 1) {
-        if (row < a.rows && !(a.dbg & 4))
-#pragma unroll
-          for (int e = 0; e < NH; ++e)
-            if (n0 + e < a.batch) store_y<T>(a.y, (int64_t)(n0 + e) * a.ldy + row, acc[e], a.out_f32);
-        continue;
-      }
-      float* part = a.ws + ((int64_t)tile_mn * stride + q) * (kRowsPerCta * N);
+        for (int e = 0; e < NH; ++e)
+          if (n0 + e < a.batch) store_y<T>(a.y, (int64_t)(n0 + e) * a.ldy + row, acc[e], a.out_f32);
+    } else {
+      const int tile_mn = nt * a.m_tiles + mt;
+      float* part = a.ws + ((int64_t)tile_mn * a.ks + kslice) * (kRowsPerCta * N);
 #pragma unroll
       for (int e = 0; e < NH; ++e) __stcg(part + (half_k * NH + e) * kRowsPerCta + r, acc[e]);
       __threadfence();
       asm volatile("bar.sync 1, %0;\n" ::"n"(kWorkers * 32) : "memory");   // all workers stored
-      if (threadIdx.x == 0) *flag = atomicAdd(a.counters + tile_mn, 1) == np - 1;
+      if (threadIdx.x == 0) *flag = atomicAdd(a.counters + tile_mn, 1) == a.ks - 1;
       asm volatile("bar.sync 1, %0;\n" ::"n"(kWorkers * 32) : "memory");
-      if (*flag) {   // the last CTA of this tile sums the partials in contributor order
+      if (*flag) {   // the last CTA of this tile sums the ks partials in slice order
         __threadfence();
-        const float* base = a.ws + (int64_t)tile_mn * stride * (kRowsPerCta * N);
-        if (row < a.rows && !(a.dbg & 4))
+        const float* base = a.ws + (int64_t)tile_mn * a.ks * (kRowsPerCta * N);
+        if (row < a.rows)
 #pragma unroll
           for (int e0 = 0; e0 < NH; e0 += 8) {   // 8 independent loads in flight per slice
             float v[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) v[e] = 0.0f;
-            for (int qq = 0; qq < np; ++qq) {
-              const float* src = base + (int64_t)qq * kRowsPerCta * N + (half_k * NH + e0) * kRowsPerCta + r;
+            for (int q = 0; q < a.ks; ++q) {
+              const float* src = base + (int64_t)q * kRowsPerCta * N + (half_k * NH + e0) * kRowsPerCta + r;
               float u[8];
 #pragma unroll
               for (int e = 0; e < 8; ++e) u[e] = __ldcg(src + e * kRowsPerCta);
@@ -623,15 +574,10 @@ constexpr size_t kUmmaCounterBytes = 256 * 1024;   // per-(m, n) tile counters (
 
 struct UmmaPlan {
   int n, n_tiles, m_tiles, ks;
-  int sk, kq, grid;   // stream-K (uniform-scale products with fewer tiles than SMs), slots per tile, CTAs
   size_t ws_bytes;
 };
 
-// sk_ok: the product may run stream-K (uniform scales: one accumulator per tile segment).  A
-// tile count below the SM count otherwise leaves SMs idle (11008 rows: 86 tiles on 148 SMs) or,
-// split evenly K-wise, ends on the tiles nobody helped; stream-K deals every CTA the same number
-// of (tile, 256-block) items, a CTA spanning at most two tiles.
-static UmmaPlan plan_umma(int batch, int rows, int cols, int ks_force, int sms, int sk_ok = 0) {
+static UmmaPlan plan_umma(int batch, int rows, int cols, int ks_force, int sms) {
   UmmaPlan p;
   p.n = batch <= 16 ? 16 : batch <= 32 ? 32 : batch <= 64 ? 64 : 128;
   p.n_tiles = (int)ceil_div(batch, p.n);
@@ -644,17 +590,6 @@ static UmmaPlan plan_umma(int batch, int rows, int cols, int ks_force, int sms, 
   if (ks < 1) ks = 1;
   p.ks = ks;
   p.ws_bytes = ks > 1 ? (size_t)base * ks * 128 * p.n * 4 : 0;
-  p.sk = 0;
-  p.kq = 0;
-  p.grid = base * ks;
-  const int64_t W = (int64_t)base * nb;
-  if (sk_ok && ks_force == 0 && p.n_tiles == 1 && base < sms && W >= 2 * sms) {
-    p.sk = 1;
-    p.ks = 1;
-    p.kq = (int)ceil_div(nb, W / sms) + 1;   // contributors to one tile, at most
-    p.grid = sms;
-    p.ws_bytes = (size_t)base * p.kq * 128 * p.n * 4;
-  }
   return p;
 }
 
@@ -671,8 +606,6 @@ size_t umma_workspace_bytes(int batch, int rows, int cols) {
     UmmaPlan p = plan_umma(batch, rows, cols, ks, sm_count());
     if (p.ws_bytes > ws) ws = p.ws_bytes;
   }
-  const UmmaPlan q = plan_umma(batch, rows, cols, 0, sm_count(), 1);
-  if (q.ws_bytes > ws) ws = q.ws_bytes;
   return kUmmaCounterBytes + ws;
 }
 
@@ -711,8 +644,7 @@ static int launch_umma(const CUtensorMap& map, const UmmaArgs& a, int grid, int 
 int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
               int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg,
               int out_f32) {
-  // (dev knob dbg & 8: no stream-K)
-  UmmaPlan p = plan_umma(batch, rows, cols, ks, sm_count(), uniform && !(dbg & 8));
+  UmmaPlan p = plan_umma(batch, rows, cols, ks, sm_count());
   if ((ldx % 8) != 0 || ((uintptr_t)x & 15) != 0) {
     set_error("tr_linear(umma): activations need 16-byte aligned rows (ldx %% 8 == 0)");
     return -1;
@@ -768,9 +700,7 @@ int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t l
   a.dbg = dbg;
   a.map3d = map3d;
   a.out_f32 = out_f32;
-  a.sk = p.sk;
-  a.kq = p.kq;
-  const int grid = p.grid;
+  const int grid = p.m_tiles * p.n_tiles * p.ks;
   const bool bf = act == kActBf16;
 #define TR_UMMA_CASE(NN)                                                                              \
   case NN:                                                                                            \

@@ -30,9 +30,3 @@ for i in (3,):
     names = ["staged", "loop_done", "stored", "x_landed"]
     print(f"{rows}x{cols} NW={NW} probe={extra & 12}: " + "  ".join(f"{nm} med {np.median(wt[:,:,k]):.0f} max {wt[:,:,k].max():.0f}"
                                                for k, nm in ((3, 'x_landed'), (0, 'staged'), (1, 'loop_done'), (2, 'stored'))) + " (cycles)")
-# kernel-boundary gap (%globaltimer, ns): first CTA of layer i+1 released from griddepcontrol.wait
-# after the last CTA end (warp 0) of layer i; plus layer i's span from its first release to its last end
-ct = [r[: 148 * 8].reshape(148, 8).astype(np.float64) for r in raw]
-gaps = [ct[i + 1][:, 1].min() - ct[i][:, 3].max() for i in range(1, L - 1)]
-spans = [ct[i][:, 3].max() - ct[i][:, 1].min() for i in range(1, L - 1)]
-print("boundary gap ns:", [round(g) for g in gaps], " layer span ns:", [round(s) for s in spans])
