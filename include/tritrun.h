@@ -114,9 +114,11 @@ TR_API size_t tr_linear_workspace_size(int fmt, int64_t batch, int64_t rows, int
 /* y[batch, rows] = x[batch, cols] @ W^T  (linear.py:137-166 gemm semantics with the
  * paper's fp16/bf16 activations, fp32 accumulation, RNE output).  w is the device
  * layout from tr_repack; x has leading dimension ldx, y has ldy (elements).
- * Batches >= 9 run the tcgen05 GEMM (K5), 3-8 the fp16 mma.sync GEMV (K3), 1-2 the
- * int8-slice GEMV (K3-S8: exact integer block sums over activations put on a 2^-24 grid
- * of each 256-column block's maximum).
+ * Dispatch (measured crossovers): batch 1-2 and batch 3-4 up to 4096 columns
+ * (8192 when the GEMM would walk >= 12 blocks per CTA) run the int8-slice GEMV (K3-S8: exact
+ * integer block sums over activations put on a 2^-24 grid of each 256-column block's
+ * maximum; TQ1 weights: K4); batch 5-8 the fp16 mma.sync GEMV (K3) up to 4096 columns when
+ * the GEMM would walk >= 12 blocks per CTA; everything else the tcgen05 GEMM (K5).
  * flags: TR_LINEAR_* bits | (knob << 8): GEMV CTA count / GEMM K split (0 = automatic). */
 TR_API int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
                      int act_dtype, int64_t ldx, int64_t ldy, int flags, void* workspace, size_t ws_bytes,
@@ -127,7 +129,9 @@ TR_API int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t bat
  *  TR_PRE_ADD_RMSNORM: x_eff = rmsnorm(x + delta) * gamma (delta may be NULL); x + delta
  *     (rounded) is also stored to x_out [batch, cols] (stride ldx) -- must not alias x;
  *  TR_PRE_SILU_MUL:    x_eff = silu(x[:, :cols]) * x[:, cols:2 cols]  (x = gate|up, ldx >= 2 cols).
- * Same arithmetic and roundings as tr_add_rmsnorm / tr_silu_mul followed by tr_linear. */
+ * Same arithmetic and roundings as tr_add_rmsnorm / tr_silu_mul followed by tr_linear.
+ * Under TR_LINEAR_PDL, w and gamma are read before the launch waits on the previous kernel
+ * (parameters, not activations): they must not be written by the kernel just before. */
 #define TR_PRE_ADD_RMSNORM 1
 #define TR_PRE_SILU_MUL 2
 TR_API int tr_linear_pre(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,

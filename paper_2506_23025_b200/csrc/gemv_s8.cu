@@ -167,6 +167,19 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
       }
     }
   }
+  // RMSNorm producer: gamma is a parameter like the weights (not written by the previous kernel,
+  // tr_linear_pre's contract), so this warp's first two gamma blocks load before the wait --
+  // per layer they are the one HBM miss among the producer's inputs
+  uint4 pgv[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+  if constexpr (PRE == 1) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int item = warp + i * NW;
+      if (item < nb * nrx)
+        pgv[i] = s8_load8(reinterpret_cast<const T*>(a.pre_gamma), (int64_t)(item >> lr) * kBlock + lane * 8, a.cols,
+                          a.x_vec);
+    }
+  }
   griddep_launch_dependents();
   griddep_wait();   // x belongs to the previous kernel until here
   if (trace) wait_clk = clock64();
@@ -188,13 +201,13 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   if (PRE == 1) {   // x = rmsnorm(x + delta) * gamma; CTA 0 stores x + delta (the residual)
     float* ss_buf = red;   // nb * nrx partial sums of squares
     const T* gam = reinterpret_cast<const T*>(a.pre_gamma);
-    // x, delta and gamma of this warp's first two blocks are loaded together up front (one
-    // memory latency instead of one per block and pass); gamma stays in registers for pass 2
-    uint4 pxv[2], pdv[2], pgv[2];
+    // x and delta of this warp's first two blocks are loaded together up front (one memory latency
+    // instead of one per block and pass); gamma (loaded before the wait) stays in registers for pass 2
+    uint4 pxv[2], pdv[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int item = warp + i * NW;
-      pxv[i] = pdv[i] = pgv[i] = make_uint4(0, 0, 0, 0);
+      pxv[i] = pdv[i] = make_uint4(0, 0, 0, 0);
       if (item < nb * nrx) {
         const int kb = item >> lr, br = item & (nrx - 1);
         const int64_t kx = (int64_t)kb * kBlock + lane * 8;
@@ -202,7 +215,6 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
           pxv[i] = s8_load8(xg + br * a.ldx, kx, a.cols, a.x_vec);
           if (a.pre_delta) pdv[i] = s8_load8(reinterpret_cast<const T*>(a.pre_delta) + br * a.ldx, kx, a.cols, a.x_vec);
         }
-        pgv[i] = s8_load8(gam, kx, a.cols, a.x_vec);
       }
     }
     issue_rest();
