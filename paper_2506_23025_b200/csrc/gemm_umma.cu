@@ -45,47 +45,54 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// D[tmem] (+)= A[tmem] * B[smem desc].  Called by a whole warp with warp-uniform operands;
-// elect.sync picks the issuing lane (a lane-0 branch makes the compiler serialise the
-// uniform-register set-up per MMA and costs ~3x the issue rate).
-__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, int acc) {
-  asm volatile(
-      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
-      ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc));
-}
 // The 16 MMAs of one 256-column block (A: 16 x 8 TMEM columns from a_tmem; B: the block's four
 // 128B-swizzled 64-K atoms at b_smem, N rows each), issued by one elected lane in one asm block.
 // The first MMA accumulates iff acc0; the rest always do.
 template <int N>
 __device__ __forceinline__ void mma_block16(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_smem, uint32_t idesc,
                                             int acc0) {
-  constexpr uint64_t kHi = (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
-  uint64_t dsc[16];
-#pragma unroll
-  for (int kk = 0; kk < 16; ++kk)
-    dsc[kk] = kHi | (uint64_t)(((b_smem + (uint32_t)((kk >> 2) * N * 128 + (kk & 3) * 32)) >> 4) & 0x3FFFu);
+  // The 16 descriptors are built inside the asm from the one base address, so ptxas moves one
+  // value into the uniform datapath per block instead of one per MMA.  Descriptor: start address
+  // (bits 0-13, 16-B units) | LBO 16 B | SBO 1024 B | version 1 | 128-B swizzle.
+  // B offset of MMA kk: (kk >> 2) * N * 128 + (kk & 3) * 32 bytes; A offset: kk * 8 columns.
   asm volatile(
-      "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %19, 0;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %2, p;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], %4, %2, 1;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], %5, %2, 1;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], %6, %2, 1;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], %7, %2, 1;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], %8, %2, 1;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], %9, %2, 1;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], %10, %2, 1;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], %11, %2, 1;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+72], %12, %2, 1;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+80], %13, %2, 1;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+88], %14, %2, 1;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+96], %15, %2, 1;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+104], %16, %2, 1;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+112], %17, %2, 1;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+120], %18, %2, 1;\n}\n"
-      ::"r"(d_tmem), "r"(a_tmem), "r"(idesc), "l"(dsc[0]), "l"(dsc[1]), "l"(dsc[2]), "l"(dsc[3]), "l"(dsc[4]),
-        "l"(dsc[5]), "l"(dsc[6]), "l"(dsc[7]), "l"(dsc[8]), "l"(dsc[9]), "l"(dsc[10]), "l"(dsc[11]), "l"(dsc[12]),
-        "l"(dsc[13]), "l"(dsc[14]), "l"(dsc[15]), "r"(acc0));
+      "{\n.reg .pred e, p;\n.reg .b32 t;\n.reg .b64 dd, hi;\n"
+      "mov.b64 hi, 0x4000404000010000;\n"
+      "elect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "add.u32 t, %2, 0;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], dd, %3, p;\n"
+      "add.u32 t, %2, 32;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], dd, %3, 1;\n"
+      "add.u32 t, %2, 64;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], dd, %3, 1;\n"
+      "add.u32 t, %2, 96;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], dd, %3, 1;\n"
+      "add.u32 t, %2, %5;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], dd, %3, 1;\n"
+      "add.u32 t, %2, %5+32;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], dd, %3, 1;\n"
+      "add.u32 t, %2, %5+64;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], dd, %3, 1;\n"
+      "add.u32 t, %2, %5+96;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], dd, %3, 1;\n"
+      "add.u32 t, %2, %6;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], dd, %3, 1;\n"
+      "add.u32 t, %2, %6+32;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+72], dd, %3, 1;\n"
+      "add.u32 t, %2, %6+64;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+80], dd, %3, 1;\n"
+      "add.u32 t, %2, %6+96;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+88], dd, %3, 1;\n"
+      "add.u32 t, %2, %7;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+96], dd, %3, 1;\n"
+      "add.u32 t, %2, %7+32;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+104], dd, %3, 1;\n"
+      "add.u32 t, %2, %7+64;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+112], dd, %3, 1;\n"
+      "add.u32 t, %2, %7+96;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+120], dd, %3, 1;\n}\n"
+      ::"r"(d_tmem), "r"(a_tmem), "r"(b_smem), "r"(idesc), "r"(acc0), "n"(N * 128), "n"(2 * N * 128),
+        "n"(3 * N * 128));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
@@ -103,23 +110,38 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
-  uint32_t r[8];
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr)
-               : "memory");
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+// 32 lanes x NC consecutive 32-bit columns -> r[NC] (NC = 8, 16 or 32); completes at tmem_wait_ld
+template <int NC>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[NC]) {
+  if constexpr (NC == 8) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr)
+                 : "memory");
+  } else if constexpr (NC == 16) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                 "[%16];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                   "=r"(r[15])
+                 : "r"(taddr)
+                 : "memory");
+  } else {
+    static_assert(NC == 32, "8, 16 or 32 columns");
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr)
+        : "memory");
+  }
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
-// shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row core groups 1024 B apart
-__device__ __forceinline__ uint64_t desc_sw128(const void* p) {
-  const uint64_t addr = smem_u32(p);
-  return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
-}
 
 // trit decode: field (digit d at mantissa bits 2j of each half, j-class of the E layout)
 // -> exact trit d - 1 as a half2 / bfloat162.  One LOP3 + one HFMA2.
@@ -326,6 +348,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
   const int dcols = per_block ? 2 * N : N;
   const int NA = (512 - dcols) / 128 < Cfg::kMaxA ? (512 - dcols) / 128 : Cfg::kMaxA;
   const uint32_t tA = tmem, tD = tmem + NA * 128;
+  if (tmem != 0u && threadIdx.x == 0) __trap();   // 512 columns: the whole TMEM, so address 0 (see MMA warp)
   griddep_launch_dependents();
 
   if (warp == kWorkers) {
@@ -386,22 +409,15 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
           reinterpret_cast<long long*>(a.y)[i * 8 + 1] = clock64();
         if (per_block) mbar_wait(&d_empty[db], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = per_block ? tD + db * N : tD;
-#ifndef UMMA_MMA_ASM16
-#define UMMA_MMA_ASM16 32   // widest N issued as one asm block (measured: +3% at N = 16, -4% at N >= 64)
-#endif
-        if (!(a.dbg & 1)) {
-          if (N <= UMMA_MMA_ASM16) {   // 16 MMAs (K = 256) from one asm block, one elect
-            mma_block16<N>(d, tA + ab * 128, sB32 + s * kStageB, idesc, (!per_block && i > 0) ? 1 : 0);
-          } else {
-            const uint8_t* b = sB + s * kStageB;
-#pragma unroll
-            for (int kk = 0; kk < 16; ++kk) {
-              const uint64_t bd = desc_sw128(b + (kk >> 2) * N * 128 + (kk & 3) * 32);
-              mma_ts(d, tA + ab * 128 + kk * 8, bd, idesc, (kk > 0 || (!per_block && i > 0)) ? 1 : 0);
-            }
-          }
-        }
+        // (the CTA allocates all 512 TMEM columns, so the allocation starts at address 0: the MMA
+        // addresses are compile-time / loop-uniform values in uniform registers, not a shared-memory
+        // load moved into uniform registers before every MMA -- checked once below)
+        const uint32_t d = per_block ? (uint32_t)(NA * 128 + db * N) : (uint32_t)(NA * 128);
+        // the block's 16 MMAs (K = 256) from one asm block, one elect, descriptors built in the
+        // uniform datapath (measured: b=16 -7%, b=64 -6%, b=128 -10% per layer against one MMA per
+        // call with descriptors moved in from ordinary registers)
+        if (!(a.dbg & 1))
+          mma_block16<N>(d, (uint32_t)(ab * 128), sB32 + s * kStageB, idesc, (!per_block && i > 0) ? 1 : 0);
         if ((a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64)
           reinterpret_cast<long long*>(a.y)[i * 8 + 2] = clock64();
         mma_commit(&empty_b[s]);                     // activation stage reusable once these MMAs finish
@@ -427,14 +443,16 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
       const int ab = i & 1;
       mbar_wait(&d_full[ab], (i >> 1) & 1);
       tc_fence_after();
+      // all of this thread's NH columns in flight at once (x32 / x16 / x8 loads), one wait
+      constexpr int NC = NH >= 32 ? 32 : NH;
+      uint32_t v[NH / NC][NC];
 #pragma unroll
-      for (int c8 = 0; c8 < NH; c8 += 8) {
-        float v[8];
-        tmem_ld8(tD + lane_off + ab * N + half_k * NH + c8, v);
-        tmem_wait_ld();
+      for (int c = 0; c < NH / NC; ++c) tmem_ld_cols<NC>(tD + lane_off + ab * N + half_k * NH + c * NC, v[c]);
+      tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 8; ++e) acc[c8 + e] = fmaf(s, v[e], acc[c8 + e]);
-      }
+      for (int c = 0; c < NH / NC; ++c)
+#pragma unroll
+        for (int e = 0; e < NC; ++e) acc[c * NC + e] = fmaf(s, __uint_as_float(v[c][e]), acc[c * NC + e]);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&d_empty[ab]);
