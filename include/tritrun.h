@@ -49,7 +49,8 @@ extern "C" {
 #define TR_LINEAR_COSCHEDULE 32    /* bit 5: chained with other GEMVs back to back: run the int8-slice GEMV
                                     * as 8-warp (half-SM) CTAs, so a layer and its successor can share
                                     * SMs (the successor prefetches its weights early); measured +5%
-                                    * on the BASELINE layer stack, neutral-to-worse as a default */
+                                    * on the BASELINE layer stack, neutral-to-worse as a default;
+                                    * batch 1 only: batch >= 2 always runs 16 warps */
 #define TR_LINEAR_EPI_SWIGLU 64    /* bit 6: W's rows are 16-row tiles alternating gate / up (2 F rows);
                                     * y[batch, F] = silu(gate) * up with the roundings of an fp16/bf16
                                     * gate|up store followed by tr_silu_mul (int8-slice GEMV, batch <= 4) */

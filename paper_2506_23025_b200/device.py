@@ -143,8 +143,8 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
     >= 7 the tcgen05 tensor-core GEMM, and 3-6 whichever the shape favours (measured
     crossovers, ``tritrun.h``); ``path`` ("umma" / "gemv" / "gemv_f16") forces one.  ``ctas`` forces the GEMV's CTA count and ``ksplit`` the GEMM's
     K split (0 = automatic); ``ws`` overrides the per-stream workspace.
-    ``cosched`` (TR_LINEAR_COSCHEDULE) marks a layer in a back-to-back GEMV chain: the
-    int8-slice GEMV then runs as half-SM CTAs so the next layer co-resides and prefetches.
+    ``cosched`` (TR_LINEAR_COSCHEDULE) marks a layer in a back-to-back GEMV chain: at batch 1
+    the int8-slice GEMV then runs as half-SM CTAs so the next layer co-resides and prefetches.
     ``epi_swiglu`` (TR_LINEAR_EPI_SWIGLU): W is a gate|up weight with 16-row tiles alternating
     gate / up (``interleave_gate_up``); the result is silu(gate) * up, rows // 2 wide.
     ``out_dtype=torch.float32`` (TR_LINEAR_OUT_F32) returns the fp32 accumulators unrounded --
