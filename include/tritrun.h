@@ -51,6 +51,8 @@ extern "C" {
                                     * SMs (the successor prefetches its weights early); measured +5%
                                     * on the BASELINE layer stack, neutral-to-worse as a default;
                                     * batch 1 only: batch >= 2 always runs 16 warps */
+#define TR_LINEAR_FULL_SM (1 << 28) /* bit 28: the int8-slice GEMV as 16-warp (whole-SM) CTAs at batch 1
+                                    * too (the decoder's fused-attention step measures best with it) */
 #define TR_LINEAR_EPI_SWIGLU 64    /* bit 6: W's rows are 16-row tiles alternating gate / up (2 F rows);
                                     * y[batch, F] = silu(gate) * up with the roundings of an fp16/bf16
                                     * gate|up store followed by tr_silu_mul (int8-slice GEMV, batch <= 4) */

@@ -27,6 +27,7 @@ LINEAR_GEMV_F16 = 16
 LINEAR_COSCHEDULE = 32
 LINEAR_EPI_SWIGLU = 64
 LINEAR_OUT_F32 = 128
+LINEAR_FULL_SM = 1 << 28
 PRE_ADD_RMSNORM = 1
 PRE_SILU_MUL = 2
 

@@ -59,6 +59,11 @@ size_t chain_workspace_bytes(int n_ops);
 //  * batch 5-8: the fp16 GEMV only for K <= 4096 columns on shapes K5 spreads badly (>= 12
 //    blocks per CTA, e.g. 11008 x 4096), else K5;
 //  * batch >= 9: K5.
+// int8-slice GEMV CTA width: 1 = half-SM 8-warp CTAs (TR_LINEAR_COSCHEDULE), 2 = whole-SM 16-warp
+// CTAs (TR_LINEAR_FULL_SM), 0 = by shape
+static int sched_mode(int flags) {
+  return (flags & TR_LINEAR_FULL_SM) ? 2 : (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0;
+}
 static bool prefer_umma(int64_t batch, int64_t rows, int64_t cols) {
   if (batch <= 2) return false;
   // blocks each K5 CTA walks: how well the GEMM spreads this shape (scripts/dev/crossover.py,
@@ -113,7 +118,7 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
     TR_REQUIRE(fmt == kFmtTq2 && s8 && !(flags & TR_LINEAR_FORCE_UMMA),
                "tr_linear: the SwiGLU epilogue runs on the int8-slice GEMV only (TQ2, batch <= 4)");
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, pdl, st, 0, nullptr, nullptr,
-                   nullptr, 0.0f, (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, 1, 0, kFmtTq2);
+                   nullptr, 0.0f, sched_mode(flags), 1, 0, kFmtTq2);
   }
   bool use_umma = aligned && (prefer_umma(batch, rows, cols) ||
                                (batch >= 3 && batch <= 8 && !gemv_stages_x((int)batch, (int)rows, (int)cols)));
@@ -133,7 +138,7 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
                      ws_bytes, pdl, st, (flags >> 24) & 0xF, out_f32);
   if (s8)
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, pdl, st, 0, nullptr, nullptr,
-                   nullptr, 0.0f, (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, 0, out_f32, fmt);
+                   nullptr, 0.0f, sched_mode(flags), 0, out_f32, fmt);
   const size_t esz = 2, ysz = out_f32 ? 4 : 2;
   for (int64_t n0 = 0; n0 < batch; n0 += 32) {
     const int nb_ = (int)(batch - n0 < 32 ? batch - n0 : 32);
@@ -163,7 +168,7 @@ int tr_linear_pre(int fmt, const void* w, const void* x, void* y, int64_t batch,
   if (batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols, kFmtTq2))
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, (flags >> 8) & 0xFFFF,
                    flags & TR_LINEAR_PDL, (cudaStream_t)stream, pre_op, delta, gamma, x_out, eps,
-                   (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0, (flags & TR_LINEAR_EPI_SWIGLU) ? 1 : 0, 0, kFmtTq2);
+                   sched_mode(flags), (flags & TR_LINEAR_EPI_SWIGLU) ? 1 : 0, 0, kFmtTq2);
   return gemv_tq2(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, (flags >> 8) & 0xFFFF,
                   flags & TR_LINEAR_PDL, (cudaStream_t)stream, pre_op, delta, gamma, x_out, eps, 0);
 }

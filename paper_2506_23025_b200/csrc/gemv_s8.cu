@@ -894,12 +894,12 @@ int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t
   const int units_of_work = epi ? a.n_tiles / 2 : a.n_tiles;   // (tile pairs for the SwiGLU epilogue)
   if (grid > units_of_work) grid = units_of_work;
   const bool bf = act != kActF16;
-  a.cosched = cosched;   // 8-warp CTAs (two per SM when their shared memory allows)
+  a.cosched = cosched == 1;   // 8-warp CTAs (two per SM when their shared memory allows); 2: 16 warps
   // batch >= 2 stages two or four activation rows per block, and sixteen warps halve each warp's
   // share of that serial staging: they win whatever the co-scheduling (BASELINE stack, us per
   // layer: b=2 8.05 -> 6.71, b=3 10.09 -> 9.17, b=4 13.02 -> 11.79; b=1 stays with 8 warps,
   // 6.08 vs 6.12; scripts/dev/nw_probe.py)
-  if (batch == 1 && (a.cosched || (s8_small(a.n_tiles, a.nb, grid) && !(a.dbg & 1))))   // (dev knob dbg&1: 16 warps)
+  if (batch == 1 && cosched != 2 && (a.cosched || (s8_small(a.n_tiles, a.nb, grid) && !(a.dbg & 1))))   // (dev knob dbg&1: 16 warps)
     return bf ? launch_s8<__nv_bfloat16, 8>(a, grid, pdl, st) : launch_s8<__half, 8>(a, grid, pdl, st);
   return bf ? launch_s8<__nv_bfloat16, 16>(a, grid, pdl, st) : launch_s8<__half, 16>(a, grid, pdl, st);
 }

@@ -119,6 +119,11 @@ class TernaryDecoder:
         self._positions = torch.arange(S, device=self.device)
         # TR_LINEAR_COSCHEDULE per decode GEMV (qkv, o, gate_up, down): 8-warp CTAs (measured)
         self.cosched = (False, False, False, False)
+        # TR_LINEAR_FULL_SM per decode GEMV (qkv, o, gate_up, down): 16-warp CTAs at batch 1.  The o
+        # projection runs after the 24-CTA attention kernel, so it has the SMs to itself: 1091 vs
+        # 1065 tok/s; the qkv GEMV must leave room for the attention kernel's early launch (16
+        # warps: 1003); gate|up and down are 16-warp by shape already (scripts/dev/decode_width.py)
+        self.full_sm = (False, True, False, False)
         # decode QKV GEMV + attention as one kernel (tr_qkv_attn_decode): off by default -- measured
         # slower inside the decode chain (its 16-warp CTAs keep the following o
         # projection from launching early); use_fused_attention(True) switches it on
@@ -240,7 +245,7 @@ class TernaryDecoder:
         for i in range(cfg.n_layers):
             lw = self.lin[i]
             # residual stream ping-pongs: the GEMV reads hs[cur] and stores hs[cur] + delta to hs[1 - cur]
-            cs = self.cosched
+            cs, fs = self.cosched, self.full_sm
             att = torch.empty((1, d), device=self.device, dtype=self.dtype)
             if self.fused_attn:   # add + RMSNorm -> QKV GEMV -> rotary, cache append, attention: one kernel
                 qkv = torch.empty((1, 3 * d), device=self.device, dtype=self.dtype)
@@ -252,15 +257,15 @@ class TernaryDecoder:
                           att.data_ptr(), H, D, S, D ** -0.5, self._qkv_attn_ws.data_ptr(),
                           self._qkv_attn_ws.numel(), _lib.LINEAR_PDL, st)
                 cur = 1 - cur
-                o = linear(att, lw["o"], pdl=True, cosched=cs[1])
+                o = linear(att, lw["o"], pdl=True, cosched=cs[1], full_sm=fs[1])
             else:
                 o = self._qkv_attn_unfused(i, hs, cur, delta, pos, att)
                 cur = 1 - cur
             if self.gate_up_il is not None:   # SwiGLU in the gate|up GEMV's epilogue
                 act_ = linear_pre(hs[cur], self.gate_up_il[i], _lib.PRE_ADD_RMSNORM, o, self.norm_mlp[i],
-                                  hs[1 - cur], cfg.eps, pdl=True, cosched=cs[2], epi_swiglu=True)
+                                  hs[1 - cur], cfg.eps, pdl=True, cosched=cs[2], epi_swiglu=True, full_sm=fs[2])
                 cur = 1 - cur
-                delta = linear(act_, lw["down"], pdl=True, cosched=cs[3])
+                delta = linear(act_, lw["down"], pdl=True, cosched=cs[3], full_sm=fs[3])
             else:
                 gu = linear_pre(hs[cur], lw["gate_up"], _lib.PRE_ADD_RMSNORM, o, self.norm_mlp[i], hs[1 - cur],
                                 cfg.eps, pdl=True, cosched=cs[2])
@@ -276,7 +281,7 @@ class TernaryDecoder:
         cfg, act, st, lw, cs = self.cfg, _ACT[self.dtype], _lib.stream_handle(), self.lin[i], self.cosched
         H, D, S = cfg.n_heads, cfg.head_dim, cfg.max_seq
         qkv = linear_pre(hs[cur], lw["qkv"], _lib.PRE_ADD_RMSNORM, delta, self.norm_attn[i], hs[1 - cur],
-                         cfg.eps, pdl=True, cosched=cs[0])
+                         cfg.eps, pdl=True, cosched=cs[0], full_sm=self.full_sm[0])
         if S <= 128:   # one CTA per head holds the whole cache
             _lib.call("tr_attn_decode", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(),
                       self.sin.data_ptr(), self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(),
@@ -285,7 +290,7 @@ class TernaryDecoder:
             _lib.call("tr_attn_decode_split", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(),
                       self.sin.data_ptr(), self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(),
                       H, D, S, D ** -0.5, self._attn_ws.data_ptr(), self._attn_ws.numel(), st)
-        return linear(att, lw["o"], pdl=True, cosched=cs[1])
+        return linear(att, lw["o"], pdl=True, cosched=cs[1], full_sm=self.full_sm[1])
 
     # -- serving --------------------------------------------------------------------------
     def prefill(self, prompt: torch.Tensor, graph: bool = True) -> None:

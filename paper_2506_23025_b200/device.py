@@ -133,7 +133,8 @@ _PATHS = {"auto": 0, "umma": _lib.LINEAR_FORCE_UMMA, "gemv": _lib.LINEAR_FORCE_G
 
 def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, pdl: bool = False,
            ctas: int = 0, ws: torch.Tensor | None = None, path: str = "auto", ksplit: int = 0,
-           cosched: bool = False, epi_swiglu: bool = False, out_dtype=None, _probe: int = 0) -> torch.Tensor:
+           cosched: bool = False, epi_swiglu: bool = False, out_dtype=None, full_sm: bool = False,
+           _probe: int = 0) -> torch.Tensor:
     """y[..., rows] = x[..., cols] @ W^T for fp16/bf16 x on the GPU (TriRun hot path).
 
     Accumulation is fp32: per 256-block partial sums are scaled by the block's
@@ -145,6 +146,7 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
     K split (0 = automatic); ``ws`` overrides the per-stream workspace.
     ``cosched`` (TR_LINEAR_COSCHEDULE) marks a layer in a back-to-back GEMV chain: at batch 1
     the int8-slice GEMV then runs as half-SM CTAs so the next layer co-resides and prefetches.
+    ``full_sm`` (TR_LINEAR_FULL_SM) asks for whole-SM 16-warp CTAs at batch 1 instead.
     ``epi_swiglu`` (TR_LINEAR_EPI_SWIGLU): W is a gate|up weight with 16-row tiles alternating
     gate / up (``interleave_gate_up``); the result is silu(gate) * up, rows // 2 wide.
     ``out_dtype=torch.float32`` (TR_LINEAR_OUT_F32) returns the fp32 accumulators unrounded --
@@ -182,6 +184,8 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
         flags |= _lib.LINEAR_EPI_SWIGLU
     if cosched:   # back-to-back GEMV chain: half-SM CTAs so consecutive layers co-reside
         flags |= _lib.LINEAR_COSCHEDULE
+    if full_sm:
+        flags |= _lib.LINEAR_FULL_SM
     # one knob: the GEMV's CTA count or the tensor-core GEMM's K split, whichever path runs
     flags |= ((int(ksplit or ctas)) & 0xFFFF) << 8
     flags |= (int(_probe) & 0xF) << 24   # development probes (see csrc); 0 in production
@@ -196,7 +200,7 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
 def linear_pre(x: torch.Tensor, w: TernaryWeight, pre: int, delta: torch.Tensor | None = None,
                gamma: torch.Tensor | None = None, x_out: torch.Tensor | None = None, eps: float = 1e-5,
                out: torch.Tensor | None = None, pdl: bool = False, cosched: bool = False,
-               epi_swiglu: bool = False) -> torch.Tensor:
+               epi_swiglu: bool = False, full_sm: bool = False) -> torch.Tensor:
     """``linear`` with the producer of its input fused into the GEMV's activation staging.
 
     pre = _lib.PRE_ADD_RMSNORM: y = rmsnorm(x + delta) * gamma @ W^T, and x + delta is
@@ -211,6 +215,7 @@ def linear_pre(x: torch.Tensor, w: TernaryWeight, pre: int, delta: torch.Tensor 
     _lib.call("tr_linear_pre", int(w.fmt), w.data.data_ptr(), x2.data_ptr(), out.data_ptr(), batch, w.rows, w.cols,
               _ACT[x.dtype], x2.stride(0), out.stride(0),
               (_lib.LINEAR_PDL if pdl else 0) | (_lib.LINEAR_COSCHEDULE if cosched else 0)
+              | (_lib.LINEAR_FULL_SM if full_sm else 0)
               | (_lib.LINEAR_EPI_SWIGLU if epi_swiglu else 0), int(pre), ptr(delta),
               ptr(gamma), ptr(x_out), float(eps), _lib.stream_handle())
     return out

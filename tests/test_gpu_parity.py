@@ -1063,3 +1063,21 @@ def test_decoder_fused_attention_matches_unfused(tp):
         m.decode(11)
     torch.cuda.synchronize()
     assert torch.equal(a.out_tokens[9:20], b.out_tokens[9:20])
+
+
+@pytest.mark.parametrize("rows,cols", [(3072, 3072), (9216, 3072), (4096, 11008)])
+def test_full_sm_gemv_vs_oracle(tp, rows, cols):
+    """TR_LINEAR_FULL_SM (16-warp int8-slice GEMV CTAs at batch 1) against the float64 oracle, and
+    against the default width within the same tolerance (the K split over warps differs)."""
+    g = torch.Generator(device="cuda").manual_seed(rows + cols)
+    W = (torch.randint(-1, 2, (rows, cols), device="cuda", generator=g).float()
+         * (0.02 * (1 + torch.rand((rows, 1), device="cuda", generator=g))))
+    w = tp.TernaryWeight.from_float(W)
+    x = (torch.rand((1, cols), device="cuda", generator=g) * 2 - 1).half()
+    y_full = tp.linear(x, w, full_sm=True).float()
+    y_def = tp.linear(x, w).float()
+    payload, scales = (t.cpu().numpy() for t in w.unpack())
+    ref = torch.from_numpy(orc.gemv_reference_batch(payload, scales, cols, 2, x.float().cpu().numpy())).float()
+    scale = ref.abs().max()
+    assert ((y_full.cpu() - ref).abs().max() / scale).item() <= 2e-3
+    assert ((y_full - y_def).abs().max().cpu() / scale).item() <= 2e-3
