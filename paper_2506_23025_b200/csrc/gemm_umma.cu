@@ -31,6 +31,12 @@ namespace tr {
 
 namespace umma {
 
+#ifndef UMMA_TRACE
+#define UMMA_TRACE 0
+#endif
+// CTA-0 clock trace (probe 4) compiled in only for dev builds (-DUMMA_TRACE=1): its checks sat in
+// the decode and MMA loops of every launch
+constexpr bool kTrace = UMMA_TRACE != 0;
 constexpr int kWorkers = 8;                    // decode/epilogue warps
 constexpr int kThreads = (kWorkers + 2) * 32;  // + producer warp + MMA warp
 constexpr int kRowsPerCta = 128;
@@ -51,48 +57,33 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 template <int N>
 __device__ __forceinline__ void mma_block16(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_smem, uint32_t idesc,
                                             int acc0) {
-  // The 16 descriptors are built inside the asm from the one base address, so ptxas moves one
-  // value into the uniform datapath per block instead of one per MMA.  Descriptor: start address
-  // (bits 0-13, 16-B units) | LBO 16 B | SBO 1024 B | version 1 | 128-B swizzle.
-  // B offset of MMA kk: (kk >> 2) * N * 128 + (kk & 3) * 32 bytes; A offset: kk * 8 columns.
+  // One descriptor is built from the base address inside the asm; the other 15 are that plus the
+  // MMA's offset in 16-B units (the 14-bit start field cannot carry: shared addresses stay below
+  // 256 KB), so ptxas keeps the whole sequence in the uniform datapath at one add per MMA.
+  // Descriptor: start address (bits 0-13, 16-B units) | LBO 16 B | SBO 1024 B | version 1 |
+  // 128-B swizzle.  B offset of MMA kk: (kk >> 2) * N * 128 + (kk & 3) * 32 bytes; A: kk * 8 columns.
   asm volatile(
-      "{\n.reg .pred e, p;\n.reg .b32 t;\n.reg .b64 dd, hi;\n"
-      "mov.b64 hi, 0x4000404000010000;\n"
-      "elect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
-      "add.u32 t, %2, 0;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], dd, %3, p;\n"
-      "add.u32 t, %2, 32;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], dd, %3, 1;\n"
-      "add.u32 t, %2, 64;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], dd, %3, 1;\n"
-      "add.u32 t, %2, 96;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], dd, %3, 1;\n"
-      "add.u32 t, %2, %5;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], dd, %3, 1;\n"
-      "add.u32 t, %2, %5+32;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], dd, %3, 1;\n"
-      "add.u32 t, %2, %5+64;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], dd, %3, 1;\n"
-      "add.u32 t, %2, %5+96;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], dd, %3, 1;\n"
-      "add.u32 t, %2, %6;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], dd, %3, 1;\n"
-      "add.u32 t, %2, %6+32;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+72], dd, %3, 1;\n"
-      "add.u32 t, %2, %6+64;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+80], dd, %3, 1;\n"
-      "add.u32 t, %2, %6+96;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+88], dd, %3, 1;\n"
-      "add.u32 t, %2, %7;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+96], dd, %3, 1;\n"
-      "add.u32 t, %2, %7+32;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+104], dd, %3, 1;\n"
-      "add.u32 t, %2, %7+64;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+112], dd, %3, 1;\n"
-      "add.u32 t, %2, %7+96;\nshr.u32 t, t, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 dd, t;\nor.b64 dd, dd, hi;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+120], dd, %3, 1;\n}\n"
-      ::"r"(d_tmem), "r"(a_tmem), "r"(b_smem), "r"(idesc), "r"(acc0), "n"(N * 128), "n"(2 * N * 128),
-        "n"(3 * N * 128));
+      "{\n.reg .pred e, p;\n.reg .b32 t;\n.reg .b64 base, dd;\n"
+      "shr.u32 t, %2, 4;\nand.b32 t, t, 0x3FFF;\ncvt.u64.u32 base, t;\nor.b64 base, base, 0x4000404000010000;\n"
+      "elect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n@!e bra SKIP_%=;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], base, %3, p;\n"
+      "add.s64 dd, base, 2;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], dd, %3, 1;\n"
+      "add.s64 dd, base, 4;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], dd, %3, 1;\n"
+      "add.s64 dd, base, 6;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], dd, %3, 1;\n"
+      "add.s64 dd, base, %5;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], dd, %3, 1;\n"
+      "add.s64 dd, base, %5+2;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], dd, %3, 1;\n"
+      "add.s64 dd, base, %5+4;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], dd, %3, 1;\n"
+      "add.s64 dd, base, %5+6;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], dd, %3, 1;\n"
+      "add.s64 dd, base, %6;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], dd, %3, 1;\n"
+      "add.s64 dd, base, %6+2;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1+72], dd, %3, 1;\n"
+      "add.s64 dd, base, %6+4;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1+80], dd, %3, 1;\n"
+      "add.s64 dd, base, %6+6;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1+88], dd, %3, 1;\n"
+      "add.s64 dd, base, %7;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1+96], dd, %3, 1;\n"
+      "add.s64 dd, base, %7+2;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1+104], dd, %3, 1;\n"
+      "add.s64 dd, base, %7+4;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1+112], dd, %3, 1;\n"
+      "add.s64 dd, base, %7+6;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1+120], dd, %3, 1;\n"
+      "SKIP_%=:\n}\n"
+      ::"r"(d_tmem), "r"(a_tmem), "r"(b_smem), "r"(idesc), "r"(acc0), "n"(N * 8), "n"(2 * N * 8), "n"(3 * N * 8));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
@@ -402,10 +393,10 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
       for (int i = 0; i < nblk; ++i) {
         const int s = i % RB, ab = i % NA, db = i & 1;
         mbar_wait(&full_b[s], (i / RB) & 1);         // activations landed
-        if ((a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64)
+        if (kTrace && (a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64)
           reinterpret_cast<long long*>(a.y)[i * 8 + 0] = clock64();
         mbar_wait(&a_full[ab], (i / NA) & 1);        // trits decoded into TMEM
-        if ((a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64)
+        if (kTrace && (a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64)
           reinterpret_cast<long long*>(a.y)[i * 8 + 1] = clock64();
         if (per_block) mbar_wait(&d_empty[db], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -418,11 +409,13 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
         // call with descriptors moved in from ordinary registers)
         if (!(a.dbg & 1))
           mma_block16<N>(d, (uint32_t)(ab * 128), sB32 + s * kStageB, idesc, (!per_block && i > 0) ? 1 : 0);
-        if ((a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64)
+        if (kTrace && (a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64)
           reinterpret_cast<long long*>(a.y)[i * 8 + 2] = clock64();
         mma_commit(&empty_b[s]);                     // activation stage reusable once these MMAs finish
         mma_commit(&a_empty[ab]);                    // TMEM A buffer reusable
         if (per_block || i == nblk - 1) mma_commit(&d_full[per_block ? db : 0]);
+        if (kTrace && (a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64)
+          reinterpret_cast<long long*>(a.y)[i * 8 + 5] = clock64();
       }
     }
   } else {
@@ -458,63 +451,68 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
       if (lane == 0) mbar_arrive(&d_empty[ab]);
     };
 
-    for (int i = 0; i < nblk; ++i) {
-      const int si = i / KS, j = i - si * KS, s = si % RW, ab = i % NA;
-      if (j == 0) mbar_wait(&full_w[s], (si / RW) & 1);
-      const uint32_t unit = sW32 + s * kStageW + j * UB;
-      uint4 wv[2];
-      uint32_t wq[7];
-      if constexpr (FMT == kFmtTq1) {
-#pragma unroll
-        for (int m = 0; m < 7; ++m) wq[m] = ld_shared_u32(unit + rt * kQ1RowBytes + (half_k * 6 + m) * 4);
-      } else {
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) wv[cc] = ld_shared_v4(unit + t16_word(hrow, 2 * half_k + cc, g) * 16);
-      }
-      const uint32_t sv = ld_shared_u32(unit + Cfg::TBB + g * 4);
-      const float s_cur = __half2float(hrow ? __high2half(*reinterpret_cast<const __half2*>(&sv))
-                                            : __low2half(*reinterpret_cast<const __half2*>(&sv)));
-      if (j == KS - 1 || i == nblk - 1) {               // weight stage fully read into registers
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_w[s]);
-      }
-      if (i == 0) s_first = s_cur;
-      mbar_wait(&a_empty[ab], ((i / NA) & 1) ^ 1);      // MMA of block i-NA done with this A buffer
-      if ((a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0 && i < 64)
-        reinterpret_cast<long long*>(a.y)[i * 8 + 3] = clock64();
-      tc_fence_after();
-      if constexpr (FMT == kFmtTq1) {
-        if (!(a.dbg & 2)) {
-          uint32_t col[64];
-          decode_q1<T>(wq, half_k, col);
-          tmem_st32(tA + lane_off + ab * 128 + half_k * 64, *reinterpret_cast<const uint32_t(*)[32]>(col));
-          tmem_st32(tA + lane_off + ab * 128 + half_k * 64 + 32, *reinterpret_cast<const uint32_t(*)[32]>(col + 32));
-        }
-      } else
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        if (a.dbg & 2) break;
-        const uint32_t W[4] = {wv[cc].x, wv[cc].y, wv[cc].z, wv[cc].w};
-        uint32_t col[32];
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const uint32_t w8 = W[w] >> 8;
-#pragma unroll
-          for (int hb = 0; hb < 2; ++hb)
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj)   // columns (2q, 2q+1) of the chunk: q = 16(w>>1) + 8hb + 2jj + (w&1)
-              col[16 * (w >> 1) + 8 * hb + 2 * jj + (w & 1)] = Dec<T>::trit2(W[w], w8, hb, jj);
-        }
-        tmem_st32(tA + lane_off + ab * 128 + (2 * half_k + cc) * 32, col);
-      }
+    auto finish_block = [&](int i, float s_cur) {
       tmem_wait_st();
-      if ((a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0 && i < 64)
-        reinterpret_cast<long long*>(a.y)[i * 8 + 4] = clock64();
+      if (kTrace && (a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64 && (warp == 0 || warp == 1 || warp == 6))
+        reinterpret_cast<long long*>(a.y)[i * 8 + (warp == 0 ? 4 : warp == 1 ? 6 : 7)] = clock64();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&a_full[ab]);
+      if (lane == 0) mbar_arrive(&a_full[i % NA]);
+      if (i == 0) s_first = s_cur;
       if (per_block && i > 0) epilogue_block(i - 1, s_prev);
       s_prev = s_cur;
+    };
+    {   // per block: weights to registers, wait for the A buffer, decode 32 columns at a time into TMEM
+      for (int i = 0; i < nblk; ++i) {
+        const int si = i / KS, j = i - si * KS, s = si % RW, ab = i % NA;
+        if (j == 0) mbar_wait(&full_w[s], (si / RW) & 1);
+        const uint32_t unit = sW32 + s * kStageW + j * UB;
+        uint4 wv[2];
+        uint32_t wq[7];
+        if constexpr (FMT == kFmtTq1) {
+#pragma unroll
+          for (int m = 0; m < 7; ++m) wq[m] = ld_shared_u32(unit + rt * kQ1RowBytes + (half_k * 6 + m) * 4);
+        } else {
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) wv[cc] = ld_shared_v4(unit + t16_word(hrow, 2 * half_k + cc, g) * 16);
+        }
+        const uint32_t sv = ld_shared_u32(unit + Cfg::TBB + g * 4);
+        const float s_cur = __half2float(hrow ? __high2half(*reinterpret_cast<const __half2*>(&sv))
+                                              : __low2half(*reinterpret_cast<const __half2*>(&sv)));
+        if (j == KS - 1 || i == nblk - 1) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty_w[s]);
+        }
+        mbar_wait(&a_empty[ab], ((i / NA) & 1) ^ 1);
+        if (kTrace && (a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0 && i < 64)
+          reinterpret_cast<long long*>(a.y)[i * 8 + 3] = clock64();
+        tc_fence_after();
+        if constexpr (FMT == kFmtTq1) {
+          if (!(a.dbg & 2)) {
+            uint32_t col[64];
+            decode_q1<T>(wq, half_k, col);
+            tmem_st32(tA + lane_off + ab * 128 + half_k * 64, *reinterpret_cast<const uint32_t(*)[32]>(col));
+            tmem_st32(tA + lane_off + ab * 128 + half_k * 64 + 32, *reinterpret_cast<const uint32_t(*)[32]>(col + 32));
+          }
+        } else
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          if (a.dbg & 2) break;
+          const uint32_t W[4] = {wv[cc].x, wv[cc].y, wv[cc].z, wv[cc].w};
+          uint32_t col[32];
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const uint32_t w8 = W[w] >> 8;
+#pragma unroll
+            for (int hb = 0; hb < 2; ++hb)
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj)
+                col[16 * (w >> 1) + 8 * hb + 2 * jj + (w & 1)] = Dec<T>::trit2(W[w], w8, hb, jj);
+          }
+          tmem_st32(tA + lane_off + ab * 128 + (2 * half_k + cc) * 32, col);
+        }
+        finish_block(i, s_cur);
+      }
     }
     if (nblk > 0) {
       if (per_block) epilogue_block(nblk - 1, s_prev);
@@ -525,7 +523,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
     const int row = mt * kRowsPerCta + r;
     const int n0 = nt * N + half_k * NH;
     if (a.ks == 1) {
-      if (row < a.rows && !(a.dbg & 4))
+      if (row < a.rows && !(kTrace && (a.dbg & 4)))
 #pragma unroll
         for (int e = 0; e < NH; ++e)
           if (n0 + e < a.batch) store_y<T>(a.y, (int64_t)(n0 + e) * a.ldy + row, acc[e], a.out_f32);

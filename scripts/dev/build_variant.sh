@@ -1,9 +1,9 @@
 #!/bin/bash
-# Dev A/B: build libtritrun.so with extra -D flags into scripts/dev/var/<name>/ (load with TRITRUN_LIB=...)
+# Dev A/B: build libtritrun.so with extra -D flags into scripts/dev/ab/<name>/ (load with TRITRUN_LIB=...)
 set -e
 name=$1; shift
 cd "$(dirname "$0")/../../paper_2506_23025_b200"
-out=../scripts/dev/var/$name; mkdir -p $out/obj
+out=../scripts/dev/ab/$name; mkdir -p $out/obj
 for f in csrc/*.cu; do
   b=$(basename $f .cu)
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
