@@ -279,7 +279,7 @@ def dense_stack(weights, batch, dtype=None):
     return g, dws
 
 
-def _time_layers(ws, x, path="auto", reps=10):
+def _time_layers(ws, x, path="auto", reps=10, probe=0):
     """Per-layer device time of independent products over rotating weights (graph + PDL)."""
     import torch
     import paper_2506_23025_b200 as tp
@@ -288,11 +288,11 @@ def _time_layers(ws, x, path="auto", reps=10):
     s, g = torch.cuda.Stream(), torch.cuda.CUDAGraph()
     with torch.cuda.stream(s):
         for w, y in zip(ws, ys):
-            tp.linear(x, w, out=y, pdl=True, path=path)
+            tp.linear(x, w, out=y, pdl=True, path=path, _probe=probe)
         s.synchronize()
         with torch.cuda.graph(g, stream=s):
             for w, y in zip(ws, ys):
-                tp.linear(x, w, out=y, pdl=True, path=path)
+                tp.linear(x, w, out=y, pdl=True, path=path, _probe=probe)
     return timed_graph(g.replay, reps, 3, None) / reps / len(ws)
 
 

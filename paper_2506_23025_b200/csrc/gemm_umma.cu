@@ -275,7 +275,10 @@ __device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
   return r;
 }
 
-template <typename T, int N, int FMT>
+// SPLIT: the product is split along K (a.ks > 1).  The unsplit instance carries no reduction code:
+// its mere presence cost the unsplit product ~6% (11008x4096 b=16: 10.0 vs 9.4 us), through the
+// register allocation of the decode and MMA loops
+template <typename T, int N, int FMT, bool SPLIT>
 __global__ void __launch_bounds__(umma::kThreads, 1)
     k_gemm_umma(const __grid_constant__ CUtensorMap tmx, const UmmaArgs a) {
   using namespace umma;
@@ -522,12 +525,12 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
     // ---- store: whole K in this CTA -> y; else partials + last-CTA reduction (fixed slice order)
     const int row = mt * kRowsPerCta + r;
     const int n0 = nt * N + half_k * NH;
-    if (a.ks == 1) {
+    if (!SPLIT || (a.dbg & 8)) {   // (dev probe 8: split-K slices store unreduced -- timing only)
       if (row < a.rows && !(kTrace && (a.dbg & 4)))
 #pragma unroll
         for (int e = 0; e < NH; ++e)
           if (n0 + e < a.batch) store_y<T>(a.y, (int64_t)(n0 + e) * a.ldy + row, acc[e], a.out_f32);
-    } else {
+    } else if constexpr (SPLIT) {
       const int tile_mn = nt * a.m_tiles + mt;
       float* part = a.ws + ((int64_t)tile_mn * a.ks + kslice) * (kRowsPerCta * N);
 #pragma unroll
@@ -539,22 +542,30 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
       if (*flag) {   // the last CTA of this tile sums the ks partials in slice order
         __threadfence();
         const float* base = a.ws + (int64_t)tile_mn * a.ks * (kRowsPerCta * N);
-        if (row < a.rows)
+        // up to 32 independent loads in flight per slice (the sum is latency-bound: one L2 round
+        // trip per slice and chunk); this CTA's own slice comes from its registers
+        constexpr int EC = NH < 32 ? NH : 32;
+        if (row < a.rows && !(kTrace && (a.dbg & 4)))
 #pragma unroll
-          for (int e0 = 0; e0 < NH; e0 += 8) {   // 8 independent loads in flight per slice
-            float v[8];
+          for (int e0 = 0; e0 < NH; e0 += EC) {
+            float v[EC];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) v[e] = 0.0f;
+            for (int e = 0; e < EC; ++e) v[e] = 0.0f;
             for (int q = 0; q < a.ks; ++q) {
-              const float* src = base + (int64_t)q * kRowsPerCta * N + (half_k * NH + e0) * kRowsPerCta + r;
-              float u[8];
+              float u[EC];
+              if (q == kslice) {
 #pragma unroll
-              for (int e = 0; e < 8; ++e) u[e] = __ldcg(src + e * kRowsPerCta);
+                for (int e = 0; e < EC; ++e) u[e] = acc[e0 + e];
+              } else {
+                const float* src = base + (int64_t)q * kRowsPerCta * N + (half_k * NH + e0) * kRowsPerCta + r;
 #pragma unroll
-              for (int e = 0; e < 8; ++e) v[e] += u[e];
+                for (int e = 0; e < EC; ++e) u[e] = __ldcg(src + e * kRowsPerCta);
+              }
+#pragma unroll
+              for (int e = 0; e < EC; ++e) v[e] += u[e];
             }
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
+            for (int e = 0; e < EC; ++e)
               if (n0 + e0 + e < a.batch) store_y<T>(a.y, (int64_t)(n0 + e0 + e) * a.ldy + row, v[e], a.out_f32);
           }
         if (threadIdx.x == 0) a.counters[tile_mn] = 0;   // self-reset
@@ -596,8 +607,12 @@ struct UmmaPlan {
 static UmmaPlan plan_umma(int batch, int rows, int cols, int ks_force, int sms) {
   UmmaPlan p;
   p.n = batch <= 16 ? 16 : batch <= 32 ? 32 : batch <= 64 ? 64 : 128;
-  p.n_tiles = (int)ceil_div(batch, p.n);
   p.m_tiles = (int)(rows_padded(rows) / 128);
+  // few row tiles at a wide batch: two 64-column tiles per row tile instead of one of 128 and half
+  // the K split -- the same MMA work per CTA, half the slices (each half the bytes) to sum
+  // (4096^2 b=128: 14.1 -> 11.0 us; 4096x11008 b=128: neutral)
+  if (p.n == 128 && 2 * p.m_tiles <= sms) p.n = 64;
+  p.n_tiles = (int)ceil_div(batch, p.n);
   const int nb = (int)ceil_div(cols, kBlock);
   const int base = p.m_tiles * p.n_tiles;
   int ks = ks_force > 0 ? ks_force : (base >= sms ? 1 : sms / base);
@@ -627,13 +642,13 @@ size_t umma_workspace_bytes(int batch, int rows, int cols) {
 
 template <typename T, int N, int FMT>
 static int launch_umma(const CUtensorMap& map, const UmmaArgs& a, int grid, int pdl, cudaStream_t st) {
-  auto kern = k_gemm_umma<T, N, FMT>;
-  static int configured_dev = -1;
+  auto kern = a.ks > 1 ? k_gemm_umma<T, N, FMT, true> : k_gemm_umma<T, N, FMT, false>;
+  static int configured_dev[2] = {-1, -1};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (configured_dev != dev) {
+  if (configured_dev[a.ks > 1] != dev) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UmmaCfg<T, N, FMT>::kSmem);
-    configured_dev = dev;
+    configured_dev[a.ks > 1] = dev;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);

@@ -18,7 +18,7 @@ for rows, cols in ((11008, 4096), (4096, 4096), (4096, 11008)):
         ws.append(tp.TernaryWeight.from_float(gam * T))
     for b in (16, 64, 128):
         x = bench.uniform_x(b, cols, b)
-        res[f"{rows}x{cols}_b{b}"] = round(bench._time_layers(ws, x, path="umma") * 1e3, 2)
+        res[f"{rows}x{cols}_b{b}"] = round(bench._time_layers(ws, x, path="umma", probe=int(os.environ.get("PROBE", "0"))) * 1e3, 2)
     del ws
     torch.cuda.empty_cache()
 print(os.environ.get("TRITRUN_LIB", "default"), json.dumps(res))
