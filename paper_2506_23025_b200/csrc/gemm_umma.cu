@@ -608,10 +608,12 @@ static UmmaPlan plan_umma(int batch, int rows, int cols, int ks_force, int sms) 
   UmmaPlan p;
   p.n = batch <= 16 ? 16 : batch <= 32 ? 32 : batch <= 64 ? 64 : 128;
   p.m_tiles = (int)(rows_padded(rows) / 128);
-  // few row tiles at a wide batch: two 64-column tiles per row tile instead of one of 128 and half
-  // the K split -- the same MMA work per CTA, half the slices (each half the bytes) to sum
-  // (4096^2 b=128: 14.1 -> 11.0 us; 4096x11008 b=128: neutral)
-  if (p.n == 128 && 2 * p.m_tiles <= sms) p.n = 64;
+  // few row tiles, wide batch, short K: two half-width column tiles per row tile and half the K
+  // split -- the same MMA work per CTA, half the slices (each half the bytes) to sum, which
+  // dominates when each CTA walks only a few blocks (4096^2: b=128 14.1 -> 11.0 us, b=64 9.5 ->
+  // 9.0; with 43 blocks of K the narrower MMAs cost more than the sum saves: 4096x11008 b=64
+  // 13.4 -> 16.4)
+  if (ceil_div(cols, kBlock) <= 16 && 2 * p.m_tiles <= sms && p.n >= 64) p.n /= 2;
   p.n_tiles = (int)ceil_div(batch, p.n);
   const int nb = (int)ceil_div(cols, kBlock);
   const int base = p.m_tiles * p.n_tiles;
