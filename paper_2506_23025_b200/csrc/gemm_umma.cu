@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
         __threadfence();
         const float* base = a.ws + (int64_t)tile_mn * a.ks * (kRowsPerCta * N);
         // up to 32 independent loads in flight per slice (the sum is latency-bound: one L2 round
-        // trip per slice and chunk); this CTA's own slice comes from its registers
+        // trip per slice and chunk)
         constexpr int EC = NH < 32 ? NH : 32;
         if (row < a.rows && !(kTrace && (a.dbg & 4)))
 #pragma unroll
@@ -552,15 +552,10 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
 #pragma unroll
             for (int e = 0; e < EC; ++e) v[e] = 0.0f;
             for (int q = 0; q < a.ks; ++q) {
-              float u[EC];
-              if (q == kslice) {
+              float u[EC];   // (this CTA's own slice too: taking it from registers measured slower)
+              const float* src = base + (int64_t)q * kRowsPerCta * N + (half_k * NH + e0) * kRowsPerCta + r;
 #pragma unroll
-                for (int e = 0; e < EC; ++e) u[e] = acc[e0 + e];
-              } else {
-                const float* src = base + (int64_t)q * kRowsPerCta * N + (half_k * NH + e0) * kRowsPerCta + r;
-#pragma unroll
-                for (int e = 0; e < EC; ++e) u[e] = __ldcg(src + e * kRowsPerCta);
-              }
+              for (int e = 0; e < EC; ++e) u[e] = __ldcg(src + e * kRowsPerCta);
 #pragma unroll
               for (int e = 0; e < EC; ++e) v[e] += u[e];
             }
