@@ -120,9 +120,9 @@ TR_API size_t tr_linear_workspace_size(int fmt, int64_t batch, int64_t rows, int
  * Dispatch (measured crossovers): batch 1-2, and batch 3-4 up to 4096 columns
  * (8192 when the GEMM would walk >= 12 blocks per CTA) unless the GEMM would walk <= 4 blocks
  * per CTA, run the int8-slice GEMV (K3-S8: exact integer block sums over activations put on a
- * 2^-24 grid of each 256-column block's maximum; TQ1 weights: K4); batch 5-6 the fp16
- * mma.sync GEMV (K3) up to 4096 columns when the GEMM would walk >= 12 blocks per CTA;
- * everything else the tcgen05 GEMM (K5).
+ * 2^-24 grid of each 256-column block's maximum; TQ1 weights: K4); everything else the tcgen05
+ * GEMM (K5).  The fp16 mma.sync GEMV (K3) runs on request (TR_LINEAR_GEMV_F16 / FORCE_GEMV) and
+ * where K3-S8 cannot stage the activations and K5 cannot take them (unaligned rows).
  * flags: TR_LINEAR_* bits | (knob << 8): GEMV CTA count / GEMM K split (0 = automatic). */
 TR_API int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
                      int act_dtype, int64_t ldx, int64_t ldy, int flags, void* workspace, size_t ws_bytes,

@@ -66,15 +66,13 @@ static int sched_mode(int flags) {
 }
 static bool prefer_umma(int64_t batch, int64_t rows, int64_t cols) {
   if (batch <= 2) return false;
-  // blocks each K5 CTA walks: how well the GEMM spreads this shape (scripts/dev/crossover.py,
-  // after the uniform-datapath MMA issue: 4096^2 b=3-4 K5 6.3 vs 6.8 us; 9216x3072 b=4 GEMV 7.1
-  // vs 8.3; 11008x4096 b=6 K3 10.1 vs 10.7, b=8 K5 10.7 vs 11.1)
+  // blocks each K5 CTA walks: how well the GEMM spreads this shape (scripts/dev/crossover.py, after
+  // K5's uniform-datapath MMA issue and split-K changes: 4096^2 b=3-4 K5 6.0-6.1 vs GEMV 6.7 us;
+  // 9216x3072 b=4 GEMV 7.6 vs 8.0; 11008x4096 b=4 GEMV 8.5 vs 9.5; from b=5 K5 wins every shape)
   const int bpc = umma_blocks_per_cta((int)batch, (int)rows, (int)cols);
   if (batch <= 4) return cols > 8192 || (cols > 4096 && bpc < 12) || bpc <= 4;
-  if (batch <= 6) return cols > 4096 || bpc < 12;
   return true;
 }
-
 }  // namespace tr
 
 using namespace tr;
