@@ -138,11 +138,6 @@ TR_API int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t bat
  * (parameters, not activations): they must not be written by the kernel just before. */
 #define TR_PRE_ADD_RMSNORM 1
 #define TR_PRE_SILU_MUL 2
-/* TR_PRE_RMSNORM_TILES (batch 1, cols % 16 == 0): x_eff = rmsnorm(x) * gamma, where x already is the
- * residual stream written by tr_linear_resid and `delta` points to its cols / 16 fp32 tile sums of
- * squares (summed here in one fixed order); x_out unused.  Same roundings as tr_add_rmsnorm on x with
- * delta = NULL, up to the fp32 summation order of the mean square. */
-#define TR_PRE_RMSNORM_TILES 3
 TR_API int tr_linear_pre(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,
                          int act_dtype, int64_t ldx, int64_t ldy, int flags, int pre_op, const void* delta,
                          const void* gamma, void* x_out, float eps, void* stream);
@@ -180,13 +175,6 @@ TR_API int tr_linear_chain_prepare(const TrChainLayer* layers, int64_t n_layers,
  * tr_linear_chain_prepare; graph-capturable.  (up to 256 products) */
 TR_API int tr_linear_chain(int act_dtype, const TrChainLayer* layers, int64_t n_layers, int64_t batch, int flags,
                            void* workspace, size_t ws_bytes, void* stream);
-
-/* Batch-1 residual update fused into a projection (decoder o / down):
- *   y = x W^T (rows), h_out = rnd(h_in + rnd(y)), ss_tiles[t] = sum over rows 16t..16t+15 of h_out^2 (fp32)
- * -- the next TR_PRE_RMSNORM_TILES GEMV reads h_out and ss_tiles instead of reducing x itself.
- * TQ2, int8-slice GEMV; flags: TR_LINEAR_PDL / COSCHEDULE / FULL_SM and the CTA-count knob. */
-TR_API int tr_linear_resid(int fmt, const void* w, const void* x, void* y, int64_t rows, int64_t cols, int act_dtype,
-                           int flags, const void* h_in, void* h_out, float* ss_tiles, void* stream);
 
 /* ---- decoder-layer glue (configs[2] decode stack; no reference analogue) ---------- */
 

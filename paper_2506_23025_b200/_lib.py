@@ -30,7 +30,6 @@ LINEAR_OUT_F32 = 128
 LINEAR_FULL_SM = 1 << 28
 PRE_ADD_RMSNORM = 1
 PRE_SILU_MUL = 2
-PRE_RMSNORM_TILES = 3
 
 _lock = threading.Lock()
 _lib = None
@@ -80,7 +79,6 @@ _SIGS = {
     "tr_silu_mul": ([_int, _c_p, _c_p, _i64, _i64, _c_p], _int),
     "tr_attn_decode_workspace_size": ([_i64, _i64, _i64], ctypes.c_size_t),
     "tr_qkv_attn_decode_workspace_size": ([_i64], ctypes.c_size_t),
-    "tr_linear_resid": ([_int, _c_p, _c_p, _c_p, _i64, _i64, _int, _int, _c_p, _c_p, _c_p, _c_p], _int),
     "tr_qkv_attn_decode": ([_int, _c_p, _c_p, _c_p, _c_p, _c_p, ctypes.c_float, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                             _c_p, _i64, _i64, _i64, ctypes.c_float, _c_p, ctypes.c_size_t, _int, _c_p], _int),
     "tr_attn_decode_split": ([_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _i64, _i64, _i64, ctypes.c_float, _c_p,

@@ -34,8 +34,7 @@ size_t gemv_workspace_bytes(int batch, int rows, int cols);
 bool gemv_s8_fits(int batch, int rows, int cols, int fmt);
 int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows, int cols,
             int ctas, int pdl, cudaStream_t st, int pre, const void* pre_delta, const void* pre_gamma, void* pre_out,
-            float eps, int cosched, int epi, int out_f32, int fmt, const void* res_in = nullptr,
-            void* res_out = nullptr, float* res_ss = nullptr);
+            float eps, int cosched, int epi, int out_f32, int fmt);
 int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
               int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg,
               int out_f32);
@@ -153,14 +152,8 @@ int tr_linear_pre(int fmt, const void* w, const void* x, void* y, int64_t batch,
                   void* x_out, float eps, void* stream) {
   TR_REQUIRE(fmt == kFmtTq2, "tr_linear_pre: TQ2 only");
   TR_REQUIRE(act_dtype == kActF16 || act_dtype == kActBf16, "tr_linear_pre: act_dtype must be F16(1) or BF16(2)");
-  TR_REQUIRE(pre_op == TR_PRE_ADD_RMSNORM || pre_op == TR_PRE_SILU_MUL || pre_op == TR_PRE_RMSNORM_TILES,
-             "tr_linear_pre: bad pre_op %d", pre_op);
-  TR_REQUIRE(pre_op == TR_PRE_SILU_MUL || gamma != nullptr, "tr_linear_pre: RMSNorm needs gamma");
-  if (pre_op == TR_PRE_RMSNORM_TILES) {   // int8-slice GEMV only
-    TR_REQUIRE(batch == 1 && cols % 16 == 0 && delta != nullptr && !(flags & TR_LINEAR_GEMV_F16) &&
-                   gemv_s8_fits(1, (int)rows, (int)cols, kFmtTq2),
-               "tr_linear_pre: TR_PRE_RMSNORM_TILES is batch 1, cols %% 16 == 0, on the int8-slice GEMV");
-  }
+  TR_REQUIRE(pre_op == TR_PRE_ADD_RMSNORM || pre_op == TR_PRE_SILU_MUL, "tr_linear_pre: bad pre_op %d", pre_op);
+  TR_REQUIRE(pre_op != TR_PRE_ADD_RMSNORM || gamma != nullptr, "tr_linear_pre: RMSNorm needs gamma");
   TR_REQUIRE(batch >= 1 && batch <= 8 && rows >= 1 && cols >= 1, "tr_linear_pre: 1 <= batch <= 8");
   TR_REQUIRE(ldx >= (pre_op == TR_PRE_SILU_MUL ? 2 * cols : cols) &&
                  ldy >= ((flags & TR_LINEAR_EPI_SWIGLU) ? rows / 2 : rows),
@@ -176,22 +169,6 @@ int tr_linear_pre(int fmt, const void* w, const void* x, void* y, int64_t batch,
                    sched_mode(flags), (flags & TR_LINEAR_EPI_SWIGLU) ? 1 : 0, 0, kFmtTq2);
   return gemv_tq2(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, (flags >> 8) & 0xFFFF,
                   flags & TR_LINEAR_PDL, (cudaStream_t)stream, pre_op, delta, gamma, x_out, eps, 0);
-}
-
-int tr_linear_resid(int fmt, const void* w, const void* x, void* y, int64_t rows, int64_t cols, int act_dtype,
-                    int flags, const void* h_in, void* h_out, float* ss_tiles, void* stream) {
-  TR_REQUIRE(fmt == kFmtTq2, "tr_linear_resid: TQ2 only");
-  TR_REQUIRE(act_dtype == kActF16 || act_dtype == kActBf16, "tr_linear_resid: act_dtype must be F16(1) or BF16(2)");
-  TR_REQUIRE(rows >= 1 && cols >= 1 && rows < (1LL << 30) && cols < (1LL << 30), "tr_linear_resid: bad shape");
-  TR_REQUIRE(((uintptr_t)w & 15) == 0, "tr_linear_resid: weight buffer must be 16-byte aligned");
-  TR_REQUIRE(h_in != nullptr && h_out != nullptr && ss_tiles != nullptr && h_in != h_out,
-             "tr_linear_resid: h_in, a distinct h_out and the tile sums are required");
-  TR_REQUIRE(!(flags & (TR_LINEAR_OUT_F32 | TR_LINEAR_EPI_SWIGLU | TR_LINEAR_FORCE_UMMA | TR_LINEAR_GEMV_F16)) &&
-                 gemv_s8_fits(1, (int)rows, (int)cols, kFmtTq2),
-             "tr_linear_resid: batch 1 on the int8-slice GEMV, plain output");
-  return gemv_s8(act_dtype, w, x, y, cols, rows, 1, (int)rows, (int)cols, (flags >> 8) & 0xFFFF,
-                 flags & TR_LINEAR_PDL, (cudaStream_t)stream, 0, nullptr, nullptr, nullptr, 0.0f, sched_mode(flags), 0,
-                 0, kFmtTq2, h_in, h_out, ss_tiles);
 }
 
 size_t tr_qkv_attn_decode_workspace_size(int64_t heads) { return heads > 0 ? (size_t)heads * 4 : 0; }

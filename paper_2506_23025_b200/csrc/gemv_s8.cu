@@ -62,18 +62,11 @@ struct S8Args {
   float att_scale;
   unsigned* att_cnt;   // per-head arrival counters (zero between launches)
   int att_m;           // CTAs per q / k / v section of a head (1, 2, 4 or 8)
-  // RES = 1 (tr_linear_resid, batch 1): the product is a residual update -- besides y, store
-  // res_out = rnd(res_in + rnd(y)) and, per 16-row tile, the fp32 sum of its squares in res_ss
-  // (the next layer's RMSNorm statistics: PRE = 3 reads them instead of reducing x itself)
-  const void* res_in;
-  void* res_out;
-  float* res_ss;
 };
 
-template <typename T, int NW, int PRE, int NG, int FMT = kFmtTq2, int ATT = 0, int RES = 0>
+template <typename T, int NW, int PRE, int NG, int FMT = kFmtTq2, int ATT = 0>
 __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Args a) {
   static_assert(FMT == kFmtTq2 || PRE == 0, "fused producers are TQ2-only");
-  static_assert(!RES || (NG == 1 && PRE == 0 && ATT == 0), "the residual epilogue is batch 1, plain x");
   using Cfg = S8Cfg<NW, NG, FMT>;
   constexpr int kSlotBytes = Cfg::kSlotBytes;
   constexpr int UB = S8Fmt<FMT>::kUnit;       // bytes per 16 x 256 unit
@@ -178,7 +171,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
   // tr_linear_pre's contract), so this warp's first two gamma blocks load before the wait --
   // per layer they are the one HBM miss among the producer's inputs
   uint4 pgv[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-  if constexpr (PRE == 1 || PRE == 3) {
+  if constexpr (PRE == 1) {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int item = warp + i * NW;
@@ -292,37 +285,6 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
     }
   } else {   // plain x, or silu(gate) * up of a gate|up product; loads for 4 items in flight
     const int n_items = nb * nrx;
-    // PRE = 3: x is the residual stream itself and its sum of squares arrives as per-16-row-tile
-    // partials from the producing GEMV's RES epilogue (cols / 16 floats in pre_delta), summed in
-    // one fixed order by every warp: x = rnd(rnd(x * iv) * gamma) needs no pass over x first
-    float iv3 = 0.0f;
-    auto rms_from_tiles = [&]() {   // (after the first activation loads are in flight: one round trip)
-      const float* ssl = reinterpret_cast<const float*>(a.pre_delta);
-      const int ntl = a.cols / 16;
-      float ss = 0.0f;
-      for (int q0 = 0; q0 < ntl; q0 += 32 * 16) {   // 16 loads in flight per lane, then their sum
-        float vals[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int q = q0 + lane + 32 * k;
-          vals[k] = q < ntl ? __ldcg(ssl + q) : 0.0f;
-        }
-#pragma unroll
-        for (int k = 0; k < 16; ++k) ss += vals[k];
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      iv3 = rsqrtf(ss / a.cols + a.eps);
-    };
-    auto res_rows = [&]() {   // RES: this CTA's h_in rows -> shared memory (after the first activation loads)
-      const T* hin = reinterpret_cast<const T*>(a.res_in);
-      float* hv = reinterpret_cast<float*>(smem + Cfg::smem(nb, nrx, NS));
-      for (int r = threadIdx.x; r < (int)(t1 - t0) * 16; r += NW * 32) {
-        const int row = (int)t0 * 16 + r;
-        hv[r] = row < a.rows ? Act<T>::to_float(hin[row]) : 0.0f;
-      }
-    };
-    if (RES && warp >= n_items) res_rows();   // (warps without an item: at once)
     for (int i0 = warp; i0 < n_items; i0 += 4 * NW) {
       uint4 va[4], vb[4];
 #pragma unroll
@@ -334,17 +296,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
           const bool live = br < nbr;   // (layout rows past the batch stage zeros)
           va[i] = live ? s8_load8(xg + br * a.ldx, kx, a.cols, a.x_vec) : make_uint4(0, 0, 0, 0);
           if (PRE == 2) vb[i] = live ? s8_load8(xg + br * a.ldx + a.cols, kx, a.cols, a.x_vec) : make_uint4(0, 0, 0, 0);
-          if (PRE == 3)
-            vb[i] = (i0 == warp && i < 2) ? pgv[i] : s8_load8(reinterpret_cast<const T*>(a.pre_gamma), kx, a.cols, a.x_vec);
         }
-      }
-      if constexpr (PRE == 3) {   // (before the rest of the weight ring: its copies would queue ahead)
-        if (i0 == warp) {
-          if (a.dbg & 8) iv3 = 0.01f; else rms_from_tiles();   // (dev probe 8: no statistics load)
-        }
-      }
-      if constexpr (RES) {
-        if (i0 == warp) res_rows();
       }
       issue_rest();
 #pragma unroll 1
@@ -371,12 +323,6 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
             for (int e = 0; e < 8; ++e)
               f[t][e] = s8_rnd<T>(s8_rnd<T>(__fdividef(f[t][e], 1.0f + __expf(-f[t][e]))) * up[e]);   // (0 past cols)
           }
-          if (PRE == 3) {
-            float gm[8];
-            s8_f8<T>(vb[t], gm);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) f[t][e] = s8_rnd<T>(s8_rnd<T>(f[t][e] * iv3) * gm[e]);
-          }
         }
         if constexpr (FMT == kFmtTq1) {
 #pragma unroll
@@ -389,7 +335,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
         }
         va[0] = va[2];
         va[1] = va[3];
-        if (PRE == 2 || PRE == 3) {
+        if (PRE == 2) {
           vb[0] = vb[2];
           vb[1] = vb[3];
         }
@@ -451,27 +397,6 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
         if (r0 < a.rows) store_y<T>(a.y, (int64_t)row * a.ldy + r0, v[G2][0], a.out_f32);
         if (r1 < a.rows) store_y<T>(a.y, (int64_t)row * a.ldy + r1, v[G2][1], a.out_f32);
       }
-    }
-    if constexpr (RES) {   // residual update of this tile's 16 rows and their sum of squares
-      float hsq = 0.0f;
-      if (c == 0) {   // (h_in rows staged in shared memory at the start)
-        const float* hv = tv + (tile - (int)t0) * 16;
-        T* hout = reinterpret_cast<T*>(a.res_out);
-        const int r0 = tile * 16 + g, r1 = r0 + 8;
-        if (r0 < a.rows) {
-          const float h0 = s8_rnd<T>(hv[g] + s8_rnd<T>(v[0][0]));
-          hout[r0] = Act<T>::from_float(h0);
-          hsq = h0 * h0;
-        }
-        if (r1 < a.rows) {
-          const float h1 = s8_rnd<T>(hv[g + 8] + s8_rnd<T>(v[0][1]));
-          hout[r1] = Act<T>::from_float(h1);
-          hsq += h1 * h1;
-        }
-      }
-#pragma unroll
-      for (int o = 4; o < 32; o <<= 1) hsq += __shfl_xor_sync(0xffffffffu, hsq, o);
-      if (lane == 0) a.res_ss[tile] = hsq;
     }
   };
   const int first_tile = wu0 < wu1 ? wu0 / nb : -1;
@@ -792,14 +717,13 @@ bool gemv_s8_fits(int batch, int rows, int cols, int fmt) {
   return batch <= 2 ? s8_fits_ng<1, kFmtTq2>(batch, nb, n_tiles, grid) : s8_fits_ng<2, kFmtTq2>(batch, nb, n_tiles, grid);
 }
 
-static size_t s8_tv_bytes(const S8Args& a, int grid) {   // SwiGLU epilogue: tile results of one CTA;
-  if (a.res_out) return (size_t)ceil_div(a.n_tiles, grid) * 16 * sizeof(float);   // RES: the CTA's h_in rows
+static size_t s8_tv_bytes(const S8Args& a, int grid) {   // SwiGLU epilogue: tile results of one CTA
   return a.epi ? (size_t)2 * ceil_div(a.n_tiles / 2, grid) * 64 * sizeof(float) : 0;
 }
 
-template <typename T, int NW, int PRE, int NG, int FMT = kFmtTq2, int RES = 0>
+template <typename T, int NW, int PRE, int NG, int FMT = kFmtTq2>
 static int launch_s8_k(S8Args& a, int grid, int pdl, cudaStream_t st) {
-  auto kern = k_gemv_s8<T, NW, PRE, NG, FMT, 0, RES>;
+  auto kern = k_gemv_s8<T, NW, PRE, NG, FMT>;
   static int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -836,10 +760,6 @@ static int launch_s8_ng(S8Args& a, int grid, int pdl, cudaStream_t st) {   // on
   if (a.fmt == kFmtTq1) return launch_s8_k<T, NW, 0, NG, kFmtTq1>(a, grid, pdl, st);
   if (a.pre == 1) return launch_s8_k<T, NW, 1, NG>(a, grid, pdl, st);
   if (a.pre == 2) return launch_s8_k<T, NW, 2, NG>(a, grid, pdl, st);
-  if constexpr (NG == 1) {   // (batch 1 only: the residual-stream forms)
-    if (a.pre == 3) return launch_s8_k<T, NW, 3, 1>(a, grid, pdl, st);
-    if (a.res_out) return launch_s8_k<T, NW, 0, 1, kFmtTq2, 1>(a, grid, pdl, st);
-  }
   return launch_s8_k<T, NW, 0, NG>(a, grid, pdl, st);
 }
 template <typename T, int NW>
@@ -935,16 +855,7 @@ int gemv_qkv_attn(int act, const void* w, const void* h, const void* delta, cons
 
 int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows, int cols,
             int ctas, int pdl, cudaStream_t st, int pre, const void* pre_delta, const void* pre_gamma, void* pre_out,
-            float eps, int cosched, int epi, int out_f32, int fmt, const void* res_in, void* res_out,
-            float* res_ss) {
-  if (pre == 3 && (batch != 1 || cols % 16 != 0 || pre_delta == nullptr || pre_gamma == nullptr)) {
-    set_error("tr_linear_pre(rmsnorm from tile sums): batch 1, cols %% 16 == 0, tile sums and gamma");
-    return -1;
-  }
-  if (res_out && (batch != 1 || pre || epi || out_f32 || fmt != kFmtTq2 || !res_in || !res_ss)) {
-    set_error("tr_linear_resid: batch 1, TQ2, no producer / epilogue / fp32 output, h_in and tile sums");
-    return -1;
-  }
+            float eps, int cosched, int epi, int out_f32, int fmt) {
   if (!gemv_s8_fits(batch, rows, cols, fmt)) {
     set_error("tr_linear(gemv-s8): batch %d x %d columns does not fit the int8-slice GEMV", batch, cols);
     return -1;
@@ -975,9 +886,6 @@ int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t
   ctas &= 0xFFF;
   a.epi = epi;
   a.out_f32 = out_f32;
-  a.res_in = res_in;
-  a.res_out = res_out;
-  a.res_ss = res_ss;
   if (epi && (rows % 32) != 0) {
     set_error("tr_linear(swiglu epilogue): rows (%d) must be whole 16-row gate/up tile pairs", rows);
     return -1;

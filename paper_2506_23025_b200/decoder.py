@@ -29,7 +29,7 @@ import torch.nn.functional as F
 
 from . import _lib
 from .blocks import DType
-from .device import _ACT, TernaryWeight, interleave_gate_up, linear, linear_pre, linear_resid
+from .device import _ACT, TernaryWeight, interleave_gate_up, linear, linear_pre
 
 
 @dataclass(frozen=True)
@@ -128,11 +128,6 @@ class TernaryDecoder:
         # slower inside the decode chain (its 16-warp CTAs keep the following o
         # projection from launching early); use_fused_attention(True) switches it on
         self.fused_attn = False
-        # decode: the o and down projections update the residual stream themselves and hand the next
-        # RMSNorm its per-tile sums of squares (tr_linear_resid -> TR_PRE_RMSNORM_TILES), so the qkv and
-        # gate|up GEMVs stage a plain activation instead of reducing it across the CTA first
-        self.resid_fused = self.gate_up_il is not None and d % 16 == 0
-        self._ss = [torch.empty(d // 16, device=self.device, dtype=torch.float32) for _ in range(2)]
         self._fused_attn_ok = (not dense and fused and D == 128 and S <= 128
                                and all(lw["qkv"].fmt is DType.TQ2 for lw in weights["layers"]))
         self._qkv_attn_ws = torch.zeros(_lib.lib().tr_qkv_attn_decode_workspace_size(H), dtype=torch.uint8,
@@ -252,9 +247,6 @@ class TernaryDecoder:
             # residual stream ping-pongs: the GEMV reads hs[cur] and stores hs[cur] + delta to hs[1 - cur]
             cs, fs = self.cosched, self.full_sm
             att = torch.empty((1, d), device=self.device, dtype=self.dtype)
-            if self.resid_fused and not self.fused_attn:
-                cur, delta = self._decoder_layer_resid(i, hs, cur, delta, pos, att)
-                continue
             if self.fused_attn:   # add + RMSNorm -> QKV GEMV -> rotary, cache append, attention: one kernel
                 qkv = torch.empty((1, 3 * d), device=self.device, dtype=self.dtype)
                 w = lw["qkv"]
@@ -280,36 +272,9 @@ class TernaryDecoder:
                 cur = 1 - cur
                 delta = linear_pre(gu, lw["down"], _lib.PRE_SILU_MUL, pdl=True, cosched=cs[3])
         xn = torch.empty((1, d), device=self.device, dtype=self.dtype)
-        _lib.call("tr_add_rmsnorm", act, hs[cur].data_ptr(), 0 if delta is None else delta.data_ptr(),
-                  self.norm_out.data_ptr(), xn.data_ptr(), 1, d, cfg.eps, st)
+        _lib.call("tr_add_rmsnorm", act, hs[cur].data_ptr(), delta.data_ptr(), self.norm_out.data_ptr(), xn.data_ptr(),
+                  1, d, cfg.eps, st)
         return F.linear(xn, self.weights["lm_head"])[0]
-
-    def _decoder_layer_resid(self, i, hs, cur, delta, pos, att):
-        """One decode layer on the residual-update path; returns (cur, None): hs[cur] holds the new
-        residual stream and self._ss[1] its tile sums of squares (no delta left to add)."""
-        cfg, act, st, lw = self.cfg, _ACT[self.dtype], _lib.stream_handle(), self.lin[i]
-        H, D, S = cfg.n_heads, cfg.head_dim, cfg.max_seq
-        cs, fs = self.cosched, self.full_sm
-        if i == 0 or delta is not None:   # no tile sums yet (embedding row): the add + RMSNorm producer
-            qkv = linear_pre(hs[cur], lw["qkv"], _lib.PRE_ADD_RMSNORM, delta, self.norm_attn[i], hs[1 - cur],
-                             cfg.eps, pdl=True, cosched=cs[0], full_sm=fs[0])
-            cur = 1 - cur
-        else:
-            qkv = linear_pre(hs[cur], lw["qkv"], _lib.PRE_RMSNORM_TILES, self._ss[1], self.norm_attn[i], None,
-                             cfg.eps, pdl=True, cosched=cs[0], full_sm=fs[0])
-        if S <= 128:
-            _lib.call("tr_attn_decode", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(), self.sin.data_ptr(),
-                      self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(), H, D, S, D ** -0.5, st)
-        else:
-            _lib.call("tr_attn_decode_split", act, qkv.data_ptr(), pos.data_ptr(), self.cos.data_ptr(),
-                      self.sin.data_ptr(), self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(),
-                      H, D, S, D ** -0.5, self._attn_ws.data_ptr(), self._attn_ws.numel(), st)
-        linear_resid(att, lw["o"], hs[cur], hs[1 - cur], self._ss[0], pdl=True, cosched=cs[1], full_sm=fs[1])
-        cur = 1 - cur
-        act_ = linear_pre(hs[cur], self.gate_up_il[i], _lib.PRE_RMSNORM_TILES, self._ss[0], self.norm_mlp[i], None,
-                          cfg.eps, pdl=True, cosched=cs[2], epi_swiglu=True, full_sm=fs[2])
-        linear_resid(act_, lw["down"], hs[cur], hs[1 - cur], self._ss[1], pdl=True, cosched=cs[3], full_sm=fs[3])
-        return 1 - cur, None
 
     def _qkv_attn_unfused(self, i, hs, cur, delta, pos, att):
         """QKV GEMV with the add + RMSNorm producer, then the attention kernel; returns o."""

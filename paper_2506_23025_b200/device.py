@@ -221,22 +221,6 @@ def linear_pre(x: torch.Tensor, w: TernaryWeight, pre: int, delta: torch.Tensor 
     return out
 
 
-def linear_resid(x: torch.Tensor, w: TernaryWeight, h_in: torch.Tensor, h_out: torch.Tensor,
-                 ss_tiles: torch.Tensor, out: torch.Tensor | None = None, pdl: bool = False, cosched: bool = False,
-                 full_sm: bool = False) -> torch.Tensor:
-    """Batch-1 projection fused with the residual update (tr_linear_resid): y = x @ W^T,
-    h_out = h_in + y (rounded like tr_add_rmsnorm), and ss_tiles[t] (fp32, rows // 16) = the sum of
-    h_out^2 over rows 16t..16t+15 -- which a following ``linear_pre(..., PRE_RMSNORM_TILES, ss_tiles,
-    gamma)`` uses for its RMSNorm instead of reducing h_out again."""
-    if out is None:
-        out = torch.empty((1, w.rows), dtype=x.dtype, device=x.device)
-    flags = (_lib.LINEAR_PDL if pdl else 0) | (_lib.LINEAR_COSCHEDULE if cosched else 0) | (
-        _lib.LINEAR_FULL_SM if full_sm else 0)
-    _lib.call("tr_linear_resid", int(w.fmt), w.data.data_ptr(), x.data_ptr(), out.data_ptr(), w.rows, w.cols,
-              _ACT[x.dtype], flags, h_in.data_ptr(), h_out.data_ptr(), ss_tiles.data_ptr(), _lib.stream_handle())
-    return out
-
-
 class TernaryLinear(torch.nn.Module):
     """nn.Linear-shaped module over a TernaryWeight (no bias, like the paper's BitLinear layers)."""
 

@@ -1081,66 +1081,3 @@ def test_full_sm_gemv_vs_oracle(tp, rows, cols):
     scale = ref.abs().max()
     assert ((y_full.cpu() - ref).abs().max() / scale).item() <= 2e-3
     assert ((y_full - y_def).abs().max().cpu() / scale).item() <= 2e-3
-
-
-@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
-def test_linear_resid_and_rmsnorm_tiles(tp, dtype):
-    """tr_linear_resid (y, h_out = h_in + y, per-16-row tile sums of h_out^2) and the
-    TR_PRE_RMSNORM_TILES GEMV that consumes them, against the unfused tr_linear + tr_add_rmsnorm +
-    tr_linear chain: y and h_out bitwise, the tile sums against fp32 torch, the second product
-    within the GEMV tolerance (only the mean square's summation order differs)."""
-    from paper_2506_23025_b200 import _lib
-    from paper_2506_23025_b200.device import _ACT, linear_pre, linear_resid
-
-    tdt = getattr(torch, dtype)
-    g = torch.Generator(device="cuda").manual_seed(11)
-    d, f = 3072, 1024
-    w1 = tp.TernaryWeight.from_float(0.02 * torch.randint(-1, 2, (d, f), device="cuda", generator=g).float())
-    w2 = tp.TernaryWeight.from_float(0.02 * torch.randint(-1, 2, (4096, d), device="cuda", generator=g).float())
-    x = torch.randn((1, f), device="cuda", generator=g).to(tdt)
-    h = torch.randn((1, d), device="cuda", generator=g).to(tdt)
-    gamma = (1 + 0.1 * torch.randn(d, device="cuda", generator=g)).to(tdt)
-    h_out = torch.empty_like(h)
-    ss = torch.empty(d // 16, device="cuda", dtype=torch.float32)
-    y = linear_resid(x, w1, h, h_out, ss)
-    y_ref = tp.linear(x, w1, path="gemv")
-    assert torch.equal(y, y_ref)
-    h_ref = (h.float() + y_ref.float()).to(tdt)
-    assert torch.equal(h_out, h_ref)
-    ss_ref = (h_ref.float() ** 2).view(-1, 16).sum(1)
-    assert torch.allclose(ss, ss_ref, rtol=1e-5, atol=0)
-    z = linear_pre(h_out, w2, _lib.PRE_RMSNORM_TILES, ss, gamma, None, 1e-5)
-    xn = torch.empty_like(h)
-    _lib.call("tr_add_rmsnorm", _ACT[tdt], h_out.data_ptr(), 0, gamma.data_ptr(), xn.data_ptr(), 1, d, 1e-5,
-              _lib.stream_handle())
-    z_ref = tp.linear(xn, w2, path="gemv").float()
-    tol = 2e-2 if dtype == "bfloat16" else 4e-3
-    assert ((z.float() - z_ref).abs().max() / z_ref.abs().max()).item() <= tol
-    with pytest.raises(_lib.TriRunError):   # batch 2 is not a residual-stream form
-        linear_pre(torch.cat([h_out, h_out]), w2, _lib.PRE_RMSNORM_TILES, ss, gamma, None, 1e-5)
-
-
-def test_decoder_resid_path_matches_old_path(tp):
-    """The decoder's residual-update decode step (tr_linear_resid + TR_PRE_RMSNORM_TILES) against the
-    add + RMSNorm producer step on shared weights: logits through prefill + decode, and greedy tokens
-    through the decode graphs."""
-    from paper_2506_23025_b200.decoder import DecoderConfig, TernaryDecoder
-
-    cfg = DecoderConfig(d_model=768, n_layers=3, n_heads=6, d_ff=2048, vocab=1000, max_seq=128)
-    a = TernaryDecoder(cfg, seed=9)
-    b = TernaryDecoder(cfg, weights=a.weights)
-    assert a.resid_fused
-    b.resid_fused = False
-    prompt = torch.randint(0, cfg.vocab, (7,), device="cuda")
-    la, lb = a.forward(prompt, torch.arange(7, device="cuda")), b.forward(prompt, torch.arange(7, device="cuda"))
-    for p in range(7, 15):
-        t1 = torch.argmax(lb).view(1)
-        p1 = torch.tensor([p], device="cuda")
-        la, lb = a.forward(t1, p1).float(), b.forward(t1, p1).float()
-        assert ((la - lb).abs().max() / lb.abs().max()).item() <= 5e-3, p
-    for m in (a, b):
-        m.reset()
-        m.prefill(prompt)
-        m.decode(9)
-    torch.cuda.synchronize()
-    assert torch.equal(a.out_tokens[7:16], b.out_tokens[7:16])
