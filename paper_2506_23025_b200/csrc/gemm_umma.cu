@@ -551,13 +551,22 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
             float v[EC];
 #pragma unroll
             for (int e = 0; e < EC; ++e) v[e] = 0.0f;
-            for (int q = 0; q < a.ks; ++q) {
-              float u[EC];   // (this CTA's own slice too: taking it from registers measured slower)
-              const float* src = base + (int64_t)q * kRowsPerCta * N + (half_k * NH + e0) * kRowsPerCta + r;
+            // QB slices' loads in flight before any of them is added (in program order the adds
+            // of one slice would hold back the next slice's loads: one L2 round trip per slice)
+            constexpr int QB = 64 / EC;
+            for (int q0 = 0; q0 < a.ks; q0 += QB) {
+              float u[QB][EC];   // (this CTA's own slice too: taking it from registers measured slower)
 #pragma unroll
-              for (int e = 0; e < EC; ++e) u[e] = __ldcg(src + e * kRowsPerCta);
+              for (int qq = 0; qq < QB; ++qq) {
+                const float* src =
+                    base + (int64_t)(q0 + qq) * kRowsPerCta * N + (half_k * NH + e0) * kRowsPerCta + r;
 #pragma unroll
-              for (int e = 0; e < EC; ++e) v[e] += u[e];
+                for (int e = 0; e < EC; ++e) u[qq][e] = q0 + qq < a.ks ? __ldcg(src + e * kRowsPerCta) : 0.0f;
+              }
+#pragma unroll
+              for (int qq = 0; qq < QB; ++qq)   // slice order (the zeros past ks leave the sum unchanged)
+#pragma unroll
+                for (int e = 0; e < EC; ++e) v[e] += u[qq][e];
             }
 #pragma unroll
             for (int e = 0; e < EC; ++e)
