@@ -171,8 +171,24 @@ __global__ void __launch_bounds__(128) k_attn_decode(const T* __restrict__ qkv, 
   int p_spec = (int)*reinterpret_cast<const volatile int64_t*>(pos);
   p_spec = p_spec < 0 ? 0 : (p_spec > S - 1 ? S - 1 : p_spec);
   load_cache(0, p_spec);
+  // the rotary angles of the speculative position are parameters too: load them under the wait
+  T cs_spec = Act<T>::from_float(0.0f), sn_spec = cs_spec;
+  if (tid < D / 2) {
+    cs_spec = cs[(int64_t)p_spec * (D / 2) + tid];
+    sn_spec = sn[(int64_t)p_spec * (D / 2) + tid];
+  }
   griddep_wait();
   griddep_launch_dependents();
+  // this token's q / k / v and pos in one round trip (the q / k / v loads do not wait for pos)
+  T qa = cs_spec, qb = cs_spec, ka = cs_spec, kb2 = cs_spec, v1 = cs_spec, v2 = cs_spec;
+  if (tid < D / 2) {
+    qa = qkv[hh * D + 2 * tid];
+    qb = qkv[hh * D + 2 * tid + 1];
+    ka = qkv[(H + hh) * D + 2 * tid];
+    kb2 = qkv[(H + hh) * D + 2 * tid + 1];
+    v1 = qkv[(2 * H + hh) * D + 2 * tid];
+    v2 = qkv[(2 * H + hh) * D + 2 * tid + 1];
+  }
   const int64_t p64 = pos[0];
   if (p64 < 0 || p64 >= S) {   // past the cache: no cache or shared-memory row p exists; output zeros
     asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -183,10 +199,10 @@ __global__ void __launch_bounds__(128) k_attn_decode(const T* __restrict__ qkv, 
   if (p > p_spec) load_cache(p_spec, p);
   // rotary embedding of this token's q and k; k and v into the caches (and shared memory)
   if (tid < D / 2) {
-    const float c = to_f(cs[(int64_t)p * (D / 2) + tid]), s = to_f(sn[(int64_t)p * (D / 2) + tid]);
-    const float q1 = to_f(qkv[hh * D + 2 * tid]), q2 = to_f(qkv[hh * D + 2 * tid + 1]);
-    const float k1 = to_f(qkv[(H + hh) * D + 2 * tid]), k2 = to_f(qkv[(H + hh) * D + 2 * tid + 1]);
-    const T v1 = qkv[(2 * H + hh) * D + 2 * tid], v2 = qkv[(2 * H + hh) * D + 2 * tid + 1];
+    const float c = to_f(p == p_spec ? cs_spec : cs[(int64_t)p * (D / 2) + tid]);
+    const float s = to_f(p == p_spec ? sn_spec : sn[(int64_t)p * (D / 2) + tid]);
+    const float q1 = to_f(qa), q2 = to_f(qb);
+    const float k1 = to_f(ka), k2 = to_f(kb2);
     qs[2 * tid] = to_f(Act<T>::from_float(q1 * c - q2 * s));
     qs[2 * tid + 1] = to_f(Act<T>::from_float(q1 * s + q2 * c));
     const T r1 = Act<T>::from_float(k1 * c - k2 * s), r2 = Act<T>::from_float(k1 * s + k2 * c);
