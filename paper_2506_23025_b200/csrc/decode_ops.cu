@@ -415,16 +415,27 @@ __global__ void __launch_bounds__(1024) k_greedy_next(const T* __restrict__ logi
   float best = -INFINITY;
   int idx = 0x7fffffff;
   const bool vec = (vocab % 8) == 0 && ((uintptr_t)logits % 16) == 0;
-  if (vec) {
-    for (int i = tid * 8; i < vocab; i += 1024 * 8) {
-      float f[8];
-      unpack8<T>(*reinterpret_cast<const uint4*>(logits + i), f);
+  if (vec) {   // four 16-byte loads in flight before their compares (one L2 round trip, not four)
+    for (int i0 = tid * 8; i0 < vocab; i0 += 4 * 1024 * 8) {
+      uint4 u[4];
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (f[e] > best) {   // ascending indices per thread: strict > keeps the lowest
-          best = f[e];
-          idx = i + e;
-        }
+      for (int k = 0; k < 4; ++k) {
+        const int i = i0 + k * 1024 * 8;
+        if (i < vocab) u[k] = *reinterpret_cast<const uint4*>(logits + i);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int i = i0 + k * 1024 * 8;
+        if (i >= vocab) break;
+        float f[8];
+        unpack8<T>(u[k], f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (f[e] > best) {   // ascending indices per thread: strict > keeps the lowest
+            best = f[e];
+            idx = i + e;
+          }
+      }
     }
   } else {
     for (int i = tid; i < vocab; i += 1024) {
