@@ -51,7 +51,8 @@ def parse():
     p.add_argument("--sweep", default="1,2,4,8,16,32,64,128")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--extras", default="bf16,decode,tq1,tp70b,boundary",
-                   help="extra sections on rank 0 at N=1: decode (configs[2]), tq1 (configs[3]), tp70b (configs[4]), "
+                   help="extra sections on rank 0 at N=1: decode (configs[2]), tq1 (configs[3]), tp70b (configs[4]; "
+                        "+ symm: the symmetric-memory one-shot all-reduce A/B), "
                         "boundary (the unmodified reference's linear.gemm on backend 'cuda', configs[0])")
     return p.parse_args()
 
@@ -440,14 +441,16 @@ def run_extras(args, stack_ws):
     return out
 
 
-def run_tp70b(rank, world, dist, batches=(1, 16), steps=50):
+def run_tp70b(rank, world, dist, batches=(1, 16), steps=50, with_symm=False):
     """configs[4] across the ranks of this job: the 70B MLP pair -- up (rows 28672 x cols 8192,
     column-parallel: rank i owns 256-aligned output rows) then down (rows 8192 x cols 28672,
     row-parallel: rank i owns the matching 256-blocks of K, fp32 partials) -- and the all-reduce of
     the fp32 partials, all inside the timed region (CUDA graph when capture works).  Reports the
     step (shards + all-reduce), the shards alone and the all-reduce alone, max over ranks (device
-    time).  All-reduce: NCCL, and the symmetric-memory one-shot kernel when this torch build and
-    the NVLink topology provide it (A/B)."""
+    time).  All-reduce: NCCL, and with ``--extras ...,symm`` the symmetric-memory one-shot kernel
+    when this torch build and the NVLink topology provide it (A/B; opt-in because it has only run
+    at one rank here -- a rendezvous that fails on one rank would stall the others and lose the
+    scaling run)."""
     import torch
     import paper_2506_23025_b200 as tp
     from paper_2506_23025_b200.parallel import shard_bounds
@@ -464,7 +467,7 @@ def run_tp70b(rank, world, dist, batches=(1, 16), steps=50):
     w_up, w_down = weight(r1 - r0, d), weight(d, r1 - r0)
     torch.cuda.empty_cache()
     symm = None
-    if dist is not None:
+    if dist is not None and with_symm:
         try:
             import torch.distributed._symmetric_memory as symm_mem
 
@@ -586,7 +589,7 @@ def run_ours(args, rank, world, dist):
     if "tp70b" in args.extras.split(","):   # every rank: the tensor-parallel MLP across this job's GPUs
         del ws
         torch.cuda.empty_cache()
-        tp70 = run_tp70b(rank, world, dist)
+        tp70 = run_tp70b(rank, world, dist, with_symm="symm" in args.extras.split(","))
         if rank == 0:
             extras["tp70b_mlp"] = tp70
 
