@@ -454,21 +454,23 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
       if (lane == 0) mbar_arrive(&d_empty[ab]);
     };
 
-    auto finish_block = [&](int i, float s_cur) {
+    auto finish_block = [&](int i, float s_cur, int ab) {
       tmem_wait_st();
       if (kTrace && (a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64 && (warp == 0 || warp == 1 || warp == 6))
         reinterpret_cast<long long*>(a.y)[i * 8 + (warp == 0 ? 4 : warp == 1 ? 6 : 7)] = clock64();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&a_full[i % NA]);
+      if (lane == 0) mbar_arrive(&a_full[ab]);
       if (i == 0) s_first = s_cur;
       if (per_block && i > 0) epilogue_block(i - 1, s_prev);
       s_prev = s_cur;
     };
     {   // per block: weights to registers, wait for the A buffer, decode 32 columns at a time into TMEM
+      // (ring positions and phases advance incrementally: the divisions by KS, RW and NA were a
+      // tenth of the decode warps' instructions at N = 16)
+      int j = 0, s = 0, wph = 0, ab = 0, aph = 1;
       for (int i = 0; i < nblk; ++i) {
-        const int si = i / KS, j = i - si * KS, s = si % RW, ab = i % NA;
-        if (j == 0) mbar_wait(&full_w[s], (si / RW) & 1);
+        if (j == 0) mbar_wait(&full_w[s], wph);
         const uint32_t unit = sW32 + s * kStageW + j * UB;
         uint4 wv[2];
         uint32_t wq[7];
@@ -486,7 +488,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty_w[s]);
         }
-        mbar_wait(&a_empty[ab], ((i / NA) & 1) ^ 1);
+        mbar_wait(&a_empty[ab], aph);
         if (kTrace && (a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0 && i < 64)
           reinterpret_cast<long long*>(a.y)[i * 8 + 3] = clock64();
         tc_fence_after();
@@ -514,7 +516,18 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
           }
           tmem_st32(tA + lane_off + ab * 128 + (2 * half_k + cc) * 32, col);
         }
-        finish_block(i, s_cur);
+        finish_block(i, s_cur, ab);
+        if (++j == KS) {
+          j = 0;
+          if (++s == RW) {
+            s = 0;
+            wph ^= 1;
+          }
+        }
+        if (++ab == NA) {
+          ab = 0;
+          aph ^= 1;
+        }
       }
     }
     if (nblk > 0) {
