@@ -393,12 +393,13 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
     // MMA descriptors are computed in uniform registers rather than moved there once per MMA
     const uint32_t sB32 = ((smem_u32(smem_raw) + 1023u) & ~1023u) + (uint32_t)Cfg::kBOff;
     {   // the whole warp runs the loop; each MMA / commit is issued by one elected lane
+      int s = 0, bph = 0, ab = 0, aph = 0;
       for (int i = 0; i < nblk; ++i) {
-        const int s = i % RB, ab = i % NA, db = i & 1;
-        mbar_wait(&full_b[s], (i / RB) & 1);         // activations landed
+        const int db = i & 1;
+        mbar_wait(&full_b[s], bph);                  // activations landed
         if (kTrace && (a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64)
           reinterpret_cast<long long*>(a.y)[i * 8 + 0] = clock64();
-        mbar_wait(&a_full[ab], (i / NA) & 1);        // trits decoded into TMEM
+        mbar_wait(&a_full[ab], aph);                 // trits decoded into TMEM
         if (kTrace && (a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64)
           reinterpret_cast<long long*>(a.y)[i * 8 + 1] = clock64();
         if (per_block) mbar_wait(&d_empty[db], ((i >> 1) & 1) ^ 1);
@@ -417,6 +418,14 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
         mma_commit(&empty_b[s]);                     // activation stage reusable once these MMAs finish
         mma_commit(&a_empty[ab]);                    // TMEM A buffer reusable
         if (per_block || i == nblk - 1) mma_commit(&d_full[per_block ? db : 0]);
+        if (++s == RB) {   // (ring positions and phases advance incrementally)
+          s = 0;
+          bph ^= 1;
+        }
+        if (++ab == NA) {
+          ab = 0;
+          aph ^= 1;
+        }
         if (kTrace && (a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64)
           reinterpret_cast<long long*>(a.y)[i * 8 + 5] = clock64();
       }
