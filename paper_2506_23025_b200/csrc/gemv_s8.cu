@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
                           a.x_vec);
     }
   }
-  griddep_launch_dependents();
+  if constexpr (!ATT) griddep_launch_dependents();   // (ATT: after the main loop, below)
   griddep_wait();   // x belongs to the previous kernel until here
   if (trace) wait_clk = clock64();
   stamp(1);
@@ -603,6 +603,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
 #ifndef S8_PRE_PROBE
   stamp(9);
 #endif
+  // the fused QKV + attention kernel lets the o projection launch only once its GEMV part is done:
+  // its 16-warp CTAs and the attention tail otherwise share the SMs with waiting o-projection CTAs
+  if constexpr (ATT) griddep_launch_dependents();
   if (cur >= 0) close_tile(cur);
 
   // ---- boundary tiles: combine the parked fragments in fixed (warp, slot) order and store
