@@ -244,11 +244,18 @@ struct UmmaCfg {
 #define UMMA_RB16 4
 #endif
   static constexpr int KS = N <= 32 ? UMMA_KS_SMALL : 2;     // 256-blocks per weight stage
-  // weight stages (N <= 32: two, re-measured after the MMA issue work -- b=16-32 1.5-2% faster than four)
-  static constexpr int RW = N <= 32 ? UMMA_RW_SMALL : (N == 128 && UMMA_N128_RB == 3) ? 2 : 3;
+  // weight stages: two (re-measured after the MMA issue work: N <= 32 b=16-32 1.5-2% faster than
+  // four; N = 64 4096^2 b=128 10.96 -> 10.58 us, 4096x11008 b=64 13.35 -> 13.12 against three)
+#ifndef UMMA_RW_MID
+#define UMMA_RW_MID 2
+#endif
+#ifndef UMMA_RB_MID
+#define UMMA_RB_MID 5
+#endif
+  static constexpr int RW = N <= 32 ? UMMA_RW_SMALL : (N == 128 && UMMA_N128_RB == 3) ? 2 : UMMA_RW_MID;
   // (N = 32, 64: the spare shared memory goes to activation stages as well: +0.5-1.2% at b = 32-64;
   // N = 16 measured no gain from 8)
-  static constexpr int RB = N <= 16 ? UMMA_RB16 : N <= 64 ? 5 : UMMA_N128_RB;   // activation stages (one block each)
+  static constexpr int RB = N <= 16 ? UMMA_RB16 : N <= 64 ? UMMA_RB_MID : UMMA_N128_RB;   // activation stages (one block each)
   static constexpr int kStageWBytes = 8 * KS * UB;          // 128 rows x KS blocks
   static constexpr int kStageBBytes = N * 512;               // N rows x 256 K (4 swizzled 64-K atoms)
   static constexpr int kMaxA = 3;                            // TMEM A buffers (128 columns = one block each)
