@@ -50,9 +50,10 @@ def parse():
     p.add_argument("--replicas", type=int, default=32)
     p.add_argument("--sweep", default="1,2,4,8,16,32,64,128")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
-    p.add_argument("--extras", default="bf16,decode,tq1,tp70b,boundary",
+    p.add_argument("--extras", default="bf16,decode,decode_batched,tq1,tp70b,boundary",
                    help="extra sections on rank 0 at N=1: decode (configs[2]), tq1 (configs[3]), tp70b (configs[4]; "
-                        "+ symm: the symmetric-memory one-shot all-reduce A/B), "
+                        "+ symm: the symmetric-memory one-shot all-reduce A/B), decode_batched (with decode: B = 1, 4, "
+                        "16 sequences per step), "
                         "boundary (the unmodified reference's linear.gemm on backend 'cuda', configs[0])")
     return p.parse_args()
 
@@ -436,6 +437,31 @@ def run_extras(args, stack_ws):
                               "decode_speedup_vs_fp16": round(d_dec / t_dec, 3),
                               "ternary_ttft_ms": round(t_ttft, 3), "fp16_cublas_ttft_ms": round(d_ttft, 3),
                               "ternary_bytes_per_token": cfg.ternary_bytes() + cfg.vocab * cfg.d_model * 2}
+        if "decode_batched" in want:   # B sequences per step (BatchedDecoder): tokens/s over all of them
+            from paper_2506_23025_b200.decoder import BatchedDecoder
+
+            res = []
+            for B in (1, 4, 16):
+                prompts = torch.randint(0, cfg.vocab, (B, 64), device="cuda",
+                                        generator=torch.Generator(device="cuda").manual_seed(2))
+                row = {"batch": B, "prompt": 64, "generated": 48}
+                for name, base in (("ternary", tern), ("fp16_cublas", dense)):
+                    bd = BatchedDecoder(base, B)
+                    bd.prefill(prompts)
+                    bd.decode(1)   # (capture + one step)
+                    best = None
+                    for _ in range(3):
+                        bd.prefill(prompts)
+                        bd.capture()
+                        torch.cuda.synchronize()
+                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        e0.record(); bd.decode(48); e1.record(); e1.synchronize()
+                        best = e0.elapsed_time(e1) if best is None else min(best, e0.elapsed_time(e1))
+                    row[f"{name}_tokens_per_s"] = round(B * 48 / best * 1e3, 1)
+                    del bd
+                row["speedup_vs_fp16"] = round(row["ternary_tokens_per_s"] / row["fp16_cublas_tokens_per_s"], 3)
+                res.append(row)
+            out["decode_batched_3p9b"] = res
         del tern, dense
         torch.cuda.empty_cache()
     return out

@@ -217,6 +217,15 @@ TR_API int tr_silu_mul(int act_dtype, const void* gu, void* out, int64_t tokens,
  * (if pos[0] < max_pos); tok[0] = idx; pos[0] += 1; h_next [d] = embed [vocab, d] row idx.  int64 on device. */
 TR_API int tr_greedy_next(int act_dtype, const void* logits, int64_t vocab, int64_t* out_tokens, int64_t max_pos,
                           int64_t* tok, int64_t* pos, const void* embed, int64_t d, void* h_next, void* stream);
+/* Batched decode (B independent sequences, one token each): the same kernels over a batch of
+ * sequences.  tr_attn_decode_batch: qkv [B, 3, H, D], pos [B], caches [B, H, S, D], out [B, H, D].
+ * tr_greedy_next_batch: logits [B, vocab], out_tokens [B, max_pos], tok [B], pos [B], h_next [B, d]. */
+TR_API int tr_attn_decode_batch(int act_dtype, const void* qkv, const int64_t* pos, const void* cos_t,
+                                const void* sin_t, void* k_cache, void* v_cache, void* out, int64_t batch,
+                                int64_t heads, int64_t head_dim, int64_t max_seq, float scale, void* stream);
+TR_API int tr_greedy_next_batch(int act_dtype, const void* logits, int64_t vocab, int64_t* out_tokens,
+                                int64_t max_pos, int64_t* tok, int64_t* pos, const void* embed, int64_t d,
+                                void* h_next, int64_t batch, void* stream);
 
 #ifdef __cplusplus
 }

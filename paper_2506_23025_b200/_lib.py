@@ -74,6 +74,9 @@ _SIGS = {
     "tr_add_rmsnorm": ([_int, _c_p, _c_p, _c_p, _c_p, _i64, _i64, ctypes.c_float, _c_p], _int),
     "tr_rope_kv": ([_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _i64, _i64, _i64, _i64, _c_p], _int),
     "tr_greedy_next": ([_int, _c_p, _i64, _c_p, _i64, _c_p, _c_p, _c_p, _i64, _c_p, _c_p], _int),
+    "tr_greedy_next_batch": ([_int, _c_p, _i64, _c_p, _i64, _c_p, _c_p, _c_p, _i64, _c_p, _i64, _c_p], _int),
+    "tr_attn_decode_batch": ([_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _i64, _i64, _i64, _i64, ctypes.c_float,
+                              _c_p], _int),
     "tr_attn_decode": ([_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _i64, _i64, _i64, ctypes.c_float, _c_p],
                        _int),
     "tr_silu_mul": ([_int, _c_p, _c_p, _i64, _i64, _c_p], _int),

@@ -141,6 +141,14 @@ __global__ void __launch_bounds__(128) k_attn_decode(const T* __restrict__ qkv, 
                                                      T* __restrict__ kc, T* __restrict__ vc, T* __restrict__ out,
                                                      int H, int S, float scale) {
   static_assert(D == 128, "one key per thread, 4 dims per lane");
+  {   // batched decode (tr_attn_decode_batch): sequence blockIdx.y -- its qkv row, position, caches, output
+    const int64_t bq = blockIdx.y;
+    qkv += bq * 3 * H * D;
+    pos += bq;
+    kc += bq * H * S * D;
+    vc += bq * H * S * D;
+    out += bq * H * D;
+  }
   __shared__ __align__(16) T vs[128][D];   // values of keys 0..pos
   __shared__ __align__(16) T kp[D];        // this token's rotated key
   __shared__ float qs[D];
@@ -406,6 +414,14 @@ __global__ void __launch_bounds__(1024) k_greedy_next(const T* __restrict__ logi
                                                       int64_t* __restrict__ out_tokens, int max_pos,
                                                       int64_t* __restrict__ tok, int64_t* __restrict__ pos,
                                                       const T* __restrict__ embed, int d, T* __restrict__ h_next) {
+  {   // batched decode (tr_greedy_next_batch): sequence blockIdx.x
+    const int64_t bq = blockIdx.x;
+    logits += bq * vocab;
+    out_tokens += bq * max_pos;
+    tok += bq;
+    pos += bq;
+    h_next += bq * d;
+  }
   griddep_wait();
   griddep_launch_dependents();
   __shared__ float bv[32];
@@ -641,6 +657,39 @@ int tr_silu_mul(int act, const void* gu, void* out, int64_t tokens, int64_t ff, 
   return check_launch("tr_silu_mul");
 }
 
+int tr_attn_decode_batch(int act, const void* qkv, const int64_t* pos, const void* cos_t, const void* sin_t,
+                         void* k_cache, void* v_cache, void* out, int64_t batch, int64_t heads, int64_t head_dim,
+                         int64_t max_seq, float scale, void* stream) {
+  TR_REQUIRE(head_dim == 128, "tr_attn_decode_batch: head_dim must be 128");
+  TR_REQUIRE(heads >= 1 && max_seq >= 1 && max_seq <= 128, "tr_attn_decode_batch: 1 <= max_seq <= 128");
+  TR_REQUIRE(batch >= 1 && batch <= 65535, "tr_attn_decode_batch: 1 <= batch <= 65535");
+  cudaStream_t st = (cudaStream_t)stream;
+  const dim3 grid((unsigned)heads, (unsigned)batch);
+  TR_ACT_DISPATCH(act,
+                  (launch_pdl(k_attn_decode<__half, 128>, grid, dim3(128), 0, st, (const __half*)qkv, pos,
+                              (const __half*)cos_t, (const __half*)sin_t, (__half*)k_cache, (__half*)v_cache,
+                              (__half*)out, (int)heads, (int)max_seq, scale)),
+                  (launch_pdl(k_attn_decode<__nv_bfloat16, 128>, grid, dim3(128), 0, st, (const __nv_bfloat16*)qkv,
+                              pos, (const __nv_bfloat16*)cos_t, (const __nv_bfloat16*)sin_t,
+                              (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, (__nv_bfloat16*)out, (int)heads,
+                              (int)max_seq, scale)));
+  return check_launch("tr_attn_decode_batch");
+}
+int tr_greedy_next_batch(int act, const void* logits, int64_t vocab, int64_t* out_tokens, int64_t max_pos,
+                         int64_t* tok, int64_t* pos, const void* embed, int64_t d, void* h_next, int64_t batch,
+                         void* stream) {
+  TR_REQUIRE(vocab >= 1 && vocab < (1LL << 31) && d >= 1 && max_pos >= 0, "tr_greedy_next_batch: bad sizes");
+  TR_REQUIRE(batch >= 1 && batch <= 65535, "tr_greedy_next_batch: 1 <= batch <= 65535");
+  cudaStream_t st = (cudaStream_t)stream;
+  TR_ACT_DISPATCH(act,
+                  (launch_pdl(k_greedy_next<__half>, dim3((unsigned)batch), dim3(1024), 0, st, (const __half*)logits,
+                              (int)vocab, out_tokens, (int)max_pos, tok, pos, (const __half*)embed, (int)d,
+                              (__half*)h_next)),
+                  (launch_pdl(k_greedy_next<__nv_bfloat16>, dim3((unsigned)batch), dim3(1024), 0, st,
+                              (const __nv_bfloat16*)logits, (int)vocab, out_tokens, (int)max_pos, tok, pos,
+                              (const __nv_bfloat16*)embed, (int)d, (__nv_bfloat16*)h_next)));
+  return check_launch("tr_greedy_next_batch");
+}
 int tr_greedy_next(int act, const void* logits, int64_t vocab, int64_t* out_tokens, int64_t max_pos, int64_t* tok,
                    int64_t* pos, const void* embed, int64_t d, void* h_next, void* stream) {
   TR_REQUIRE(vocab >= 1 && vocab < (1LL << 31) && d >= 1 && max_pos >= 0, "tr_greedy_next: bad sizes");

@@ -392,3 +392,148 @@ class TernaryDecoder:
         self.v_cache.zero_()
         self.tok.zero_()
         self.pos.zero_()
+
+
+class BatchedDecoder:
+    """B independent sequences decoded together, one token each per step, on a TernaryDecoder's
+    weights (or its dense fp16 twin's).  Every projection runs at batch B through ``tr_linear``'s
+    dispatch (the int8-slice GEMV up to batch 2-4, the tcgen05 GEMM beyond); attention and greedy
+    selection run one CTA per (sequence, head) / sequence (``tr_attn_decode_batch``,
+    ``tr_greedy_next_batch``).  Prompts of equal length; each sequence keeps its own KV cache rows
+    [L, B, H, S, D] and position.  decode(n) replays one captured CUDA graph per step."""
+
+    def __init__(self, base: TernaryDecoder, batch: int):
+        if not base.fused:
+            raise ValueError("BatchedDecoder runs on the fused (libtritrun glue) decoder")
+        cfg = base.cfg
+        self.base, self.B, self.cfg = base, int(batch), cfg
+        L, H, S, D, d = cfg.n_layers, cfg.n_heads, cfg.max_seq, cfg.head_dim, cfg.d_model
+        if D != 128 or S > 128:
+            raise ValueError("batched decode attention: head_dim 128, max_seq <= 128")
+        dev, dt = base.device, base.dtype
+        self.k_cache = torch.zeros((L, self.B, H, S, D), device=dev, dtype=dt)
+        self.v_cache = torch.zeros((L, self.B, H, S, D), device=dev, dtype=dt)
+        self.tok = torch.zeros(self.B, dtype=torch.long, device=dev)
+        self.pos = torch.zeros(self.B, dtype=torch.long, device=dev)
+        self.out_tokens = torch.zeros((self.B, S), dtype=torch.long, device=dev)
+        self.h0 = torch.zeros((self.B, d), device=dev, dtype=dt)
+        self._host_pos = 0
+        self.graph = None
+
+    def reset(self) -> None:
+        self._host_pos = 0
+        self.k_cache.zero_()
+        self.v_cache.zero_()
+        self.tok.zero_()
+        self.pos.zero_()
+        self.graph = None
+
+    def prefill(self, prompts: torch.Tensor) -> None:
+        """prompts [B, T]: each sequence's prompt through the base decoder's prompt pass, into its
+        own cache rows; seeds tok / pos / the next embedding row of every sequence."""
+        base, T = self.base, prompts.shape[1]
+        if prompts.shape[0] != self.B or T > self.cfg.max_seq:
+            raise ValueError(f"prompts must be [{self.B}, T <= {self.cfg.max_seq}]")
+        kc, vc = base.k_cache, base.v_cache
+        try:
+            for b in range(self.B):
+                base.k_cache, base.v_cache = self.k_cache[:, b], self.v_cache[:, b]
+                logits = base.forward(prompts[b].to(base.device), base._positions[:T], from_start=True)
+                self.tok[b] = logits.argmax()
+        finally:
+            base.k_cache, base.v_cache = kc, vc
+        self.pos.fill_(T)
+        self.h0.copy_(base.weights["embed"][self.tok])
+        self._host_pos = T
+        self.graph = None
+
+    def _step(self) -> None:
+        base, cfg, B = self.base, self.cfg, self.B
+        if B <= 4 and not base.dense and base.gate_up_il is not None:
+            return self._step_fused()
+        act, st = _ACT[base.dtype], _lib.stream_handle()
+        d, H, D, S = cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.max_seq
+        h = self.h0
+        xn = torch.empty((B, d), device=base.device, dtype=base.dtype)
+        att = torch.empty((B, d), device=base.device, dtype=base.dtype)
+        delta = None
+        for i in range(cfg.n_layers):
+            lw = base.lin[i]
+            _lib.call("tr_add_rmsnorm", act, h.data_ptr(), 0 if delta is None else delta.data_ptr(),
+                      base.norm_attn[i].data_ptr(), xn.data_ptr(), B, d, cfg.eps, st)
+            qkv = base._lin(xn, lw["qkv"])
+            _lib.call("tr_attn_decode_batch", act, qkv.data_ptr(), self.pos.data_ptr(), base.cos.data_ptr(),
+                      base.sin.data_ptr(), self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(),
+                      B, H, D, S, D ** -0.5, st)
+            o = base._lin(att, lw["o"])
+            _lib.call("tr_add_rmsnorm", act, h.data_ptr(), o.data_ptr(), base.norm_mlp[i].data_ptr(), xn.data_ptr(),
+                      B, d, cfg.eps, st)
+            gu = base._lin(xn, lw["gate_up"])
+            a = torch.empty((B, cfg.d_ff), device=base.device, dtype=base.dtype)
+            _lib.call("tr_silu_mul", act, gu.data_ptr(), a.data_ptr(), B, cfg.d_ff, st)
+            delta = base._lin(a, lw["down"])
+        _lib.call("tr_add_rmsnorm", act, h.data_ptr(), delta.data_ptr(), base.norm_out.data_ptr(), xn.data_ptr(),
+                  B, d, cfg.eps, st)
+        logits = F.linear(xn, base.weights["lm_head"])
+        self.last_logits = logits   # (the graph's buffer: the latest step's logits after a replay)
+        _lib.call("tr_greedy_next_batch", act, logits.data_ptr(), logits.shape[-1], self.out_tokens.data_ptr(),
+                  self.out_tokens.shape[1], self.tok.data_ptr(), self.pos.data_ptr(),
+                  base.weights["embed"].data_ptr(), d, self.h0.data_ptr(), B, st)
+
+    def _step_fused(self) -> None:
+        """Batch 2-4 on the int8-slice GEMV: residual add + RMSNorm fused into the qkv and gate|up
+        products, SwiGLU into gate|up's epilogue (the single-sequence decode step, batched)."""
+        base, cfg, B = self.base, self.cfg, self.B
+        act, st = _ACT[base.dtype], _lib.stream_handle()
+        d, H, D, S = cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.max_seq
+        hs = [self.h0, torch.empty((B, d), device=base.device, dtype=base.dtype)]
+        att = torch.empty((B, d), device=base.device, dtype=base.dtype)
+        cur, delta = 0, None
+        for i in range(cfg.n_layers):
+            lw = base.lin[i]
+            qkv = linear_pre(hs[cur], lw["qkv"], _lib.PRE_ADD_RMSNORM, delta, base.norm_attn[i], hs[1 - cur], cfg.eps,
+                             pdl=True)
+            cur = 1 - cur
+            _lib.call("tr_attn_decode_batch", act, qkv.data_ptr(), self.pos.data_ptr(), base.cos.data_ptr(),
+                      base.sin.data_ptr(), self.k_cache[i].data_ptr(), self.v_cache[i].data_ptr(), att.data_ptr(),
+                      B, H, D, S, D ** -0.5, st)
+            o = linear(att, lw["o"], pdl=True)
+            act_ = linear_pre(hs[cur], base.gate_up_il[i], _lib.PRE_ADD_RMSNORM, o, base.norm_mlp[i], hs[1 - cur],
+                              cfg.eps, pdl=True, epi_swiglu=True)
+            cur = 1 - cur
+            delta = linear(act_, lw["down"], pdl=True)
+        xn = torch.empty((B, d), device=base.device, dtype=base.dtype)
+        _lib.call("tr_add_rmsnorm", act, hs[cur].data_ptr(), delta.data_ptr(), base.norm_out.data_ptr(), xn.data_ptr(),
+                  B, d, cfg.eps, st)
+        logits = F.linear(xn, base.weights["lm_head"])
+        self.last_logits = logits
+        _lib.call("tr_greedy_next_batch", act, logits.data_ptr(), logits.shape[-1], self.out_tokens.data_ptr(),
+                  self.out_tokens.shape[1], self.tok.data_ptr(), self.pos.data_ptr(),
+                  base.weights["embed"].data_ptr(), d, self.h0.data_ptr(), B, st)
+
+    def capture(self) -> None:
+        cur = torch.cuda.current_stream(self.base.device)
+        s = torch.cuda.Stream(device=self.base.device)
+        saved = (self.tok.clone(), self.pos.clone(), self.k_cache.clone(), self.v_cache.clone(), self.h0.clone(),
+                 self.out_tokens.clone())
+        s.wait_stream(cur)
+        with torch.cuda.stream(s):
+            self._step()   # warm-up outside capture
+            s.synchronize()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=s):
+                self._step()
+        torch.cuda.synchronize(self.base.device)
+        cur.wait_stream(s)
+        for t, v in zip((self.tok, self.pos, self.k_cache, self.v_cache, self.h0, self.out_tokens), saved):
+            t.copy_(v)
+
+    def decode(self, n: int) -> None:
+        """n greedy steps for every sequence (out_tokens[b, pos] holds sequence b's tokens)."""
+        if self._host_pos + n > self.cfg.max_seq:
+            raise ValueError(f"decode({n}) from position {self._host_pos} exceeds max_seq={self.cfg.max_seq}")
+        if self.graph is None:
+            self.capture()
+        for _ in range(n):
+            self.graph.replay()
+        self._host_pos += n
