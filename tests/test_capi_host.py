@@ -97,3 +97,36 @@ def test_critical_batch_and_weight_bytes():
     assert critical_batch(1678.2e12 / 6553e9, 2.0625) == 33
     assert weight_bytes(8, 300, DType.TQ2) == 1056 and weight_bytes(8, 300, DType.TQ1) == 864
     assert weight_bytes(8, 300, DType.F16) == 4800 and weight_bytes(8, 300, DType.F32) == 9600
+
+
+def test_decode_entry_points_validate_without_gpu():
+    """The round-2 decode entry points check their arguments before touching the GPU: wrong head
+    size, cache length, batch bounds, workspace size and flag combinations come back as -1 with a
+    message (the product path never silently falls back)."""
+    from paper_2506_23025_b200 import _lib
+
+    lib = _lib.lib()
+    assert lib.tr_qkv_attn_decode_workspace_size(24) == 24 * 4
+    assert lib.tr_qkv_attn_decode_workspace_size(0) == 0
+    assert lib.tr_attn_decode_workspace_size(24, 128, 128) >= 0
+    cases = [
+        # (entry point, args, message fragment)
+        ("tr_attn_decode_batch", (1, None, None, None, None, None, None, None, 2, 24, 64, 128, 0.1, None), b"head_dim"),
+        ("tr_attn_decode_batch", (1, None, None, None, None, None, None, None, 0, 24, 128, 128, 0.1, None), b"batch"),
+        ("tr_attn_decode_batch", (1, None, None, None, None, None, None, None, 2, 24, 128, 256, 0.1, None), b"max_seq"),
+        ("tr_greedy_next_batch", (1, None, 0, None, 8, None, None, None, 16, None, 2, None), b"sizes"),
+        ("tr_greedy_next_batch", (1, None, 100, None, 8, None, None, None, 16, None, 0, None), b"batch"),
+        ("tr_qkv_attn_decode", (1, None, None, None, None, None, 1e-5, None, None, None, None, None, None, None,
+                                24, 128, 128, 0.1, None, 0, 0, None), b"workspace"),
+        ("tr_qkv_attn_decode", (3, None, None, None, None, None, 1e-5, None, None, None, None, None, None, None,
+                                24, 128, 128, 0.1, None, 96, 0, None), b"act_dtype"),
+        ("tr_attn_decode", (1, None, None, None, None, None, None, None, 24, 128, 512, 0.1, None), b"max_seq"),
+    ]
+    for name, args, frag in cases:
+        rc = getattr(lib, name)(*args)
+        assert rc == -1, name
+        assert frag in lib.tr_last_error(), (name, lib.tr_last_error())
+    # the SwiGLU epilogue never falls through to a path that does not know it
+    flags = _lib.LINEAR_EPI_SWIGLU | _lib.LINEAR_FORCE_UMMA
+    rc = lib.tr_linear(2, None, None, None, 1, 64, 64, 1, 64, 32, flags, None, 0, None)
+    assert rc == -1
