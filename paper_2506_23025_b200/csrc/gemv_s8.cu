@@ -266,18 +266,25 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
 #ifdef S8_PRE_PROBE
     stamp(10);
 #endif
+    // inverse RMS of every staged row, once per warp before its items (the same fixed-order sum in
+    // every warp and CTA; it was recomputed per item, a reduction chain in front of each staging)
+    float ivr[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (r >= nrx) break;   // (warp-uniform)
+      float ss = 0.0f;
+      for (int q = lane; q < nb; q += 32) ss += ss_buf[q * nrx + r];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      ivr[r] = rsqrtf(ss / a.cols + a.eps);
+    }
     for (int item = warp, ii = 0; item < nb * nrx; item += NW, ++ii) {
       const int kb = item >> lr, br = item & (nrx - 1);
       const int64_t kx = (int64_t)kb * kBlock + lane * 8;
       float f[8], gm[8];
       s8_f8<T>(*reinterpret_cast<const uint4*>(xs + (size_t)item * kS8ItemBytes + lane * 16), f);
       s8_f8<T>(ii == 0 ? pgv[0] : ii == 1 ? pgv[1] : s8_load8(gam, kx, a.cols, a.x_vec), gm);
-      // inverse RMS of row br: the same fixed-order sum in every warp and CTA
-      float ss = 0.0f;
-      for (int q = lane; q < nb; q += 32) ss += ss_buf[q * nrx + br];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      const float iv = rsqrtf(ss / a.cols + a.eps);
+      const float iv = br == 0 ? ivr[0] : br == 1 ? ivr[1] : br == 2 ? ivr[2] : ivr[3];
 #pragma unroll
       for (int e = 0; e < 8; ++e) f[e] = s8_rnd<T>(s8_rnd<T>(f[e] * iv) * gm[e]);
       __syncwarp();   // every lane holds its h before the item's bytes are overwritten
