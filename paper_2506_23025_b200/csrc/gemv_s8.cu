@@ -673,11 +673,16 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_gemv_s8(const S8Ar
 
 // ------------------------------------------------------------------------------------ host
 
+#ifndef S8_NS16
+#define S8_NS16 2   // weight-ring slots per warp at 16 warps (measured: decode 1114 -> 1128 tok/s; the
+                    // BASELINE stack and the 70B layers within 0.5%)
+#endif
 template <int NW>
 static int s8_ns(int n_tiles, int nb, int grid) {
   const int tiles_max = (int)ceil_div(n_tiles, grid);
   const int ops = (int)ceil_div(ceil_div((int64_t)tiles_max * nb, NW), kS8SU);
-  return ops >= kS8NSMax ? kS8NSMax : ops > 2 ? 4 : ops > 1 ? 2 : 1;
+  const int cap = NW == 16 ? S8_NS16 : kS8NSMax;
+  return ops >= cap ? cap : ops > 2 ? 4 : ops > 1 ? 2 : 1;
 }
 
 #ifndef S8_SMALL_UNITS

@@ -14,7 +14,10 @@ constexpr int kS8SU = 2;
 #ifndef S8_TWO_CHAINS
 #define S8_TWO_CHAINS 0   // 1: each unit's 8 IMMAs as two accumulator chains (measured 1-2% slower)
 #endif              // units per ring slot (one bulk copy)
-constexpr int kS8NSMax = 4;
+#ifndef S8_NS_MAX
+#define S8_NS_MAX 4
+#endif
+constexpr int kS8NSMax = S8_NS_MAX;
 constexpr int kS8ItemBytes = 1024;    // staged x per (block, batch row): 4 slices x 4 chunks x 16 words
 constexpr int kQ1ItemBytes = 1280;    // TQ1: 4 slices x 4 lane columns x 80 B (18 words of 9 MMAs + pad)
 
