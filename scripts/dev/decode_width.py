@@ -10,10 +10,10 @@ prompt = torch.randint(0, cfg.vocab, (64,), device="cuda", generator=torch.Gener
 m = TernaryDecoder(cfg)
 res = {}
 for fa in (False,):
-    for fs in [(False, True, g, d) for g in (False, True) for d in (False, True)]:
+    for fs in [(False, True, False, False), (True, True, False, False), (False, False, False, False)]:
         m.use_fused_attention(fa)
-        m.full_sm = (False, True, False, False)
-        m.cosched = fs
+        m.full_sm = fs
+        m.cosched = (False, False, False, False)
         m.reset(); m.prefill(prompt); m.capture()
         best = None
         for _ in range(3):
@@ -22,5 +22,5 @@ for fa in (False,):
             e[0].record(); m.prefill(prompt); e[1].record(); m.decode(64); e[2].record(); e[2].synchronize()
             t = e[1].elapsed_time(e[2])
             best = t if best is None or t < best else best
-        res[f"fa={int(fa)} cosched={''.join(str(int(v)) for v in fs)}"] = round(64 / best * 1e3, 1)
+        res[f"fa={int(fa)} full_sm={''.join(str(int(v)) for v in fs)}"] = round(64 / best * 1e3, 1)
 print(json.dumps(res))
