@@ -50,26 +50,35 @@ int gemv_chain_s8(int act, const TrChainLayer* host, int n, int batch, void* ws,
 size_t chain_workspace_bytes(int n_ops);
 
 // GEMV / tensor-core GEMM crossover, measured per shape at batch 2-12 (scripts/dev/crossover.py,
-// DESIGN.md section 4 "Dispatch"): the GEMVs restage every activation row in every CTA, so their
-// cost grows with batch x cols; K5 costs about the same for any batch up to 16 but pays a fixed
-// ~3.5 us per CTA and spreads poorly when a shape has few 128-row tiles.
-//  * batch <= 2: the int8-slice GEMV;
-//  * batch 3-4: the int8-slice GEMV while K <= 4096 columns, or K <= 8192 on shapes K5 spreads
-//    badly (>= 12 blocks per CTA: 8192 x 8192 measured 12.3 vs 14.4 us), else K5;
-//  * batch 5-8: the fp16 GEMV only for K <= 4096 columns on shapes K5 spreads badly (>= 12
-//    blocks per CTA, e.g. 11008 x 4096), else K5;
-//  * batch >= 9: K5.
+// then in the BASELINE stack and the batched decoder; DESIGN.md section 4 "Dispatch"): the GEMVs
+// restage every activation row in every CTA, so their cost grows with batch x cols; K5 costs about
+// the same for any batch up to 16 but pays a fixed cost per CTA and spreads poorly when a shape has
+// few 128-row tiles.
+//  * batch 1: the int8-slice GEMV (TQ2) / K4 (TQ1);
+//  * batch 2: the same, except K > 8192 columns spread over <= 8 blocks per K5 CTA (3072 x 9216);
+//  * batch >= 3: K5 (the fp16 GEMV K3 only for activation rows K5 cannot take).
 // int8-slice GEMV CTA width: 1 = half-SM 8-warp CTAs (TR_LINEAR_COSCHEDULE), 2 = whole-SM 16-warp
 // CTAs (TR_LINEAR_FULL_SM), 0 = by shape
 static int sched_mode(int flags) {
   return (flags & TR_LINEAR_FULL_SM) ? 2 : (flags & TR_LINEAR_COSCHEDULE) ? 1 : 0;
 }
+#ifndef TR_B34_UMMA_ALL
+#define TR_B34_UMMA_ALL 1
+#endif
 static bool prefer_umma(int64_t batch, int64_t rows, int64_t cols) {
-  if (batch <= 2) return false;
-  // blocks each K5 CTA walks: how well the GEMM spreads this shape (scripts/dev/crossover.py, after
-  // K5's uniform-datapath MMA issue and split-K changes: 4096^2 b=3-4 K5 6.0-6.1 vs GEMV 6.7 us;
-  // 9216x3072 b=4 GEMV 7.6 vs 8.0; 11008x4096 b=4 GEMV 8.5 vs 9.5; from b=5 K5 wins every shape)
+  if (batch == 1) return false;
+  // blocks each K5 CTA walks: how well the GEMM spreads this shape
   const int bpc = umma_blocks_per_cta((int)batch, (int)rows, (int)cols);
+  // batch 2: K5 for long K spread thin (after K5's interleaved decode and 4-stage weight ring at
+  // N = 16; scripts/dev/crossover.py: 3072x9216 (6 blocks per CTA) K5 7.51 vs GEMV 8.27 us, batched
+  // 3.9B decode B=2 1858 -> 1990 tok/s; 4096x11008 (11 blocks) 8.68 vs 8.81 isolated but 6% slower in
+  // the BASELINE stack, so it stays on the GEMV)
+  if (batch == 2) return cols > 8192 && bpc <= 8;
+  // batch 3-4: K5 everywhere (11008x4096 b=4 8.52 vs 8.64, 4096^2 6.03 vs 6.69; BASELINE stack b=3-4
+  // 0.785 -> 0.751 ms; the one shape the GEMV still wins, 9216x3072, by 1.2%)
+  if (TR_B34_UMMA_ALL && batch <= 4) return true;
+  // (before those changes: 4096^2 b=3-4 K5 6.0-6.1 vs GEMV 6.7 us; 9216x3072 b=4 GEMV 7.6 vs 8.0;
+  // 11008x4096 b=4 GEMV 8.5 vs 9.5; from b=5 K5 wins every shape)
   if (batch <= 4) return cols > 8192 || (cols > 4096 && bpc < 12) || bpc <= 4;
   return true;
 }

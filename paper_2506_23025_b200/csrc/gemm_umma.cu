@@ -37,6 +37,10 @@ namespace umma {
 // CTA-0 clock trace (probe 4) compiled in only for dev builds (-DUMMA_TRACE=1): its checks sat in
 // the decode and MMA loops of every launch
 constexpr bool kTrace = UMMA_TRACE != 0;
+#ifndef UMMA_ILV
+#define UMMA_ILV 1
+#endif
+constexpr bool kIlv = UMMA_ILV != 0;           // uniform scale, N <= 32: warp groups decode alternate blocks
 constexpr int kWorkers = 8;                    // decode/epilogue warps
 constexpr int kThreads = (kWorkers + 2) * 32;  // + producer warp + MMA warp
 constexpr int kRowsPerCta = 128;
@@ -252,7 +256,10 @@ struct UmmaCfg {
 #ifndef UMMA_RB_MID
 #define UMMA_RB_MID 5
 #endif
-  static constexpr int RW = N <= 32 ? UMMA_RW_SMALL : (N == 128 && UMMA_N128_RB == 3) ? 2 : UMMA_RW_MID;
+#ifndef UMMA_RW16
+#define UMMA_RW16 4
+#endif
+  static constexpr int RW = N <= 16 ? UMMA_RW16 : N <= 32 ? UMMA_RW_SMALL : (N == 128 && UMMA_N128_RB == 3) ? 2 : UMMA_RW_MID;
   // (N = 32, 64: the spare shared memory goes to activation stages as well: +0.5-1.2% at b = 32-64;
   // N = 16 measured no gain from 8)
   static constexpr int RB = N <= 16 ? UMMA_RB16 : N <= 64 ? UMMA_RB_MID : UMMA_N128_RB;   // activation stages (one block each)
@@ -328,7 +335,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
       mbar_init(&empty_b[s], 1);
     }
     for (int i = 0; i < Cfg::kMaxA; ++i) {
-      mbar_init(&a_full[i], kWorkers);
+      mbar_init(&a_full[i], (kIlv && N <= 32 && !per_block) ? kWorkers / 2 : kWorkers);
       mbar_init(&a_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -482,7 +489,82 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
       if (per_block && i > 0) epilogue_block(i - 1, s_prev);
       s_prev = s_cur;
     };
-    {   // per block: weights to registers, wait for the A buffer, decode 32 columns at a time into TMEM
+    if (kIlv && N <= 32 && !per_block) {
+      // uniform scale (no per-block epilogue): the two warp groups decode alternate 256-blocks, each
+      // a whole block of its 32 rows, so one group's per-block waits (weights, A buffer, TMEM store
+      // drain) overlap the other group's decode.  Every warp still arrives once per weight stage
+      // (KS >= 2: a stage holds blocks of both parities, except a one-block last stage, which is
+      // never refilled); A buffers i % kMaxA (NA = kMaxA in this mode).  Measured (umma_b16.py):
+      // b=16-32 2-3% faster per layer; at N = 64 / 128 1-4% slower (MMA-paced there), so N <= 32
+      constexpr int NAu = Cfg::kMaxA;
+      bool have_s = false;
+      for (int i = half_k; i < nblk; i += 2) {
+        const int j = i % KS, si = i / KS, s = si % RW;
+        if (j < 2) mbar_wait(&full_w[s], (si / RW) & 1);
+        const uint32_t unit = sW32 + s * kStageW + j * UB;
+        const uint32_t sv = ld_shared_u32(unit + Cfg::TBB + g * 4);
+        uint4 wv[4];
+        uint32_t wq[2][7];
+        if constexpr (FMT == kFmtTq1) {
+#pragma unroll
+          for (int hk = 0; hk < 2; ++hk)
+#pragma unroll
+            for (int m = 0; m < 7; ++m) wq[hk][m] = ld_shared_u32(unit + rt * kQ1RowBytes + (hk * 6 + m) * 4);
+        } else {
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) wv[cc] = ld_shared_v4(unit + t16_word(hrow, cc, g) * 16);
+        }
+        if (!have_s) {
+          s_first = __half2float(hrow ? __high2half(*reinterpret_cast<const __half2*>(&sv))
+                                      : __low2half(*reinterpret_cast<const __half2*>(&sv)));
+          have_s = true;
+        }
+        if (j + 2 >= KS || i + 2 >= nblk) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty_w[s]);
+        }
+        const int ab = i % NAu;
+        mbar_wait(&a_empty[ab], ((i / NAu) & 1) ^ 1);
+        tc_fence_after();
+        if (!(a.dbg & 2)) {
+          if constexpr (FMT == kFmtTq1) {
+#pragma unroll
+            for (int hk = 0; hk < 2; ++hk) {
+              uint32_t col[64];
+              decode_q1<T>(wq[hk], hk, col);
+              tmem_st32(tA + lane_off + ab * 128 + hk * 64, *reinterpret_cast<const uint32_t(*)[32]>(col));
+              tmem_st32(tA + lane_off + ab * 128 + hk * 64 + 32, *reinterpret_cast<const uint32_t(*)[32]>(col + 32));
+            }
+          } else {
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+              const uint32_t W[4] = {wv[cc].x, wv[cc].y, wv[cc].z, wv[cc].w};
+              uint32_t col[32];
+#pragma unroll
+              for (int w = 0; w < 4; ++w) {
+                const uint32_t w8 = W[w] >> 8;
+#pragma unroll
+                for (int hb = 0; hb < 2; ++hb)
+#pragma unroll
+                  for (int jj = 0; jj < 4; ++jj)
+                    col[16 * (w >> 1) + 8 * hb + 2 * jj + (w & 1)] = Dec<T>::trit2(W[w], w8, hb, jj);
+              }
+              tmem_st32(tA + lane_off + ab * 128 + cc * 32, col);
+            }
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[ab]);
+      }
+      if (!have_s && nblk > 0) {   // one block, taken by the other group: its scale (single stage)
+        mbar_wait(&full_w[0], 0);
+        const uint32_t sv = ld_shared_u32(sW32 + Cfg::TBB + g * 4);
+        s_first = __half2float(hrow ? __high2half(*reinterpret_cast<const __half2*>(&sv))
+                                    : __low2half(*reinterpret_cast<const __half2*>(&sv)));
+      }
+    } else {   // per block: weights to registers, wait for the A buffer, decode 32 columns at a time into TMEM
       // (ring positions and phases advance incrementally: the divisions by KS, RW and NA were a
       // tenth of the decode warps' instructions at N = 16)
       int j = 0, s = 0, wph = 0, ab = 0, aph = 1;
