@@ -117,11 +117,10 @@ TR_API size_t tr_linear_workspace_size(int fmt, int64_t batch, int64_t rows, int
 /* y[batch, rows] = x[batch, cols] @ W^T  (linear.py:137-166 gemm semantics with the
  * paper's fp16/bf16 activations, fp32 accumulation, RNE output).  w is the device
  * layout from tr_repack; x has leading dimension ldx, y has ldy (elements).
- * Dispatch (measured crossovers): batch 1-2, and batch 3-4 up to 4096 columns
- * (8192 when the GEMM would walk >= 12 blocks per CTA) unless the GEMM would walk <= 4 blocks
- * per CTA, run the int8-slice GEMV (K3-S8: exact integer block sums over activations put on a
- * 2^-24 grid of each 256-column block's maximum; TQ1 weights: K4); everything else the tcgen05
- * GEMM (K5).  The fp16 mma.sync GEMV (K3) runs on request (TR_LINEAR_GEMV_F16 / FORCE_GEMV) and
+ * Dispatch (measured crossovers): batch 1-2 run the int8-slice GEMV (K3-S8:
+ * exact integer block sums over activations put on a 2^-24 grid of each 256-column block's
+ * maximum; TQ1 weights: K4), except batch 2 with more than 8192 columns spread over <= 8
+ * blocks per GEMM CTA; everything else the tcgen05 GEMM (K5).  The fp16 mma.sync GEMV (K3) runs on request (TR_LINEAR_GEMV_F16 / FORCE_GEMV) and
  * where K3-S8 cannot stage the activations and K5 cannot take them (unaligned rows).
  * flags: TR_LINEAR_* bits | (knob << 8): GEMV CTA count / GEMM K split (0 = automatic). */
 TR_API int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int64_t rows, int64_t cols,

@@ -140,8 +140,8 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
     Accumulation is fp32: per 256-block partial sums are scaled by the block's
     binary16 scale in fp32 and accumulated in ascending block order; the output
     is rounded once to x.dtype.  ``pdl`` launches with programmatic dependent
-    launch (for CUDA-graph-chained layers).  Batches 1-2 run the decode GEMV, batches
-    >= 5 the tcgen05 tensor-core GEMM, and 3-4 whichever the shape favours (measured
+    launch (for CUDA-graph-chained layers).  Batches 1-2 run the decode GEMV (batch 2
+    with a long, thinly spread K the GEMM), batches >= 3 the tcgen05 tensor-core GEMM (measured
     crossovers, ``tritrun.h``); ``path`` ("umma" / "gemv" / "gemv_f16") forces one.  ``ctas`` forces the GEMV's CTA count and ``ksplit`` the GEMM's
     K split (0 = automatic); ``ws`` overrides the per-stream workspace.
     ``cosched`` (TR_LINEAR_COSCHEDULE) marks a layer in a back-to-back GEMV chain: at batch 1

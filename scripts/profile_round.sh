@@ -11,6 +11,8 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_ge
   -o gpurun_out/prof_gemv env COSCHED=1 python scripts/ncu_target.py 11008 4096 1 > /dev/null 2>&1; echo "gemv prof rc=$?"
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_gemm_umma -s 6 -c 1 \
   -o gpurun_out/prof_umma python scripts/ncu_target.py 11008 4096 128 > /dev/null 2>&1; echo "umma prof rc=$?"
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_gemm_umma -s 6 -c 1 \
+  -o gpurun_out/prof_u16 python scripts/ncu_target.py 11008 4096 16 > /dev/null 2>&1; echo "umma b16 prof rc=$?"
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_gemv_s8 -s 6 -c 1 \
   -o gpurun_out/prof_q1 env FMT=TQ1 python scripts/ncu_target.py 8192 8192 1 > /dev/null 2>&1; echo "q1 prof rc=$?"
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_gemv_chain -s 2 -c 1 \

@@ -41,6 +41,7 @@ import os
 
 for name, rep, shape in [("gemv", "gpurun_out/prof_gemv.ncu-rep", "rows 11008 x cols 4096, batch 1, fp16"),
                          ("umma", "gpurun_out/prof_umma.ncu-rep", "rows 11008 x cols 4096, batch 128, fp16"),
+                         ("umma_b16", "gpurun_out/prof_u16.ncu-rep", "rows 11008 x cols 4096, batch 16, fp16"),
                          ("gemv_tq1", "gpurun_out/prof_q1.ncu-rep", "TQ1 rows 8192 x cols 8192, batch 1, fp16"),
                          ("chain", "gpurun_out/prof_chain.ncu-rep",
                           "K6 chain, 8 replicas of (4096x4096, 11008x4096, 4096x11008), batch 1, fp16")]:
