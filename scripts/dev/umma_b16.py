@@ -1,5 +1,5 @@
 """Dev: K5 per-layer us at b = 16 / 32 on the configs[1] shapes (graph + PDL, rotating copies > L2);
-run under different TRITRUN_LIB builds for A/B."""
+run under different TRITRUN_LIB builds for A/B; DT=bf16 for bfloat16 activations."""
 import sys, os, json
 sys.path.insert(0, os.getcwd())
 import torch
@@ -18,7 +18,7 @@ for rows, cols in ((11008, 4096), (4096, 4096), (4096, 11008)):
         gam = (0.02 * (1 + torch.rand((rows, 1), generator=g, device="cuda"))).half().float()
         ws.append(tp.TernaryWeight.from_float(gam * T))
     for b in (16, 32):
-        x = bench.uniform_x(b, cols, b)
+        x = bench.uniform_x(b, cols, b, torch.bfloat16 if os.environ.get("DT") == "bf16" else None)
         res[f"{rows}x{cols}_b{b}"] = round(bench._time_layers(ws, x, path="umma") * 1e3, 2)
     del ws
     torch.cuda.empty_cache()

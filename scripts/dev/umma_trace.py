@@ -9,8 +9,8 @@ import paper_2506_23025_b200 as tp
 rows, cols, b = (int(v) for v in sys.argv[1:4])
 torch.cuda.set_device(0)
 ws = [tp.TernaryWeight.from_float(torch.randint(-1, 2, (rows, cols), device="cuda").float() * 0.02) for _ in range(4)]
-x = (torch.rand(b, cols, device="cuda") * 2 - 1).half()
-ys = [torch.zeros(b, rows, dtype=torch.float16, device="cuda") for _ in ws]
+x = (torch.rand(b, cols, device="cuda") * 2 - 1).to(torch.bfloat16 if os.environ.get("DT") == "bf16" else torch.half)
+ys = [torch.zeros(b, rows, dtype=x.dtype, device="cuda") for _ in ws]
 for rep in range(3):
     for w, y in zip(ws, ys):
         tp.linear(x, w, out=y, path="umma", _probe=4 | int(os.environ.get("PROBE", "0")), pdl=True)
