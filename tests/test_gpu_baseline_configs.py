@@ -133,3 +133,30 @@ def test_config5_row_parallel_recombination(tp, tpn, batch):
 @pytest.mark.parametrize("rows,cols", [(9216, 3072), (3072, 3072), (18432, 3072), (3072, 9216)])
 def test_config3_decoder_layer_shapes(tp, rows, cols):
     _check(tp, rows, cols, tp.DType.TQ2, 1)
+
+
+# the bench's timed stack itself (bench.make_stack_weights + graph.LinearStack): activations stay
+# finite through the chained layers (its synthetic gamma keeps each layer's RMS; a fixed 0.02-0.04
+# had overflowed fp16 to NaN from layer 16 on), and the last layer matches the oracle on the input
+# the chain actually fed it
+@pytest.mark.parametrize("batch,dtype", [(1, "float16"), (16, "float16"), (4, "bfloat16")])
+def test_bench_stack_finite_and_last_layer_vs_oracle(tp, batch, dtype):
+    import bench
+    from paper_2506_23025_b200.graph import LinearStack
+
+    dt = getattr(torch, dtype)
+    ws = bench.make_stack_weights(8, seed=1234)   # 24 chained layers
+    st = LinearStack(ws, batch=batch, dtype=dt)
+    st.x.copy_(bench.uniform_x(batch, st.x.shape[1], 4242 + batch, dt))
+    st.replay()
+    torch.cuda.synchronize()
+    for i, o in enumerate(st.bufs):
+        assert bool(torch.isfinite(o).all()), f"layer {i}: non-finite output"
+        m = float(o.float().abs().max())
+        assert 0.1 < m < 100.0, f"layer {i}: |y|max {m:.3g} drifted"
+    w = ws[-1]
+    p, s = w.unpack()
+    ref = orc.gemv_reference_batch(p.cpu().numpy(), s.cpu().numpy(), w.cols, int(w.fmt),
+                                   st.bufs[-2].float().cpu().numpy())
+    err = rel_err(st.bufs[-1].float().cpu().numpy(), ref)
+    assert err <= (2e-3 if dtype == "float16" else 6e-3), f"last layer b={batch} {dtype}: rel err {err:.3e}"
