@@ -242,14 +242,16 @@ struct UmmaCfg {
 #define UMMA_KS_SMALL 4
 #endif
 #ifndef UMMA_RW_SMALL
-#define UMMA_RW_SMALL 2
+#define UMMA_RW_SMALL 4   // (N = 32 only: N = 16 has UMMA_RW16)
 #endif
 #ifndef UMMA_RB16
 #define UMMA_RB16 4
 #endif
   static constexpr int KS = N <= 32 ? UMMA_KS_SMALL : 2;     // 256-blocks per weight stage
-  // weight stages: two (re-measured after the MMA issue work: N <= 32 b=16-32 1.5-2% faster than
-  // four; N = 64 4096^2 b=128 10.96 -> 10.58 us, 4096x11008 b=64 13.35 -> 13.12 against three)
+  // weight stages: two at N = 64 / 128 (re-measured after the MMA issue work: N = 64 4096^2 b=128
+  // 10.96 -> 10.58 us, 4096x11008 b=64 13.35 -> 13.12 against three).  N = 16 / 32 take four since
+  // K5's interleaved decode (the weight ring underflowed every stage of KS blocks): N = 16 with four
+  // 8 KB activation stages (stack b=8-16 -5%), N = 32 with three 16 KB ones (stack b=24-32 -1.9%)
 #ifndef UMMA_RW_MID
 #define UMMA_RW_MID 2
 #endif
@@ -260,9 +262,12 @@ struct UmmaCfg {
 #define UMMA_RW16 4
 #endif
   static constexpr int RW = N <= 16 ? UMMA_RW16 : N <= 32 ? UMMA_RW_SMALL : (N == 128 && UMMA_N128_RB == 3) ? 2 : UMMA_RW_MID;
-  // (N = 32, 64: the spare shared memory goes to activation stages as well: +0.5-1.2% at b = 32-64;
-  // N = 16 measured no gain from 8)
-  static constexpr int RB = N <= 16 ? UMMA_RB16 : N <= 64 ? UMMA_RB_MID : UMMA_N128_RB;   // activation stages (one block each)
+  // (N = 64: the spare shared memory goes to activation stages, +0.5-1.2% at b = 64; N = 16 / 32
+  // measured best with four weight stages instead, above)
+#ifndef UMMA_RB32
+#define UMMA_RB32 3
+#endif
+  static constexpr int RB = N <= 16 ? UMMA_RB16 : N <= 32 ? UMMA_RB32 : N <= 64 ? UMMA_RB_MID : UMMA_N128_RB;   // activation stages (one block each)
   static constexpr int kStageWBytes = 8 * KS * UB;          // 128 rows x KS blocks
   static constexpr int kStageBBytes = N * 512;               // N rows x 256 K (4 swizzled 64-K atoms)
   static constexpr int kMaxA = 3;                            // TMEM A buffers (128 columns = one block each)
