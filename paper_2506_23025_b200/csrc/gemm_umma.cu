@@ -41,6 +41,9 @@ constexpr bool kTrace = UMMA_TRACE != 0;
 #define UMMA_ILV 1
 #endif
 constexpr bool kIlv = UMMA_ILV != 0;           // uniform scale, N <= 32: warp groups decode alternate blocks
+#ifndef UMMA_ILV_MAXN
+#define UMMA_ILV_MAXN 32
+#endif
 constexpr int kWorkers = 8;                    // decode/epilogue warps
 constexpr int kThreads = (kWorkers + 2) * 32;  // + producer warp + MMA warp
 constexpr int kRowsPerCta = 128;
@@ -340,7 +343,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
       mbar_init(&empty_b[s], 1);
     }
     for (int i = 0; i < Cfg::kMaxA; ++i) {
-      mbar_init(&a_full[i], (kIlv && N <= 32 && !per_block) ? kWorkers / 2 : kWorkers);
+      mbar_init(&a_full[i], (kIlv && N <= UMMA_ILV_MAXN && !per_block) ? kWorkers / 2 : kWorkers);
       mbar_init(&a_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -494,7 +497,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
       if (per_block && i > 0) epilogue_block(i - 1, s_prev);
       s_prev = s_cur;
     };
-    if (kIlv && N <= 32 && !per_block) {
+    if (kIlv && N <= UMMA_ILV_MAXN && !per_block) {
       // uniform scale (no per-block epilogue): the two warp groups decode alternate 256-blocks, each
       // a whole block of its 32 rows, so one group's per-block waits (weights, A buffer, TMEM store
       // drain) overlap the other group's decode.  Every warp still arrives once per weight stage
