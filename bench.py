@@ -86,7 +86,8 @@ class CpuReference:
         self.mats = []
         for rows, cols in SHAPES:
             T = (rng.integers(0, 3, size=(rows, cols), dtype=np.int8) - 1).astype(np.float32)
-            gam = np.float16(0.02 * (1 + rng.uniform(0, 1, size=(rows, 1)))).astype(np.float32)
+            c = 1.0 / (math.sqrt(7.0 / 3.0) * math.sqrt(2.0 * cols / 3.0))   # as make_stack_weights
+            gam = np.float16(c * (1 + rng.uniform(0, 1, size=(rows, 1)))).astype(np.float32)
             payload, scales = oracle.pack_matrix(gam * T, oracle.TQ2)
             self.mats.append((payload, scales, cols))
         self.x = np.float16(rng.uniform(-1, 1, size=(1, 4096))).astype(np.float32)
