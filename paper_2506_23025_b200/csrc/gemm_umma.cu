@@ -41,6 +41,9 @@ constexpr bool kTrace = UMMA_TRACE != 0;
 #define UMMA_ILV 1
 #endif
 constexpr bool kIlv = UMMA_ILV != 0;           // uniform scale, N <= 32: warp groups decode alternate blocks
+#ifndef UMMA_MERGE
+#define UMMA_MERGE 1
+#endif
 #ifndef UMMA_ILV_MAXN
 #define UMMA_ILV_MAXN 32
 #endif
@@ -324,6 +327,11 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
   uint8_t* sB = smem + Cfg::kBOff;
   uint8_t* sW = smem + Cfg::kWOff;
 
+  // activation ring and TMEM A ring of the same depth (N <= 64: NA = kMaxA = 3 in both scale modes):
+  // one commit per block releases both, and the producer waits on the A ring's barrier.  Applies to
+  // N = 32 (three activation stages): stack b=32 0.869 -> 0.857 ms; at N = 16 it only recovers what
+  // a third activation stage instead of four costs
+  constexpr bool kMergeB = UMMA_MERGE && RB == Cfg::kMaxA && N <= 64;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mt = blockIdx.x % a.m_tiles;
   const int nt = (blockIdx.x / a.m_tiles) % a.n_tiles;
@@ -402,7 +410,8 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
           mbar_wait(&empty_w[nw_ % RW], ((nw_ / RW) & 1) ^ 1);
           issue_w(nw_++);
         } else {
-          mbar_wait(&empty_b[nb_ % RB], ((nb_ / RB) & 1) ^ 1);
+          if (kMergeB) mbar_wait(&a_empty[nb_ % RB], ((nb_ / RB) & 1) ^ 1);   // (same ring: one commit)
+          else mbar_wait(&empty_b[nb_ % RB], ((nb_ / RB) & 1) ^ 1);
           issue_b(nb_++);
         }
       }
@@ -438,7 +447,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
           mma_block16<N>(d, (uint32_t)(ab * 128), sB32 + s * kStageB, idesc, (!per_block && i > 0) ? 1 : 0);
         if (kTrace && (a.dbg & 4) && blockIdx.x == 0 && lane == 0 && i < 64)
           reinterpret_cast<long long*>(a.y)[i * 8 + 2] = clock64();
-        mma_commit(&empty_b[s]);                     // activation stage reusable once these MMAs finish
+        if (!kMergeB) mma_commit(&empty_b[s]);       // activation stage reusable once these MMAs finish
         mma_commit(&a_empty[ab]);                    // TMEM A buffer reusable
         if (per_block || i == nblk - 1) mma_commit(&d_full[per_block ? db : 0]);
         if (++s == RB) {   // (ring positions and phases advance incrementally)
