@@ -397,10 +397,15 @@ class TernaryDecoder:
 class BatchedDecoder:
     """B independent sequences decoded together, one token each per step, on a TernaryDecoder's
     weights (or its dense fp16 twin's).  Every projection runs at batch B through ``tr_linear``'s
-    dispatch (the int8-slice GEMV up to batch 2-4, the tcgen05 GEMM beyond); attention and greedy
+    dispatch (the int8-slice GEMV at batch 2, the tcgen05 GEMM beyond); attention and greedy
     selection run one CTA per (sequence, head) / sequence (``tr_attn_decode_batch``,
     ``tr_greedy_next_batch``).  Prompts of equal length; each sequence keeps its own KV cache rows
     [L, B, H, S, D] and position.  decode(n) replays one captured CUDA graph per step."""
+
+    # batches up to this run the fused int8-slice step (_step_fused); from batch 3 the GEMM (K5, the
+    # dispatch's choice there) with separate RMSNorm / SwiGLU kernels is faster: B=3 2236 -> 2286,
+    # B=4 2988 -> 3041 tok/s; B=2 stays fused (1989 against 1714)
+    FUSED_MAX_B = 2
 
     def __init__(self, base: TernaryDecoder, batch: int):
         if not base.fused:
@@ -449,7 +454,7 @@ class BatchedDecoder:
 
     def _step(self) -> None:
         base, cfg, B = self.base, self.cfg, self.B
-        if B <= 4 and not base.dense and base.gate_up_il is not None:
+        if B <= self.FUSED_MAX_B and not base.dense and base.gate_up_il is not None:
             return self._step_fused()
         act, st = _ACT[base.dtype], _lib.stream_handle()
         d, H, D, S = cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.max_seq
@@ -481,7 +486,7 @@ class BatchedDecoder:
                   base.weights["embed"].data_ptr(), d, self.h0.data_ptr(), B, st)
 
     def _step_fused(self) -> None:
-        """Batch 2-4 on the int8-slice GEMV: residual add + RMSNorm fused into the qkv and gate|up
+        """Batch 2 (up to FUSED_MAX_B) on the int8-slice GEMV: residual add + RMSNorm fused into the qkv and gate|up
         products, SwiGLU into gate|up's epilogue (the single-sequence decode step, batched)."""
         base, cfg, B = self.base, self.cfg, self.B
         act, st = _ACT[base.dtype], _lib.stream_handle()

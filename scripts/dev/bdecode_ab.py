@@ -7,6 +7,8 @@ from paper_2506_23025_b200.decoder import DecoderConfig, TernaryDecoder, Batched
 torch.cuda.set_device(0)
 cfg = DecoderConfig(max_seq=128)
 tern = TernaryDecoder(cfg)
+if os.environ.get("FUSED_MAX_B"):
+    BatchedDecoder.FUSED_MAX_B = int(os.environ["FUSED_MAX_B"])
 res = {}
 for B in [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "2,3,4,8,16").split(",")]:
     prompts = torch.randint(0, cfg.vocab, (B, 64), device="cuda", generator=torch.Generator(device="cuda").manual_seed(2))
