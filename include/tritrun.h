@@ -55,7 +55,9 @@ extern "C" {
                                     * too (the decoder's fused-attention step measures best with it) */
 #define TR_LINEAR_EPI_SWIGLU 64    /* bit 6: W's rows are 16-row tiles alternating gate / up (2 F rows);
                                     * y[batch, F] = silu(gate) * up with the roundings of an fp16/bf16
-                                    * gate|up store followed by tr_silu_mul (int8-slice GEMV, batch <= 4) */
+                                    * gate|up store followed by tr_silu_mul (int8-slice GEMV at batch
+                                    * <= 4, or the tcgen05 GEMM where the dispatch picks it: rows a
+                                    * multiple of 32, 16-byte aligned activation rows) */
 #define TR_LINEAR_OUT_F32 128      /* bit 7: y is float32 (the fp32 accumulators, not rounded to the
                                     * activation type): row-parallel partials for an fp32 all-reduce */
 

@@ -37,7 +37,7 @@ int gemv_s8(int act, const void* w, const void* x, void* y, int64_t ldx, int64_t
             float eps, int cosched, int epi, int out_f32, int fmt);
 int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
               int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg,
-              int out_f32);
+              int out_f32, int epi);
 size_t umma_workspace_bytes(int batch, int rows, int cols);
 int umma_blocks_per_cta(int batch, int rows, int cols);
 int gemv_qkv_attn(int act, const void* w, const void* h, const void* delta, const void* gamma, void* h_out,
@@ -121,9 +121,16 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
   const bool aligned = (ldx % 8) == 0 && ((uintptr_t)x & 15) == 0;
   const bool s8 = batch <= 4 && !(flags & TR_LINEAR_GEMV_F16) && gemv_s8_fits((int)batch, (int)rows, (int)cols, fmt) &&
                   (fmt == kFmtTq2 || !prefer_umma(batch, rows, cols) || (flags & TR_LINEAR_FORCE_GEMV));
-  if (epi) {   // only the int8-slice GEMV knows the gate/up tile pairing: never fall through to another path
-    TR_REQUIRE(fmt == kFmtTq2 && s8 && !(flags & TR_LINEAR_FORCE_UMMA),
-               "tr_linear: the SwiGLU epilogue runs on the int8-slice GEMV only (TQ2, batch <= 4)");
+  if (epi) {   // SwiGLU: the int8-slice GEMV or K5 (the two kernels that know the gate/up tile pairing)
+    TR_REQUIRE(fmt == kFmtTq2, "tr_linear: the SwiGLU epilogue takes TQ2 weights");
+    const bool umma_epi = aligned && (rows % 32) == 0 && !(flags & (TR_LINEAR_FORCE_GEMV | TR_LINEAR_GEMV_F16)) &&
+                          ((flags & TR_LINEAR_FORCE_UMMA) || !s8 || prefer_umma(batch, rows, cols));
+    if (umma_epi)
+      return gemm_umma(fmt, act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, uniform, workspace,
+                       ws_bytes, pdl, st, (flags >> 24) & 0xF, 0, 1);
+    TR_REQUIRE(s8 && !(flags & TR_LINEAR_FORCE_UMMA),
+               "tr_linear: the SwiGLU epilogue runs on the int8-slice GEMV (batch <= 4) or the tensor-core GEMM "
+               "(16-byte aligned activation rows, rows a multiple of 32)");
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, pdl, st, 0, nullptr, nullptr,
                    nullptr, 0.0f, sched_mode(flags), 1, 0, kFmtTq2);
   }
@@ -142,7 +149,7 @@ int tr_linear(int fmt, const void* w, const void* x, void* y, int64_t batch, int
   }
   if (use_umma)
     return gemm_umma(fmt, act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, uniform, workspace,
-                     ws_bytes, pdl, st, (flags >> 24) & 0xF, out_f32);
+                     ws_bytes, pdl, st, (flags >> 24) & 0xF, out_f32, 0);
   if (s8)
     return gemv_s8(act_dtype, w, x, y, ldx, ldy, (int)batch, (int)rows, (int)cols, knob, pdl, st, 0, nullptr, nullptr,
                    nullptr, 0.0f, sched_mode(flags), 0, out_f32, fmt);

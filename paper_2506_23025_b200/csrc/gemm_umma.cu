@@ -230,7 +230,22 @@ struct UmmaArgs {
                       // decoded [2] MMAs issued; decode warp 0 [3] A buffer free [4] TMEM stores done
   int map3d;          // activations described by the 3-D tensor map (one TMA request per block)
   int out_f32;        // TR_LINEAR_OUT_F32: y is float32
+  int epi;            // TR_LINEAR_EPI_SWIGLU: rows are 16-row gate / up tile pairs; y[:, rows / 2] = silu(gate) * up
 };
+
+// SwiGLU store of one warp's 32 rows (a gate tile in lanes 0-15, its up tile in lanes 16-31) for
+// activation rows n0.., with the roundings of the unfused gate|up store + tr_silu_mul
+template <typename T, int NV>
+__device__ __forceinline__ void store_swiglu(const UmmaArgs& a, const float (&v)[NV], int n0, int pair, int lane) {
+  const int orow = pair * 16 + (lane & 15);
+#pragma unroll
+  for (int e = 0; e < NV; ++e) {
+    const float g = Act<T>::to_float(Act<T>::from_float(v[e]));
+    const float u = Act<T>::to_float(Act<T>::from_float(__shfl_xor_sync(0xffffffffu, v[e], 16)));
+    const float sg = Act<T>::to_float(Act<T>::from_float(__fdividef(g, 1.0f + __expf(-g))));
+    if (lane < 16 && n0 + e < a.batch) store_y<T>(a.y, (int64_t)(n0 + e) * a.ldy + orow, sg * u, 0);
+  }
+}
 
 template <typename T, int N, int FMT>
 struct UmmaCfg {
@@ -654,11 +669,19 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
     // ---- store: whole K in this CTA -> y; else partials + last-CTA reduction (fixed slice order)
     const int row = mt * kRowsPerCta + r;
     const int n0 = nt * N + half_k * NH;
+    // (SwiGLU: rows % 32 == 0, so a warp's 32 rows are all in range or all out, and the gate / up
+    // shuffle runs warp-wide)
+    const int pair = mt * 4 + quad;
     if (!SPLIT || (a.dbg & 8)) {   // (dev probe 8: split-K slices store unreduced -- timing only)
-      if (row < a.rows && !(kTrace && (a.dbg & 4)))
+      if (row < a.rows && !(kTrace && (a.dbg & 4))) {
+        if (a.epi) {
+          store_swiglu<T, NH>(a, acc, n0, pair, lane);
+        } else {
 #pragma unroll
-        for (int e = 0; e < NH; ++e)
-          if (n0 + e < a.batch) store_y<T>(a.y, (int64_t)(n0 + e) * a.ldy + row, acc[e], a.out_f32);
+          for (int e = 0; e < NH; ++e)
+            if (n0 + e < a.batch) store_y<T>(a.y, (int64_t)(n0 + e) * a.ldy + row, acc[e], a.out_f32);
+        }
+      }
     } else if constexpr (SPLIT) {
       const int tile_mn = nt * a.m_tiles + mt;
       float* part = a.ws + ((int64_t)tile_mn * a.ks + kslice) * (kRowsPerCta * N);
@@ -697,9 +720,13 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
 #pragma unroll
                 for (int e = 0; e < EC; ++e) v[e] += u[qq][e];
             }
+            if (a.epi) {
+              store_swiglu<T, EC>(a, v, n0 + e0, pair, lane);
+            } else {
 #pragma unroll
-            for (int e = 0; e < EC; ++e)
-              if (n0 + e0 + e < a.batch) store_y<T>(a.y, (int64_t)(n0 + e0 + e) * a.ldy + row, v[e], a.out_f32);
+              for (int e = 0; e < EC; ++e)
+                if (n0 + e0 + e < a.batch) store_y<T>(a.y, (int64_t)(n0 + e0 + e) * a.ldy + row, v[e], a.out_f32);
+            }
           }
         if (threadIdx.x == 0) a.counters[tile_mn] = 0;   // self-reset
       }
@@ -809,7 +836,7 @@ static int launch_umma(const CUtensorMap& map, const UmmaArgs& a, int grid, int 
 
 int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t ldx, int64_t ldy, int batch, int rows,
               int cols, int ks, int uniform, void* workspace, size_t ws_bytes, int pdl, cudaStream_t st, int dbg,
-              int out_f32) {
+              int out_f32, int epi) {
   UmmaPlan p = plan_umma(batch, rows, cols, ks, sm_count());
   if ((ldx % 8) != 0 || ((uintptr_t)x & 15) != 0) {
     set_error("tr_linear(umma): activations need 16-byte aligned rows (ldx %% 8 == 0)");
@@ -866,6 +893,11 @@ int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t l
   a.dbg = dbg;
   a.map3d = map3d;
   a.out_f32 = out_f32;
+  a.epi = epi;
+  if (epi && (rows % 32 != 0 || out_f32)) {
+    set_error("tr_linear(umma, swiglu epilogue): rows (%d) must be whole 32-row gate/up pairs, fp16/bf16 out", rows);
+    return -1;
+  }
   const int grid = p.m_tiles * p.n_tiles * p.ks;
   const bool bf = act == kActBf16;
 #define TR_UMMA_CASE(NN)                                                                              \

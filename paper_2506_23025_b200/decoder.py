@@ -149,6 +149,17 @@ class TernaryDecoder:
     def _lin(self, x, w):
         return F.linear(x, w) if self.dense else linear(x, w, pdl=True)
 
+    def _swiglu(self, i, xn):
+        """silu(gate) * up of layer i's MLP for xn [T, d]: the gate|up product's own SwiGLU store on the
+        interleaved weight (int8-slice GEMV or K5), else the product and tr_silu_mul."""
+        if self.gate_up_il is not None and self.cfg.d_ff % 32 == 0:
+            return linear(xn, self.gate_up_il[i], pdl=True, epi_swiglu=True)
+        gu = self._lin(xn, self.lin[i]["gate_up"])
+        a = torch.empty((xn.shape[0], self.cfg.d_ff), device=self.device, dtype=self.dtype)
+        _lib.call("tr_silu_mul", _ACT[self.dtype], gu.data_ptr(), a.data_ptr(), xn.shape[0], self.cfg.d_ff,
+                  _lib.stream_handle())
+        return a
+
     def _rms(self, x, wgt):
         xf = x.float()
         return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + self.cfg.eps)).to(self.dtype) * wgt
@@ -228,9 +239,7 @@ class TernaryDecoder:
             o = self._lin(att, lw["o"])
             _lib.call("tr_add_rmsnorm", act, h.data_ptr(), o.data_ptr(), self.norm_mlp[i].data_ptr(), xn.data_ptr(),
                       T, d, cfg.eps, st)
-            gu = self._lin(xn, lw["gate_up"])
-            a = torch.empty((T, cfg.d_ff), device=self.device, dtype=self.dtype)
-            _lib.call("tr_silu_mul", act, gu.data_ptr(), a.data_ptr(), T, cfg.d_ff, st)
+            a = self._swiglu(i, xn)
             delta = self._lin(a, lw["down"])
         _lib.call("tr_add_rmsnorm", act, h.data_ptr(), delta.data_ptr(), self.norm_out.data_ptr(), xn.data_ptr(),
                   T, d, cfg.eps, st)
@@ -473,9 +482,7 @@ class BatchedDecoder:
             o = base._lin(att, lw["o"])
             _lib.call("tr_add_rmsnorm", act, h.data_ptr(), o.data_ptr(), base.norm_mlp[i].data_ptr(), xn.data_ptr(),
                       B, d, cfg.eps, st)
-            gu = base._lin(xn, lw["gate_up"])
-            a = torch.empty((B, cfg.d_ff), device=base.device, dtype=base.dtype)
-            _lib.call("tr_silu_mul", act, gu.data_ptr(), a.data_ptr(), B, cfg.d_ff, st)
+            a = base._swiglu(i, xn)
             delta = base._lin(a, lw["down"])
         _lib.call("tr_add_rmsnorm", act, h.data_ptr(), delta.data_ptr(), base.norm_out.data_ptr(), xn.data_ptr(),
                   B, d, cfg.eps, st)

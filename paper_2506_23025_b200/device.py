@@ -180,7 +180,7 @@ def linear(x: torch.Tensor, w: TernaryWeight, out: torch.Tensor | None = None, p
     flags = (_lib.LINEAR_PDL if pdl else 0) | (_lib.LINEAR_UNIFORM_SCALE if w.uniform_scale else 0) | _PATHS[path]
     if odt == torch.float32:
         flags |= _lib.LINEAR_OUT_F32
-    if epi_swiglu:   # (tr_linear rejects it on every path but the int8-slice GEMV: TriRunError)
+    if epi_swiglu:   # (the int8-slice GEMV or K5; tr_linear rejects the fp16 GEMV: TriRunError)
         flags |= _lib.LINEAR_EPI_SWIGLU
     if cosched:   # back-to-back GEMV chain: half-SM CTAs so consecutive layers co-reside
         flags |= _lib.LINEAR_COSCHEDULE

@@ -732,10 +732,11 @@ def test_linear_pre_fused_producers(tp, dtype, batch):
 
 
 @pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
-@pytest.mark.parametrize("batch", [1, 2, 3, 4])
+@pytest.mark.parametrize("batch", [1, 2, 3, 4, 5, 16])
 @pytest.mark.parametrize("d,f", [(3072, 9216), (1496, 48), (4096, 11008)])
 def test_linear_epi_swiglu(tp, dtype, batch, d, f):
     # TR_LINEAR_EPI_SWIGLU on an interleaved gate|up weight == plain linear, then tr_silu_mul
+    # (batch 1-2: the int8-slice GEMV; 3+: K5's SwiGLU store, both per-block scales here)
     from paper_2506_23025_b200 import _lib
     from paper_2506_23025_b200.device import _ACT, interleave_gate_up, linear_pre
 
@@ -754,6 +755,11 @@ def test_linear_epi_swiglu(tp, dtype, batch, d, f):
     y = tp.linear(x, w_il, epi_swiglu=True).float()
     assert y.shape == (batch, f)
     assert ((y - ref).abs().amax(1) / ref.abs().amax(1)).max().item() <= tol
+    # the tensor-core GEMM's SwiGLU store on request, at any batch (split-K reduction included)
+    yu = tp.linear(x, w_il, epi_swiglu=True, path="umma").float()
+    assert ((yu - ref).abs().amax(1) / ref.abs().amax(1)).max().item() <= tol
+    if batch > 4:
+        return
     # fused with the add + rmsnorm producer (the decoder's MLP entry)
     delta = torch.randn(batch, d, generator=g, device="cuda").to(tdt)
     gamma = (torch.rand(d, generator=g, device="cuda") + 0.5).to(tdt)
@@ -771,7 +777,8 @@ def test_linear_epi_swiglu(tp, dtype, batch, d, f):
 
 
 def test_linear_epi_swiglu_rejects_unsupported(tp):
-    # the epilogue needs whole gate/up tile pairs and the int8-slice GEMV (batch <= 4): loud errors
+    # the epilogue needs whole gate/up tile pairs (K5: whole 32-row pairs) and a path that knows
+    # the pairing (the int8-slice GEMV or K5, not the fp16 GEMV): loud errors, nothing written
     from paper_2506_23025_b200 import _lib
 
     g = torch.Generator(device="cuda").manual_seed(0)
@@ -779,14 +786,12 @@ def test_linear_epi_swiglu_rejects_unsupported(tp):
     with pytest.raises(_lib.TriRunError):
         tp.linear(torch.randn(1, 512, generator=g, device="cuda").half(), w_odd, epi_swiglu=True)
     w = tp.TernaryWeight.from_float(torch.randn(64, 512, generator=g, device="cuda"))
-    with pytest.raises(_lib.TriRunError):
-        tp.linear(torch.randn(5, 512, generator=g, device="cuda").half(), w, epi_swiglu=True)
-    # batch >= 9 / a forced tensor-core path used to run K5 and write all rows into
-    # the rows/2-wide output; now every non-GEMV path is refused before any launch
-    for b, path in ((16, "auto"), (2, "umma")):
-        out = torch.full((b, 32), 7.0, dtype=torch.float16, device="cuda")
+    # a path that does not know the pairing must not write all rows into the rows/2-wide
+    # output: the fp16 GEMV is refused before any launch, and so is K5 on 48 rows
+    for b, ww, path in ((2, w, "gemv_f16"), (16, w_odd, "auto"), (2, w_odd, "umma")):
+        out = torch.full((b, ww.rows // 2), 7.0, dtype=torch.float16, device="cuda")
         with pytest.raises(_lib.TriRunError):
-            tp.linear(torch.randn(b, 512, generator=g, device="cuda").half(), w, out=out, epi_swiglu=True, path=path)
+            tp.linear(torch.randn(b, 512, generator=g, device="cuda").half(), ww, out=out, epi_swiglu=True, path=path)
         assert bool((out == 7.0).all())
     with pytest.raises(_lib.TriRunError):   # fp32 output does not combine with the epilogue
         tp.linear(torch.randn(1, 512, generator=g, device="cuda").half(), w, epi_swiglu=True, out_dtype=torch.float32)
