@@ -319,7 +319,7 @@ __device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
 // SPLIT: the product is split along K (a.ks > 1).  The unsplit instance carries no reduction code:
 // its mere presence cost the unsplit product ~6% (11008x4096 b=16: 10.0 vs 9.4 us), through the
 // register allocation of the decode and MMA loops
-template <typename T, int N, int FMT, bool SPLIT>
+template <typename T, int N, int FMT, bool SPLIT, bool EPI>
 __global__ void __launch_bounds__(umma::kThreads, 1)
     k_gemm_umma(const __grid_constant__ CUtensorMap tmx, const UmmaArgs a) {
   using namespace umma;
@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
     const int pair = mt * 4 + quad;
     if (!SPLIT || (a.dbg & 8)) {   // (dev probe 8: split-K slices store unreduced -- timing only)
       if (row < a.rows && !(kTrace && (a.dbg & 4))) {
-        if (a.epi) {
+        if constexpr (EPI) {
           store_swiglu<T, NH>(a, acc, n0, pair, lane);
         } else {
 #pragma unroll
@@ -720,7 +720,7 @@ __global__ void __launch_bounds__(umma::kThreads, 1)
 #pragma unroll
                 for (int e = 0; e < EC; ++e) v[e] += u[qq][e];
             }
-            if (a.epi) {
+            if constexpr (EPI) {
               store_swiglu<T, EC>(a, v, n0 + e0, pair, lane);
             } else {
 #pragma unroll
@@ -804,13 +804,18 @@ size_t umma_workspace_bytes(int batch, int rows, int cols) {
 
 template <typename T, int N, int FMT>
 static int launch_umma(const CUtensorMap& map, const UmmaArgs& a, int grid, int pdl, cudaStream_t st) {
-  auto kern = a.ks > 1 ? k_gemm_umma<T, N, FMT, true> : k_gemm_umma<T, N, FMT, false>;
-  static int configured_dev[2] = {-1, -1};
+  // (SwiGLU store: its own instances, TQ2 only -- a runtime branch in the shared store code cost
+  // b=128 3.8% and b=64 2% through the register allocation, as the split-K sum once did)
+  auto kern = a.ks > 1 ? k_gemm_umma<T, N, FMT, true, false> : k_gemm_umma<T, N, FMT, false, false>;
+  if constexpr (FMT == kFmtTq2)
+    if (a.epi) kern = a.ks > 1 ? k_gemm_umma<T, N, FMT, true, true> : k_gemm_umma<T, N, FMT, false, true>;
+  const int inst = (a.ks > 1) + 2 * (a.epi != 0);
+  static int configured_dev[4] = {-1, -1, -1, -1};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (configured_dev[a.ks > 1] != dev) {
+  if (configured_dev[inst] != dev) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UmmaCfg<T, N, FMT>::kSmem);
-    configured_dev[a.ks > 1] = dev;
+    configured_dev[inst] = dev;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
@@ -894,7 +899,7 @@ int gemm_umma(int fmt, int act, const void* w, const void* x, void* y, int64_t l
   a.map3d = map3d;
   a.out_f32 = out_f32;
   a.epi = epi;
-  if (epi && (rows % 32 != 0 || out_f32)) {
+  if (epi && (rows % 32 != 0 || out_f32 || fmt != kFmtTq2)) {
     set_error("tr_linear(umma, swiglu epilogue): rows (%d) must be whole 32-row gate/up pairs, fp16/bf16 out", rows);
     return -1;
   }
